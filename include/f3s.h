@@ -1,0 +1,172 @@
+/*
+ * f3s.h — C ABI of the B200-native fused 3S sparse-attention library (libf3s.so).
+ *
+ *   O = softmax_row( scale * (Q K^T) ⊙ A ) V      per head,
+ *
+ * Eq.1 of Fused3S decomposed as SDDMM -> row softmax -> SpMM
+ * (PAPER.md:116-120), computed in one fused kernel (Alg.1).
+ *
+ * Conventions (readings of the paper, listed in DESIGN.md §Readings):
+ *  - A is binary: only its support matters; duplicate (row, col) entries are merged and
+ *    rows may be unsorted.  The softmax runs over the support of row i
+ *    only: non-edges get weight exactly 0.  No self-loops are added.
+ *  - Rows of A with no entries produce O rows of exact zeros (Alg.1 line 24, divides
+ *    by l_o = 0; reading c4).
+ *  - Precision follows Tab.mixedp: Q, K, V in fp16 (or bf16); scores,
+ *    softmax statistics and O accumulation in fp32; normalised scores cast to the input
+ *    dtype before the second contraction; O written in fp32.
+ *  - Every call returns f3s_status; nothing throws across this boundary.  Detail for the
+ *    last failure on the calling thread is in f3s_last_error().
+ *
+ * Memory: "device" pointers are CUDA device pointers on the current device; "host"
+ * pointers are ordinary host memory (pinned host memory makes the _host call faster).
+ * The library never retains caller pointers past the call, except that kernels launched by
+ * f3s_attention read Q/K/V and write O asynchronously on `stream`.
+ */
+#ifndef F3S_H_
+#define F3S_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* identical to the CUDA runtime's own declaration (driver_types.h) */
+typedef struct CUstream_st* cudaStream_t;
+
+typedef struct f3s_plan_impl* f3s_plan_t; /* opaque; owns device memory until f3s_plan_destroy */
+
+typedef enum {
+    F3S_OK = 0,
+    F3S_ERR_INVALID_VALUE = 1, /* bad pointer / negative size / heads < 1 / non-finite scale   */
+    F3S_ERR_INVALID_CSR = 2,   /* row_ptr not monotone (or row_ptr[0] != 0 for f3s_plan), or a
+                                  column index outside [0, n_cols)                             */
+    F3S_ERR_UNSUPPORTED = 3,   /* d not in {64, 128}, sizes >= 2^31, misaligned tensors        */
+    F3S_ERR_OUT_OF_MEMORY = 4,
+    F3S_ERR_CUDA = 5,          /* a CUDA runtime/driver call failed; see f3s_last_error()     */
+    F3S_ERR_INTERNAL = 6
+} f3s_status;
+
+typedef enum { F3S_FP16 = 0, F3S_BF16 = 1 } f3s_dtype;
+
+typedef struct {
+    int32_t n_rows;       /* rows of A (local rows for f3s_plan_rows)                          */
+    int32_t n_cols;       /* columns of A                                                      */
+    int32_t num_rw;       /* R = ceil(n_rows / 16) row windows (r = 16)          */
+    int32_t max_width;    /* largest compacted width of a row window                           */
+    int64_t nnz;          /* deduplicated nonzeros of A = sum of mask popcounts                */
+    int64_t total_cols;   /* W = sum of compacted widths                        */
+    int64_t total_tcb8;   /* sum over RWs of ceil(w/8): 16x8 TCB count  */
+    int64_t device_bytes; /* device memory owned by the plan                                   */
+    float build_ms;       /* device time of the plan build                                     */
+    float reserved;
+} f3s_plan_info;
+
+/*
+ * Build the row-window plan of an n x n binary A given in CSR on the DEVICE (§3.1,
+ * PAPER.md:206-216, plus the RW reordering of PAPER.md:402-405):
+ *   for RW k (rows 16k .. 16k+15):  cols_k = ascending unique column ids of those rows
+ *   (compaction; sptd analogue), masks_k[p] bit i set iff (16k+i, cols_k[p])
+ *   is in A (bitmap analogue), rw_ptr = prefix sum of widths (tro analogue),
+ *   rw_order = RW indices sorted by ceil(w/8) descending, ties by index ascending.
+ *
+ *  row_ptr  device int32[n+1], row_ptr[0] == 0, non-decreasing.     (read-only, caller-owned)
+ *  col_idx  device int32[row_ptr[n]], each in [0, n).                (read-only, caller-owned)
+ *  n        number of nodes, 0 <= n < 2^31.  n == 0 gives a valid empty plan.
+ *  stream   work is ordered on this stream; the call synchronises the stream (twice) to size
+ *           the plan's buffers and to report CSR errors, so both inputs may be freed on return.
+ *  out      receives the plan handle (set to NULL on failure).
+ * Errors: INVALID_VALUE, INVALID_CSR (detected on the device), OUT_OF_MEMORY, CUDA.
+ */
+f3s_status f3s_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n, cudaStream_t stream,
+                    f3s_plan_t* out);
+
+/*
+ * Plan for a row block of a rectangular A (n_rows x n_cols): the multi-GPU shard form.
+ * Row r of the block has entries col_idx[row_ptr[r] .. row_ptr[r+1]) with row_ptr[0] >= 0
+ * allowed to be non-zero, so a caller can pass `global_row_ptr + row_begin` and the global
+ * col_idx without copying.  Column ids are global (in [0, n_cols)).  If row_begin is a
+ * multiple of 16, every row window equals the corresponding window of the global plan, so
+ * per-row results are bitwise identical to the single-GPU call.
+ * Other semantics as f3s_plan.
+ */
+f3s_status f3s_plan_rows(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_rows, int32_t n_cols,
+                         cudaStream_t stream, f3s_plan_t* out);
+
+/* Free the plan's device memory.  No call using the plan may still be in flight.  NULL is OK. */
+f3s_status f3s_plan_destroy(f3s_plan_t plan);
+
+/* Sizes and statistics of a plan (host struct written by the call). */
+f3s_status f3s_plan_get_info(f3s_plan_t plan, f3s_plan_info* info);
+
+/*
+ * Copy the canonical plan arrays to HOST memory (synchronous): rw_ptr[R+1], cols[W],
+ * masks[W] (uint16, bit i = row 16k+i), rw_order[R].  Any pointer may be NULL to skip it.
+ * These arrays are independent of the kernel's tile size and are what the tests compare
+ * bit-exactly with the oracle's block builder.
+ */
+f3s_status f3s_plan_export(f3s_plan_t plan, int32_t* rw_ptr, int32_t* cols, uint16_t* masks, int32_t* rw_order);
+
+/*
+ * The fused 3S pass (Alg.1) on sm_100a: per row window and head, gathers
+ * of K and V rows by the compacted column list (Alg.1 l.7-8) into shared memory with TMA,
+ * S^T = K_c Q_w^T on tcgen05 tensor cores into TMEM (l.13), bitmap mask (l.14), online
+ * softmax in fp32 (l.16-18), P cast to the input dtype (l.19), O^T += V_c^T P^T on tcgen05
+ * (l.21-22), O = O / l written once (l.24).  Row windows are scheduled longest-first
+ * from a persistent work queue.
+ *
+ *  Q      device [n_rows, heads, d] dtype, contiguous, 16-byte aligned
+ *  K, V   device [n_cols, heads, d] dtype, contiguous, 16-byte aligned
+ *  O      device [n_rows, heads, d] float32, contiguous; must not alias Q/K/V
+ *  scale  multiplies Q K^T before the softmax (scale = 1 reproduces Eq.1; 1/sqrt(d) for GT)
+ *  heads  >= 1;  d in {64, 128};  dtype F3S_FP16 or F3S_BF16
+ * Asynchronous on `stream`; only launch-time errors are reported (device faults surface at
+ * the caller's next synchronisation, CUDA convention).  Bitwise deterministic.
+ */
+f3s_status f3s_attention(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
+                         int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
+
+/* Kernel variants for ablations (bench.py --variant); f3s_attention uses F3S_VARIANT_DEFAULT. */
+typedef enum {
+    F3S_VARIANT_DEFAULT = 0, /* tcgen05 + TMA gather kernel, LPT-ordered persistent queue       */
+    F3S_VARIANT_NO_REORDER = 1, /* same kernel, row windows in natural order */
+    F3S_VARIANT_SIMT = 2     /* CUDA-core reference kernel of the same dataflow (no tensor core) */
+} f3s_variant;
+
+f3s_status f3s_attention_ex(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
+                            int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, cudaStream_t stream);
+
+/*
+ * End-to-end form with HOST buffers: copies Q, K, V host->device, runs f3s_attention, copies
+ * O device->host and synchronises `stream`.  Device staging buffers are owned by the plan and
+ * reused across calls.  Q: host [n_rows,heads,d], K/V: host [n_cols,heads,d], O: host float32.
+ */
+f3s_status f3s_attention_host(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O,
+                              float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
+
+/*
+ * Host partitioner for multi-GPU runs: split rows [0, n) into `parts` contiguous ranges whose
+ * boundaries are multiples of 16 (row-window aligned, except bounds[parts] = n), balancing
+ * nnz: bounds[p] is the window boundary whose prefix nnz is closest to p * nnz / parts.
+ *  row_ptr_host  host int32[n+1] (row_ptr[0] may be non-zero)
+ *  bounds        host int32[parts+1] written: 0 = bounds[0] <= ... <= bounds[parts] = n
+ */
+f3s_status f3s_partition_rows(const int32_t* row_ptr_host, int32_t n, int32_t parts, int32_t* bounds);
+
+/* Same, but only cutting at the given candidate boundaries (e.g. graph starts in batched
+ * mode): cuts[n_cuts] ascending in [0, n]. */
+f3s_status f3s_partition_at(const int32_t* row_ptr_host, int32_t n, const int32_t* cuts, int32_t n_cuts,
+                            int32_t parts, int32_t* bounds);
+
+const char* f3s_status_string(f3s_status s);
+const char* f3s_last_error(void); /* thread-local detail of the last failure, "" if none */
+
+/* Number of kernels the library launched since load (bench.py's gpu_launches evidence). */
+int64_t f3s_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* F3S_H_ */

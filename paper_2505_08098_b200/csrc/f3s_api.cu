@@ -1,0 +1,256 @@
+// f3s_api.cu — the C ABI of include/f3s.h: argument validation, status codes, plan
+// ownership, host-buffer end-to-end call, row partitioner.  No C++ exception crosses it.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "internal.h"
+
+namespace f3s {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+f3s_status cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    (void)cudaGetLastError();  // clear a sticky-free error so later calls are not poisoned
+    return e == cudaErrorMemoryAllocation ? F3S_ERR_OUT_OF_MEMORY : F3S_ERR_CUDA;
+}
+
+static f3s_status check_attention_args(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O,
+                                       float scale, int32_t heads, int32_t d, f3s_dtype dtype, bool device) {
+    if (!plan) { set_error("plan is NULL"); return F3S_ERR_INVALID_VALUE; }
+    if (heads < 1) { set_error("heads must be >= 1"); return F3S_ERR_INVALID_VALUE; }
+    if (!std::isfinite(scale)) { set_error("scale must be finite"); return F3S_ERR_INVALID_VALUE; }
+    if (dtype != F3S_FP16 && dtype != F3S_BF16) { set_error("dtype must be F3S_FP16 or F3S_BF16"); return F3S_ERR_INVALID_VALUE; }
+    const Plan& p = *reinterpret_cast<const Plan*>(plan);
+    if (p.n_rows > 0 && (!Q || !O)) { set_error("Q/O is NULL"); return F3S_ERR_INVALID_VALUE; }
+    if (p.n_cols > 0 && (!K || !V)) { set_error("K/V is NULL"); return F3S_ERR_INVALID_VALUE; }
+    if (d != 64 && d != 128) { set_error("d must be 64 or 128"); return F3S_ERR_UNSUPPORTED; }
+    if ((int64_t)heads * d > (int64_t)1 << 24) { set_error("heads*d too large"); return F3S_ERR_UNSUPPORTED; }
+    if ((int64_t)p.num_rw * heads > 0x7FFFFFFFLL) { set_error("num_rw*heads >= 2^31"); return F3S_ERR_UNSUPPORTED; }
+    if (device) {
+        auto mis = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) != 0; };
+        if (mis(Q) || mis(K) || mis(V) || mis(O)) { set_error("Q/K/V/O must be 16-byte aligned"); return F3S_ERR_UNSUPPORTED; }
+        if (O && (O == Q || O == K || O == V)) { set_error("O aliases an input"); return F3S_ERR_INVALID_VALUE; }
+    }
+    return F3S_OK;
+}
+
+static f3s_status run_attention(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
+                                int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, cudaStream_t stream) {
+    f3s_status st = check_attention_args(plan, Q, K, V, O, scale, heads, d, dtype, true);
+    if (st != F3S_OK) return st;
+    AttnArgs a{reinterpret_cast<const Plan*>(plan), Q, K, V, O, scale, heads, d, dtype,
+               variant != F3S_VARIANT_NO_REORDER, stream};
+    if (a.plan->n_rows == 0) return F3S_OK;
+    switch (variant) {
+        case F3S_VARIANT_DEFAULT:
+        case F3S_VARIANT_NO_REORDER: return launch_attention_sm100(a);
+        case F3S_VARIANT_SIMT: return launch_attention_simt(a);
+        default: set_error("unknown variant"); return F3S_ERR_INVALID_VALUE;
+    }
+}
+
+}  // namespace f3s
+
+using namespace f3s;
+
+extern "C" {
+
+f3s_status f3s_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n, cudaStream_t stream, f3s_plan_t* out) {
+    if (!out) { set_error("out is NULL"); return F3S_ERR_INVALID_VALUE; }
+    *out = nullptr;
+    try {
+        Plan* p = nullptr;
+        f3s_status st = build_plan(row_ptr, col_idx, n, n, true, stream, &p);
+        if (st == F3S_OK) *out = reinterpret_cast<f3s_plan_t>(p);
+        return st;
+    } catch (const std::bad_alloc&) {
+        return F3S_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_plan_rows(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_rows, int32_t n_cols,
+                         cudaStream_t stream, f3s_plan_t* out) {
+    if (!out) { set_error("out is NULL"); return F3S_ERR_INVALID_VALUE; }
+    *out = nullptr;
+    try {
+        Plan* p = nullptr;
+        f3s_status st = build_plan(row_ptr, col_idx, n_rows, n_cols, false, stream, &p);
+        if (st == F3S_OK) *out = reinterpret_cast<f3s_plan_t>(p);
+        return st;
+    } catch (const std::bad_alloc&) {
+        return F3S_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_plan_destroy(f3s_plan_t plan) {
+    if (!plan) return F3S_OK;
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    cudaFree(p->rw_ptr);
+    cudaFree(p->cols);
+    cudaFree(p->masks);
+    cudaFree(p->rw_order);
+    cudaFree(p->rw_natural);
+    cudaFree(p->counters);
+    cudaFree(p->staging);
+    delete p;
+    return F3S_OK;
+}
+
+f3s_status f3s_plan_get_info(f3s_plan_t plan, f3s_plan_info* info) {
+    if (!plan || !info) { set_error("plan/info is NULL"); return F3S_ERR_INVALID_VALUE; }
+    const Plan& p = *reinterpret_cast<const Plan*>(plan);
+    std::memset(info, 0, sizeof(*info));
+    info->n_rows = p.n_rows;
+    info->n_cols = p.n_cols;
+    info->num_rw = p.num_rw;
+    info->max_width = p.max_width;
+    info->nnz = p.nnz;
+    info->total_cols = p.total_cols;
+    info->total_tcb8 = p.total_tcb8;
+    info->device_bytes = p.device_bytes;
+    info->build_ms = p.build_ms;
+    return F3S_OK;
+}
+
+f3s_status f3s_plan_export(f3s_plan_t plan, int32_t* rw_ptr, int32_t* cols, uint16_t* masks, int32_t* rw_order) {
+    if (!plan) { set_error("plan is NULL"); return F3S_ERR_INVALID_VALUE; }
+    const Plan& p = *reinterpret_cast<const Plan*>(plan);
+    if (rw_ptr) F3S_CUDA_TRY(cudaMemcpy(rw_ptr, p.rw_ptr, sizeof(int32_t) * (p.num_rw + 1), cudaMemcpyDeviceToHost));
+    if (cols && p.total_cols) F3S_CUDA_TRY(cudaMemcpy(cols, p.cols, sizeof(int32_t) * p.total_cols, cudaMemcpyDeviceToHost));
+    if (masks && p.total_cols) F3S_CUDA_TRY(cudaMemcpy(masks, p.masks, sizeof(uint16_t) * p.total_cols, cudaMemcpyDeviceToHost));
+    if (rw_order && p.num_rw) F3S_CUDA_TRY(cudaMemcpy(rw_order, p.rw_order, sizeof(int32_t) * p.num_rw, cudaMemcpyDeviceToHost));
+    return F3S_OK;
+}
+
+f3s_status f3s_attention(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
+                         int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
+    try {
+        return run_attention(plan, Q, K, V, O, scale, heads, d, dtype, F3S_VARIANT_DEFAULT, stream);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_ex(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
+                            int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, cudaStream_t stream) {
+    try {
+        return run_attention(plan, Q, K, V, O, scale, heads, d, dtype, variant, stream);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_host(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
+                              int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
+    f3s_status st = check_attention_args(plan, Q, K, V, O, scale, heads, d, dtype, false);
+    if (st != F3S_OK) return st;
+    Plan& p = *reinterpret_cast<Plan*>(plan);
+    const size_t qn = (size_t)p.n_rows * heads * d, kn = (size_t)p.n_cols * heads * d;
+    auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t need = up(qn * 2) + 2 * up(kn * 2) + up(qn * 4);
+    std::lock_guard<std::mutex> lock(p.staging_mu);
+    if (p.staging_bytes < need) {
+        cudaFree(p.staging);
+        p.staging = nullptr;
+        p.staging_bytes = 0;
+        F3S_CUDA_TRY(cudaMalloc(&p.staging, need));
+        p.staging_bytes = need;
+    }
+    char* base = static_cast<char*>(p.staging);
+    void* dQ = base;
+    void* dK = base + up(qn * 2);
+    void* dV = base + up(qn * 2) + up(kn * 2);
+    float* dO = reinterpret_cast<float*>(base + up(qn * 2) + 2 * up(kn * 2));
+    if (qn) F3S_CUDA_TRY(cudaMemcpyAsync(dQ, Q, qn * 2, cudaMemcpyHostToDevice, stream));
+    if (kn) {
+        F3S_CUDA_TRY(cudaMemcpyAsync(dK, K, kn * 2, cudaMemcpyHostToDevice, stream));
+        F3S_CUDA_TRY(cudaMemcpyAsync(dV, V, kn * 2, cudaMemcpyHostToDevice, stream));
+    }
+    st = run_attention(plan, dQ, dK, dV, dO, scale, heads, d, dtype, F3S_VARIANT_DEFAULT, stream);
+    if (st != F3S_OK) return st;
+    if (qn) F3S_CUDA_TRY(cudaMemcpyAsync(O, dO, qn * 4, cudaMemcpyDeviceToHost, stream));
+    F3S_CUDA_TRY(cudaStreamSynchronize(stream));
+    return F3S_OK;
+}
+
+// ---- partitioner (host) ---------------------------------------------------------------------
+static f3s_status partition_impl(const int32_t* rp, int32_t n, const int32_t* cuts, int32_t n_cuts, int32_t parts,
+                                 int32_t* bounds) {
+    // candidate boundary c (row index) has prefix nnz rp[c] - rp[0]; bounds[p] is the
+    // candidate whose prefix is closest to p*total/parts, never moving backwards.
+    const int64_t total = (int64_t)rp[n] - rp[0];
+    bounds[0] = 0;
+    int32_t ci = 0;  // index into candidates
+    auto cand = [&](int32_t i) -> int32_t { return cuts ? cuts[i] : std::min(16 * i, n); };
+    const int32_t n_cand = cuts ? n_cuts : (n + 15) / 16 + 1;
+    for (int32_t q = 1; q < parts; ++q) {
+        const double target = (double)total * q / parts;
+        while (ci + 1 < n_cand && (double)(rp[cand(ci + 1)] - rp[0]) < target) ++ci;
+        int32_t best = ci;
+        if (ci + 1 < n_cand) {
+            const double lo = target - (double)(rp[cand(ci)] - rp[0]);
+            const double hi = (double)(rp[cand(ci + 1)] - rp[0]) - target;
+            if (hi < lo) best = ci + 1;
+        }
+        bounds[q] = std::max(bounds[q - 1], cand(best));
+    }
+    bounds[parts] = n;
+    for (int32_t q = 1; q < parts; ++q) bounds[q] = std::min(bounds[q], n);
+    return F3S_OK;
+}
+
+f3s_status f3s_partition_rows(const int32_t* row_ptr_host, int32_t n, int32_t parts, int32_t* bounds) {
+    if (!row_ptr_host || !bounds || n < 0 || parts < 1) { set_error("bad partition arguments"); return F3S_ERR_INVALID_VALUE; }
+    for (int32_t i = 0; i < n; ++i)
+        if (row_ptr_host[i + 1] < row_ptr_host[i]) { set_error("row_ptr is not non-decreasing"); return F3S_ERR_INVALID_CSR; }
+    return partition_impl(row_ptr_host, n, nullptr, 0, parts, bounds);
+}
+
+f3s_status f3s_partition_at(const int32_t* row_ptr_host, int32_t n, const int32_t* cuts, int32_t n_cuts,
+                            int32_t parts, int32_t* bounds) {
+    if (!row_ptr_host || !bounds || !cuts || n < 0 || parts < 1 || n_cuts < 1) {
+        set_error("bad partition arguments");
+        return F3S_ERR_INVALID_VALUE;
+    }
+    for (int32_t i = 0; i < n; ++i)
+        if (row_ptr_host[i + 1] < row_ptr_host[i]) { set_error("row_ptr is not non-decreasing"); return F3S_ERR_INVALID_CSR; }
+    for (int32_t i = 0; i < n_cuts; ++i)
+        if (cuts[i] < 0 || cuts[i] > n || (i && cuts[i] < cuts[i - 1])) { set_error("cuts must be ascending in [0, n]"); return F3S_ERR_INVALID_VALUE; }
+    return partition_impl(row_ptr_host, n, cuts, n_cuts, parts, bounds);
+}
+
+const char* f3s_status_string(f3s_status s) {
+    switch (s) {
+        case F3S_OK: return "F3S_OK";
+        case F3S_ERR_INVALID_VALUE: return "F3S_ERR_INVALID_VALUE";
+        case F3S_ERR_INVALID_CSR: return "F3S_ERR_INVALID_CSR";
+        case F3S_ERR_UNSUPPORTED: return "F3S_ERR_UNSUPPORTED";
+        case F3S_ERR_OUT_OF_MEMORY: return "F3S_ERR_OUT_OF_MEMORY";
+        case F3S_ERR_CUDA: return "F3S_ERR_CUDA";
+        case F3S_ERR_INTERNAL: return "F3S_ERR_INTERNAL";
+    }
+    return "F3S_ERR_UNKNOWN";
+}
+
+const char* f3s_last_error(void) { return g_last_error.c_str(); }
+
+int64_t f3s_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

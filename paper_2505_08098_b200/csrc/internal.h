@@ -1,0 +1,65 @@
+// internal.h — shared declarations of libf3s (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "../../include/f3s.h"
+
+namespace f3s {
+
+constexpr int kRowsPerWindow = 16;  // r = 16 (reading c10)
+
+struct Plan {
+    int32_t n_rows = 0, n_cols = 0, num_rw = 0, max_width = 0;
+    int64_t nnz = 0, total_cols = 0, total_tcb8 = 0, device_bytes = 0;
+    float build_ms = 0.f;
+    int device = 0;
+    // canonical arrays (device)
+    int32_t* rw_ptr = nullptr;    // [R+1]
+    int32_t* cols = nullptr;      // [W]
+    uint16_t* masks = nullptr;    // [W]
+    int32_t* rw_order = nullptr;  // [R]  LPT order
+    int32_t* rw_natural = nullptr;  // [R] identity order (ablation)
+    int32_t* counters = nullptr;  // work-queue counters, kNumCounterSlots
+    // e2e staging buffers for f3s_attention_host
+    std::mutex staging_mu;
+    void* staging = nullptr;
+    size_t staging_bytes = 0;
+};
+
+constexpr int kNumCounterSlots = 64;
+
+// error reporting (thread-local detail)
+void set_error(const std::string& msg);
+f3s_status cuda_fail(cudaError_t e, const char* what);
+void count_launch(int64_t n = 1);
+
+f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_rows, int32_t n_cols,
+                      bool require_zero_base, cudaStream_t stream, Plan** out);
+
+struct AttnArgs {
+    const Plan* plan;
+    const void* Q;
+    const void* K;
+    const void* V;
+    float* O;
+    float scale;
+    int heads, d;
+    f3s_dtype dtype;
+    bool lpt;
+    cudaStream_t stream;
+};
+
+f3s_status launch_attention_sm100(const AttnArgs& a);
+f3s_status launch_attention_simt(const AttnArgs& a);
+
+}  // namespace f3s
+
+#define F3S_CUDA_TRY(expr)                                        \
+    do {                                                          \
+        cudaError_t e_ = (expr);                                  \
+        if (e_ != cudaSuccess) return ::f3s::cuda_fail(e_, #expr); \
+    } while (0)

@@ -1,0 +1,191 @@
+"""Thin Python binding of the C ABI in include/f3s.h (argument marshalling only).
+
+Every step of the hot path runs in libf3s.so's CUDA kernels; torch supplies device memory
+and streams.  There is no fallback: if libf3s.so is missing, importing this module raises.
+Names follow the C ABI: plan, plan_rows, attention, attention_host, partition_rows.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libf3s.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+OK, INVALID_VALUE, INVALID_CSR, UNSUPPORTED, OUT_OF_MEMORY, CUDA, INTERNAL = range(7)
+FP16, BF16 = 0, 1
+VARIANT_DEFAULT, VARIANT_NO_REORDER, VARIANT_SIMT = 0, 1, 2
+VARIANTS = {"default": VARIANT_DEFAULT, "no_reorder": VARIANT_NO_REORDER, "simt": VARIANT_SIMT}
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int32), ("n_cols", ctypes.c_int32), ("num_rw", ctypes.c_int32),
+                ("max_width", ctypes.c_int32), ("nnz", ctypes.c_int64), ("total_cols", ctypes.c_int64),
+                ("total_tcb8", ctypes.c_int64), ("device_bytes", ctypes.c_int64), ("build_ms", ctypes.c_float),
+                ("reserved", ctypes.c_float)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+_i32, _i64, _vp, _f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_float
+_lib.f3s_plan.argtypes = [_vp, _vp, _i32, _vp, ctypes.POINTER(_vp)]
+_lib.f3s_plan_rows.argtypes = [_vp, _vp, _i32, _i32, _vp, ctypes.POINTER(_vp)]
+_lib.f3s_plan_destroy.argtypes = [_vp]
+_lib.f3s_plan_get_info.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
+_lib.f3s_plan_export.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.f3s_attention.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
+_lib.f3s_partition_rows.argtypes = [_vp, _i32, _i32, _vp]
+_lib.f3s_partition_at.argtypes = [_vp, _i32, _vp, _i32, _i32, _vp]
+_lib.f3s_status_string.argtypes = [_i32]
+_lib.f3s_status_string.restype = ctypes.c_char_p
+_lib.f3s_last_error.restype = ctypes.c_char_p
+_lib.f3s_launch_count.restype = _i64
+for _name in ("f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export",
+              "f3s_attention", "f3s_attention_ex", "f3s_attention_host", "f3s_partition_rows", "f3s_partition_at"):
+    getattr(_lib, _name).restype = _i32
+
+EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export",
+            "f3s_attention", "f3s_attention_ex", "f3s_attention_host", "f3s_partition_rows", "f3s_partition_at",
+            "f3s_status_string", "f3s_last_error", "f3s_launch_count"]
+
+
+class F3SError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        detail = _lib.f3s_last_error().decode()
+        super().__init__(f"{where}: {_lib.f3s_status_string(status).decode()}: {detail}")
+
+
+def _check(status: int, where: str) -> None:
+    if status != OK:
+        raise F3SError(status, where)
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype == torch.float16:
+        return FP16
+    if t.dtype == torch.bfloat16:
+        return BF16
+    raise TypeError(f"Q/K/V must be float16 or bfloat16, got {t.dtype}")
+
+
+class Plan:
+    """Owning handle of a device plan (f3s_plan_t)."""
+
+    def __init__(self, handle: int):
+        self._h = ctypes.c_void_p(handle)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> dict:
+        inf = PlanInfo()
+        _check(_lib.f3s_plan_get_info(self._h, ctypes.byref(inf)), "f3s_plan_get_info")
+        return inf.as_dict()
+
+    def export(self):
+        """Host copies of the canonical arrays: rw_ptr, cols, masks, rw_order (numpy)."""
+        inf = self.info()
+        R, W = inf["num_rw"], inf["total_cols"]
+        rw_ptr = np.empty(R + 1, np.int32)
+        cols = np.empty(max(W, 1), np.int32)
+        masks = np.empty(max(W, 1), np.uint16)
+        order = np.empty(max(R, 1), np.int32)
+        _check(_lib.f3s_plan_export(self._h, rw_ptr.ctypes.data, cols.ctypes.data, masks.ctypes.data,
+                                    order.ctypes.data), "f3s_plan_export")
+        return rw_ptr, cols[:W], masks[:W], order[:R]
+
+    def destroy(self) -> None:
+        if self._h:
+            _lib.f3s_plan_destroy(self._h)
+            self._h = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def plan(row_ptr, col_idx, n: int, stream=None) -> Plan:
+    """f3s_plan on device CSR tensors (int32, cuda)."""
+    h = ctypes.c_void_p()
+    _check(_lib.f3s_plan(row_ptr.data_ptr(), col_idx.data_ptr() if col_idx.numel() else None, n, _stream(stream),
+                         ctypes.byref(h)), "f3s_plan")
+    return Plan(h.value)
+
+
+def plan_rows(row_ptr, col_idx, n_rows: int, n_cols: int, stream=None) -> Plan:
+    """f3s_plan_rows: row_ptr may be a view into a global row_ptr (non-zero base)."""
+    h = ctypes.c_void_p()
+    _check(_lib.f3s_plan_rows(row_ptr.data_ptr(), col_idx.data_ptr() if col_idx.numel() else None, n_rows, n_cols,
+                              _stream(stream), ctypes.byref(h)), "f3s_plan_rows")
+    return Plan(h.value)
+
+
+def attention(p: Plan, Q, K, V, O=None, *, scale: float = 1.0, variant: str | int = "default", stream=None):
+    """f3s_attention(_ex) on device tensors Q [n_rows,H,d], K/V [n_cols,H,d] (fp16/bf16); O float32."""
+    import torch
+    H, d = Q.shape[1], Q.shape[2]
+    if O is None:
+        O = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    st = _lib.f3s_attention_ex(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), O.data_ptr(), float(scale), H, d,
+                               _dtype_code(Q), v, _stream(stream))
+    _check(st, "f3s_attention")
+    return O
+
+
+def attention_raw(p: Plan, q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, scale: float, heads: int, d: int,
+                  dtype: int, stream: int, variant: int = VARIANT_DEFAULT) -> None:
+    """Pointer-level call (no torch); used by bench loops and CUDA-graph capture."""
+    _check(_lib.f3s_attention_ex(p.handle, q_ptr, k_ptr, v_ptr, o_ptr, float(scale), heads, d, dtype, variant, stream),
+           "f3s_attention")
+
+
+def attention_host(p: Plan, Q, K, V, O, *, scale: float, heads: int, d: int, dtype: int, stream=None) -> None:
+    """f3s_attention_host on HOST buffers (numpy uint16 bit patterns or pinned torch tensors); O float32 host."""
+    def ptr(x):
+        return x.ctypes.data if isinstance(x, np.ndarray) else x.data_ptr()
+    _check(_lib.f3s_attention_host(p.handle, ptr(Q), ptr(K), ptr(V), ptr(O), float(scale), heads, d, dtype,
+                                   _stream(stream)), "f3s_attention_host")
+
+
+def partition_rows(row_ptr: np.ndarray, parts: int) -> np.ndarray:
+    row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+    bounds = np.empty(parts + 1, np.int32)
+    _check(_lib.f3s_partition_rows(row_ptr.ctypes.data, len(row_ptr) - 1, parts, bounds.ctypes.data),
+           "f3s_partition_rows")
+    return bounds
+
+
+def partition_at(row_ptr: np.ndarray, cuts: np.ndarray, parts: int) -> np.ndarray:
+    row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+    cuts = np.ascontiguousarray(cuts, np.int32)
+    bounds = np.empty(parts + 1, np.int32)
+    _check(_lib.f3s_partition_at(row_ptr.ctypes.data, len(row_ptr) - 1, cuts.ctypes.data, len(cuts), parts,
+                                 bounds.ctypes.data), "f3s_partition_at")
+    return bounds
+
+
+def launch_count() -> int:
+    return int(_lib.f3s_launch_count())
