@@ -138,6 +138,16 @@ f3s_status f3s_attention_ex(f3s_plan_t plan, const void* Q, const void* K, const
                             int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, cudaStream_t stream);
 
 /*
+ * Diagnostics (F3S_TRACE): the default kernel with a device buffer trace[grid][trace_chunks][8]
+ * of uint64 globaltimer stamps per CTA and chunk: 0 ids/masks requested, 1 gathers issued,
+ * 2 MMA1 issued, 3 scores seen, 4 P written, 5 MMA2 issued, 6 O seen, 7 rows stored (last
+ * chunk of an item).  grid > 0 overrides the persistent grid size (0 = default).
+ */
+f3s_status f3s_attention_trace(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
+                               int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, uint64_t* trace,
+                               int32_t trace_chunks, int32_t grid, cudaStream_t stream);
+
+/*
  * End-to-end form with HOST buffers: copies Q, K, V host->device, runs f3s_attention, copies
  * O device->host and synchronises `stream`.  Device staging buffers are owned by the plan and
  * reused across calls.  Q: host [n_rows,heads,d], K/V: host [n_cols,heads,d], O: host float32.

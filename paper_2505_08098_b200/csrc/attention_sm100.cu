@@ -12,11 +12,15 @@
 //       MMA2  O^T[d x 16]  = V_c^T[d x C] . P^T[C x 16] (SpMM,  l.22; M = d,   N = 16)
 //     S^T lane p is compacted column p, so the 16-bit plan mask of that column is the
 //     bitmap row (l.14) of exactly one thread;
-//   * warps 2-5 (128 threads): tcgen05.ld S^T, mask to -inf, chunk row max by warp
+//   * warp 2 (index): pops items from the queue in batches and bulk-copies each chunk's
+//     column ids and 16-bit row masks (the BSB bitmap) into a chunk slot;
+//   * softmax warpgroup (warps 3-6): tcgen05.ld S^T, mask to -inf, chunk row max by warp
 //     shuffles + a 4-warp combine, online softmax in fp32 with exp2 (l.16-18), P cast to the
-//     input dtype into shared memory (l.19), then fold the chunk's O^T into fp32 registers
-//     with the running rescale (l.21), and at the last chunk write O = O / l (l.24; rows with
-//     l = 0 -> 0, reading c4).
+//     input dtype into shared memory (l.19), per-row rescale factors to the correction group;
+//   * correction warpgroup (warps 7-10): folds each chunk's O^T from TMEM into fp32 registers
+//     with the running rescale (l.21-22) and at the item's last chunk writes O = O / l (l.24;
+//     rows with l = 0 -> 0, reading c4).  Keeping the O stores out of the softmax group keeps
+//     its proxy fence (MEMBAR) cheap.
 //
 // Everything between the gathers and the O store stays on chip.  No atomics on
 // the data path: results are bitwise deterministic.
@@ -25,6 +29,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <mutex>
 #include <type_traits>
@@ -41,52 +46,81 @@ template <int D>
 struct Cfg {
     static constexpr int P = D / 64;                 // 128-byte panels per gathered row of one head
     static constexpr int kGroupBytes = 1024 * P;     // 8 gathered rows (one swizzle atom per panel)
-    static constexpr int kMaxRows = 128;             // chunk = up to 128 compacted columns (MMA1 M)
-    static constexpr int kRingBytes = D == 128 ? 160 * 1024 : 80 * 1024;
-    static constexpr int kNS = 16;                   // chunk slots (descriptor + barriers)
-    static constexpr int kNQ = 4;                    // Q tile slots
+    static constexpr int kMaxRows = 128;             // compacted columns per chunk at most (MMA1 M = 128)
+    // K tiles live until MMA1 completes, V tiles until MMA2 completes: two FIFO rings
+    static constexpr int kRingK = D == 128 ? 64 * 1024 : 64 * 1024;
+    static constexpr int kRingV = D == 128 ? 80 * 1024 : 88 * 1024;
+    static constexpr int kRingBytes = kRingK + kRingV;
+    static constexpr int kNS = 24;                   // chunk slots (ids, masks, descriptor, barriers)
+    static constexpr int kNQ = D == 128 ? 8 : 16;    // Q tile slots (items in flight per CTA)
     static constexpr int kQBytes = 16 * D * 2;
     static constexpr int kPBytes = 16 * kMaxRows * 2;
-    static constexpr int kPad = D == 128 ? 8 * 1024 : 0;  // MMA1 may read past a short tile (masked lanes)
-    static constexpr int oRing = 0;
+    static constexpr int kSB = 4;                    // S/P/O buffers in flight (TMEM and SMEM)
+    static constexpr int kSlotBytes = 32 + 128 * 4 + 128 * 2;  // sizeof(Slot)
+    static constexpr int oRing = 0;                  // K ring, then V ring
+    static constexpr int oRingV = kRingK;
     static constexpr int oQ = oRing + kRingBytes;
     static constexpr int oP = oQ + kNQ * kQBytes;
-    static constexpr int oRed = oP + 2 * kPBytes + kPad;  // float [2][4][16] chunk row-max partials
-    static constexpr int oLred = oRed + 2 * 4 * 16 * 4;   // float [4][16] row-sum partials
-    static constexpr int oDesc = oLred + 4 * 16 * 4;      // ChunkDesc [kNS]
-    static constexpr int oReg = oDesc + kNS * 32;         // int2 [kNS] ring regions
-    static constexpr int kNumBars = 3 * kNS + 2 * kNQ + 6;
-    static constexpr int oBar = oReg + kNS * 8;
+    static constexpr int oSlot = oP + kSB * kPBytes;
+    static constexpr int oRed = oSlot + kNS * kSlotBytes;  // float [kSB][4][16] chunk row-max partials
+    static constexpr int oLred = oRed + kSB * 4 * 16 * 4;  // float [2][4][16] row-sum partials per item
+    static constexpr int oCorr = oLred + 2 * 4 * 16 * 4;   // CorrSlot [kSB]
+    static constexpr int oReg = oCorr + kSB * 96;          // int2 [2][kNS] ring regions (K, V)
+    static constexpr int kNumBars = 6 * kNS + 2 * kNQ + 4 * kSB + 4;
+    static constexpr int oBar = oReg + 2 * kNS * 8;
     static constexpr int oTmem = oBar + kNumBars * 8;
-    static constexpr int kSmemBytes = oTmem + 16 + 1024;  // + slack for 1024-byte alignment
-    static constexpr int kCtasPerSm = D == 128 ? 1 : 2;
-    static constexpr int kThreads = 192;
-    static_assert(kRingBytes >= 2 * 2 * (kMaxRows / 8) * kGroupBytes, "ring must hold two full chunks");
-    static_assert(oQ + kNQ * kQBytes + 2 * kPBytes + kPad >= kRingBytes + 12 * kGroupBytes, "over-read pad");
+    static constexpr int kSmemBytes = oTmem + 16;
+    static constexpr int kCtasPerSm = 1;
+    static constexpr int kLoaderWarps = 8;           // cp.async gather warps (memory-level parallelism)
+    static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps, kCorr0 = kSoftmax0 + 4;
+    static constexpr int kThreads = 32 * (kCorr0 + 4);  // control, MMA, index, loaders, softmax, correction
+    static constexpr int kBatch = 8;                 // items fetched per queue round trip
+    static_assert(kRingK >= (kMaxRows / 8) * kGroupBytes && kRingV >= (kMaxRows / 8) * kGroupBytes,
+                  "each ring must hold one full tile");
+    // MMA1 (M = 128) may read up to 12 row groups past a short tile; those lanes are masked
+    // (the K ring is followed by the V ring, the V ring by Q/P/slots: valid shared memory)
+    static_assert(oRed >= kRingBytes + 12 * kGroupBytes && kRingV >= 12 * kGroupBytes, "over-read pad");
+    static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 };
 
-// barrier indices
 template <int D> struct Bars {
     using C = Cfg<D>;
-    __host__ __device__ static constexpr int kfull(int s) { return s; }
-    __host__ __device__ static constexpr int vfull(int s) { return C::kNS + s; }
-    __host__ __device__ static constexpr int empty(int s) { return 2 * C::kNS + s; }
-    __host__ __device__ static constexpr int qfull(int q) { return 3 * C::kNS + q; }
-    __host__ __device__ static constexpr int qempty(int q) { return 3 * C::kNS + C::kNQ + q; }
-    __host__ __device__ static constexpr int sfull(int b) { return 3 * C::kNS + 2 * C::kNQ + b; }
-    __host__ __device__ static constexpr int pfull(int b) { return 3 * C::kNS + 2 * C::kNQ + 2 + b; }
-    __host__ __device__ static constexpr int ofull(int b) { return 3 * C::kNS + 2 * C::kNQ + 4 + b; }
+    __host__ __device__ static constexpr int idxfull(int s) { return s; }
+    __host__ __device__ static constexpr int kfull(int s) { return C::kNS + s; }
+    __host__ __device__ static constexpr int vfull(int s) { return 2 * C::kNS + s; }
+    __host__ __device__ static constexpr int empty(int s) { return 3 * C::kNS + s; }
+    __host__ __device__ static constexpr int qfull(int q) { return 4 * C::kNS + q; }
+    __host__ __device__ static constexpr int qempty(int q) { return 4 * C::kNS + C::kNQ + q; }
+    static constexpr int kB0 = 4 * C::kNS + 2 * C::kNQ;
+    __host__ __device__ static constexpr int sfull(int b) { return kB0 + b; }
+    __host__ __device__ static constexpr int pfull(int b) { return kB0 + C::kSB + b; }
+    __host__ __device__ static constexpr int ofull(int b) { return kB0 + 2 * C::kSB + b; }
+    __host__ __device__ static constexpr int pempty(int b) { return kB0 + 3 * C::kSB + b; }
+    __host__ __device__ static constexpr int lfull(int b) { return kB0 + 4 * C::kSB + b; }
+    __host__ __device__ static constexpr int lempty(int b) { return kB0 + 4 * C::kSB + 2 + b; }
+    __host__ __device__ static constexpr int rfull(int s) { return kB0 + 4 * C::kSB + 4 + s; }
+    __host__ __device__ static constexpr int kempty(int s) { return kB0 + 4 * C::kSB + 4 + C::kNS + s; }
 };
 
-struct __align__(16) ChunkDesc {
+// One chunk of one work item: written by the index warp (ids/masks by cp.async.bulk), the
+// ring offset by the producer; read by the MMA and softmax warps.
+struct __align__(16) Slot {
     int32_t rw;        // row window k
     int32_t head;      // head h
-    int32_t col_base;  // index of the chunk's first compacted column in cols/masks
     int32_t rows;      // valid compacted columns in this chunk (0 for an empty RW, -1 = stop)
     int32_t ring_off;  // byte offset of the K tile in the ring (V tile follows)
     int32_t qslot;
     int32_t flags;     // bit0 first chunk of item, bit1 last chunk, bit2 Q-slot phase
-    int32_t ralloc;    // rows allocated (multiple of 16)
+    int32_t ralloc;    // rows allocated in the ring (multiple of 16)
+    int32_t pad;       // byte offset of the V tile in the V ring
+    int32_t cols[128];     // gathered row ids (tail repeats the last column)
+    uint16_t masks[128];   // 16-bit row masks (bitmap)
+};
+// softmax -> correction hand-off for one chunk (double-buffered with P)
+struct __align__(16) CorrSlot {
+    float alpha[16];   // e^{m_old - m_new} per query row (Alg.1 l.21)
+    int32_t rows, flags, rw, head;
+    uint64_t t_s, t_p; // F3S_TRACE stamps of the softmax group (written out by the correction group)
 };
 
 // Transposing butterfly: 16 per-row values in each of 32 lanes -> lane l holds the
@@ -117,27 +151,49 @@ __device__ __forceinline__ float rowreduce16(const float (&v)[16], int lane, Op 
 struct OpMax { __device__ float operator()(float a, float b) const { return fmaxf(a, b); } };
 struct OpAdd { __device__ float operator()(float a, float b) const { return a + b; } };
 
-template <typename T> __device__ __forceinline__ uint16_t to_bits(float x);
-template <> __device__ __forceinline__ uint16_t to_bits<__half>(float x) { return __half_as_ushort(__float2half_rn(x)); }
-template <> __device__ __forceinline__ uint16_t to_bits<__nv_bfloat16>(float x) {
-    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
-}
+template <typename T> __device__ __forceinline__ uint32_t pack2(float lo, float hi);
+template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) { return pack_f16x2(lo, hi); }
+template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) { return pack_bf16x2(lo, hi); }
 
-template <int D, typename T>
+template <int D, typename T, bool kDiag>
 __global__ void __launch_bounds__(Cfg<D>::kThreads, Cfg<D>::kCtasPerSm)
 k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-            const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ rw_ptr,
-            const int32_t* __restrict__ cols, const uint16_t* __restrict__ masks, const int32_t* __restrict__ order,
-            int32_t* __restrict__ counter, int32_t n_items, int32_t H, int32_t n_rows, float* __restrict__ O,
-            float scale_log2) {
+            const __grid_constant__ CUtensorMap tmV, const int4* __restrict__ meta,
+            const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
+            int32_t* __restrict__ counter, int32_t n_items, int32_t H, int32_t n_rows, int32_t chunk_rows,
+            const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float* __restrict__ O, float scale_log2,
+            uint64_t* __restrict__ trace, int32_t trace_chunks) {
     using C = Cfg<D>;
     using B = Bars<D>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sb = smem_u32(smem);
+    if (sb & 1023) __trap();  // swizzled tiles need 1024-byte alignment
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto bar = [&](int i) -> uint32_t { return sb + C::oBar + 8u * i; };
-    ChunkDesc* descs = reinterpret_cast<ChunkDesc*>(smem + C::oDesc);
+    Slot* slots = reinterpret_cast<Slot*>(smem + C::oSlot);
+    CorrSlot* corr = reinterpret_cast<CorrSlot*>(smem + C::oCorr);
+    // F3S_TRACE: per CTA and chunk, globaltimer stamps of the pipeline events
+    // [0 slot written, 1 gathers issued, 2 MMA1 issued, 3 S seen, 4 P written, 5 MMA2 issued, 6 O seen, 7 item stored]
+    auto stamp = [&](int32_t c, int ev) {
+        if (kDiag && trace != nullptr && c < trace_chunks)
+            trace[((size_t)blockIdx.x * trace_chunks + c) * 8 + ev] = globaltimer_ns();
+    };
+    // profile mode (trace_chunks == 0): each role accumulates ns spent per phase in registers
+    // and writes trace[cta][32] once at the end (no stores on the hot path)
+    const bool prof = kDiag && trace != nullptr && trace_chunks == 0;
+    uint64_t pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint64_t pt0 = prof ? globaltimer_ns() : 0;
+    auto lap = [&](int k) {  // charge the time since the previous lap to counter k
+        if (prof) {
+            const uint64_t t = globaltimer_ns();
+            pc[k] += t - pt0;
+            pt0 = t;
+        }
+    };
+    auto prof_flush = [&](int base) {  // base in units of roles: 8 counters each
+        if (prof)
+            for (int k = 0; k < 8; ++k) trace[(size_t)blockIdx.x * 64 + base * 8 / 6 + k] = pc[k];
+    };
 
     // ---- setup -------------------------------------------------------------------------------
     // Ring bytes that no gather overwrites are read by MMA2 (rows between the last gathered
@@ -146,18 +202,26 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         reinterpret_cast<int4*>(smem + C::oRing)[i] = make_int4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::kNS; ++s) {
-            mbar_init(bar(B::kfull(s)), 1);
-            mbar_init(bar(B::vfull(s)), 1);
-            mbar_init(bar(B::empty(s)), 1);
+            mbar_init(bar(B::idxfull(s)), 1);
+            mbar_init(bar(B::kfull(s)), 32 * C::kLoaderWarps);  // one cp.async completion per loader lane
+            mbar_init(bar(B::vfull(s)), 32 * C::kLoaderWarps);
+            mbar_init(bar(B::rfull(s)), 1);
+            mbar_init(bar(B::empty(s)), 1);   // V tile (and the slot) retired: MMA2 done
+            mbar_init(bar(B::kempty(s)), 1);  // K tile retired: MMA1 done
         }
         for (int q = 0; q < C::kNQ; ++q) {
             mbar_init(bar(B::qfull(q)), 1);
             mbar_init(bar(B::qempty(q)), 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < C::kSB; ++b) {
             mbar_init(bar(B::sfull(b)), 1);
             mbar_init(bar(B::pfull(b)), 128);
             mbar_init(bar(B::ofull(b)), 1);
+            mbar_init(bar(B::pempty(b)), 128);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bar(B::lfull(b)), 128);
+            mbar_init(bar(B::lempty(b)), 128);
         }
         fence_mbar_init();
     }
@@ -167,7 +231,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         tma_prefetch_desc(&tmV);
     }
     if (warp == 1) {
-        tmem_alloc<64>(sb + C::oTmem);
+        tmem_alloc<32 * C::kSB>(sb + C::oTmem);
         tmem_relinquish();
     }
     fence_proxy_async_smem();
@@ -176,258 +240,465 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     tc_fence_after();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + C::oTmem);
 
-    if (warp == 0) {
-        // ===== producer: work queue, Q tiles, K/V gathers ======================================
-        const uint64_t pol = policy_evict_normal();
-        int2* reg = reinterpret_cast<int2*>(smem + C::oReg);
-        int32_t seq = 0, tail = 0, qseq = 0;
-        uint32_t head = 0;
-        for (;;) {
-            int32_t item = 0;
-            if (lane == 0) item = atomicAdd(counter, 1);
-            item = __shfl_sync(0xffffffffu, item, 0);
-            if (item >= n_items) break;
-            const int32_t kq = item / H;
-            const int32_t h = item - kq * H;
-            const int32_t k = __ldg(order + kq);
-            const int32_t cb = __ldg(rw_ptr + k), w = __ldg(rw_ptr + k + 1) - cb;
-            const int qs = qseq % C::kNQ;
-            const uint32_t qph = (qseq / C::kNQ) & 1;
-            mbar_wait(bar(B::qempty(qs)), qph ^ 1);
-            if (lane == 0) {
-                mbar_arrive_expect_tx(bar(B::qfull(qs)), C::kQBytes);
-#pragma unroll
-                for (int pp = 0; pp < C::P; ++pp)
-                    tma_load_2d(sb + C::oQ + qs * C::kQBytes + pp * 2048, &tmQ, bar(B::qfull(qs)), h * D + 64 * pp,
-                                16 * k);
+    if (warp == 2) {
+        // ===== index warp: work queue (LPT order) -> chunk slots =========================
+        // kBatch lanes each take one item per queue round trip; per chunk one lane issues two
+        // bulk copies (column ids, masks) straight into the slot.
+        int32_t seq = 0, qseq = 0;
+        bool done = false;
+        while (!done) {
+            int32_t it = 0x7FFFFFFF;
+            int4 mt = make_int4(0, 0, 0, 0);
+            if (lane < C::kBatch) {
+                it = atomicAdd(counter, 1);
+                if (it < n_items) mt = __ldg(meta + it / H);
             }
-            const int nch = w > 0 ? (w + C::kMaxRows - 1) / C::kMaxRows : 1;
-            for (int j = 0; j < nch; ++j) {
-                const int rows = w > 0 ? min(C::kMaxRows, w - C::kMaxRows * j) : 0;
-                const int ralloc = rows > 0 ? ((rows + 15) & ~15) : 0;
-                const uint32_t tile = (uint32_t)(ralloc / 8) * C::kGroupBytes;
-                const uint32_t bytes = 2 * tile;
-                // the slot's previous chunk must be retired (descriptor and barriers reused)
-                while (tail <= seq - C::kNS) {
-                    mbar_wait(bar(B::empty(tail % C::kNS)), (tail / C::kNS) & 1);
-                    ++tail;
-                }
-                uint32_t off = 0;
-                if (bytes > 0) {
-                    off = head + bytes <= (uint32_t)C::kRingBytes ? head : 0;
-                    for (;;) {  // retire the oldest chunks until [off, off+bytes) is free
-                        bool ov = false;
-                        for (int t = tail; t < seq; ++t) {
-                            const int2 r = reg[t % C::kNS];
-                            if (r.y > r.x && (int)off < r.y && (int)(off + bytes) > r.x) { ov = true; break; }
+            __syncwarp();
+            if (lane == 0) lap(1);
+            for (int b = 0; b < C::kBatch; ++b) {
+                const int32_t itb = __shfl_sync(0xffffffffu, it, b);
+                const int32_t k = __shfl_sync(0xffffffffu, mt.x, b);
+                const int32_t cb8 = __shfl_sync(0xffffffffu, mt.y, b);
+                const int32_t w = __shfl_sync(0xffffffffu, mt.z, b);
+                if (itb >= n_items) { done = true; continue; }
+                const int32_t h = itb - (itb / H) * H;
+                const int nch = w > 0 ? (w + chunk_rows - 1) / chunk_rows : 1;
+                const int qs = qseq % C::kNQ;
+                const int qph = (qseq / C::kNQ) & 1;
+                for (int j = 0; j < nch; ++j) {
+                    const int rows = w > 0 ? min(chunk_rows, w - chunk_rows * j) : 0;
+                    const int s = seq % C::kNS;
+                    if (lane == 0) {
+                        mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+                        lap(0);
+                        Slot& sl = slots[s];
+                        sl.rw = k;
+                        sl.head = h;
+                        sl.rows = rows;
+                        sl.qslot = qs;
+                        sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2);
+                        sl.ralloc = rows > 0 ? ((rows + 15) & ~15) : 0;
+                        const uint32_t fb = bar(B::idxfull(s));
+                        if (rows > 0) {
+                            const uint32_t r8 = (uint32_t)((rows + 7) & ~7);
+                            mbar_arrive_expect_tx(fb, r8 * 6u);
+                            bulk_g2s(smem_u32(sl.cols), kcols + cb8 + chunk_rows * j, r8 * 4u, fb);
+                            bulk_g2s(smem_u32(sl.masks), kmasks + cb8 + chunk_rows * j, r8 * 2u, fb);
+                        } else {
+                            mbar_arrive(fb);
                         }
-                        if (!ov) break;
-                        mbar_wait(bar(B::empty(tail % C::kNS)), (tail / C::kNS) & 1);
-                        ++tail;
+                        stamp(seq, 0);
+                        lap(2);
                     }
-                    head = off + bytes;
+                    ++seq;
                 }
-                const int s = seq % C::kNS;
-                __syncwarp();
-                if (lane == 0) {
-                    reg[s] = make_int2((int)off, (int)(off + bytes));
-                    ChunkDesc dsc;
-                    dsc.rw = k;
-                    dsc.head = h;
-                    dsc.col_base = cb + C::kMaxRows * j;
-                    dsc.rows = rows;
-                    dsc.ring_off = (int)off;
-                    dsc.qslot = qs;
-                    dsc.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (int)(qph << 2);
-                    dsc.ralloc = ralloc;
-                    descs[s] = dsc;
-                }
-                __syncwarp();
-                const uint32_t kfb = bar(B::kfull(s)), vfb = bar(B::vfull(s));
-                const int ng = (rows + 3) >> 2;  // gather4 groups
-                if (lane == 0) {
-                    if (rows > 0) {
-                        mbar_arrive_expect_tx(kfb, (uint32_t)ng * 512u * C::P);
-                        mbar_arrive_expect_tx(vfb, (uint32_t)ng * 512u * C::P);
-                    } else {
-                        mbar_arrive(kfb);
-                        mbar_arrive(vfb);
-                    }
-                }
-                __syncwarp();
-                if (lane < ng) {
-                    // rows past the end of the chunk repeat its last column: finite data,
-                    // masked out of the softmax and weighted 0 in the SpMM
-                    const int32_t* cp = cols + cb + C::kMaxRows * j;
-                    const int r0 = 4 * lane, last = rows - 1;
-                    const int32_t i0 = __ldg(cp + min(r0, last)), i1 = __ldg(cp + min(r0 + 1, last));
-                    const int32_t i2 = __ldg(cp + min(r0 + 2, last)), i3 = __ldg(cp + min(r0 + 3, last));
-                    const uint32_t go = (uint32_t)(lane >> 1) * C::kGroupBytes + (uint32_t)(lane & 1) * 512u;
-                    const uint32_t kt = sb + C::oRing + off + go, vt = kt + tile;
-#pragma unroll
-                    for (int pp = 0; pp < C::P; ++pp)
-                        tma_gather4(kt + pp * 1024, &tmK, kfb, h * D + 64 * pp, i0, i1, i2, i3, pol);
-#pragma unroll
-                    for (int pp = 0; pp < C::P; ++pp)
-                        tma_gather4(vt + pp * 1024, &tmV, vfb, h * D + 64 * pp, i0, i1, i2, i3, pol);
-                }
-                ++seq;
+                ++qseq;
             }
-            ++qseq;
         }
-        // stop marker
-        while (tail <= seq - C::kNS) {
-            mbar_wait(bar(B::empty(tail % C::kNS)), (tail / C::kNS) & 1);
-            ++tail;
-        }
-        __syncwarp();
         if (lane == 0) {
             const int s = seq % C::kNS;
-            descs[s].rows = -1;
-            mbar_arrive(bar(B::kfull(s)));
-            mbar_arrive(bar(B::vfull(s)));
+            mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+            slots[s].rows = -1;
+            mbar_arrive(bar(B::idxfull(s)));
+            prof_flush(0);
         }
         __syncwarp();
-    } else if (warp == 1) {
-        // ===== MMA issuer ==========================================================================
-        constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
-        constexpr uint32_t idesc1 = idesc_f16(fmt, 0, 0, 128, 16);  // S^T = K_c . Q_w^T
-        constexpr uint32_t idesc2 = idesc_f16(fmt, 1, 0, D, 16);    // O^T = V_c^T . P^T (A MN-major)
+    } else if (warp == 0) {
+        // ===== producer: Q tiles and K/V gathers into the ring ====================================
+        int2* regk = reinterpret_cast<int2*>(smem + C::oReg);
+        int2* regv = regk + C::kNS;
+        int32_t seq = 0, tailk = 0, tailv = 0;
+        uint32_t headk = 0, headv = 0;
+        for (;;) {
+            const int s = seq % C::kNS;
+            mbar_wait(bar(B::idxfull(s)), (seq / C::kNS) & 1);
+            lap(0);
+            Slot& sl = slots[s];
+            const int rows = sl.rows;
+            if (rows < 0) {
+                if (lane == 0) {
+                    mbar_arrive(bar(B::rfull(s)));
+                    prof_flush(6);
+                }
+                break;
+            }
+            const int flags = sl.flags, k = sl.rw, h = sl.head, qs = sl.qslot;
+            if (flags & 1) {  // Alg.1 l.5: Q_i for the item's first chunk
+                mbar_wait(bar(B::qempty(qs)), ((flags >> 2) & 1) ^ 1);
+                lap(1);
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(bar(B::qfull(qs)), C::kQBytes);
+#pragma unroll
+                    for (int pp = 0; pp < C::P; ++pp)
+                        tma_load_2d(sb + C::oQ + qs * C::kQBytes + pp * 2048, &tmQ, bar(B::qfull(qs)),
+                                    h * D + 64 * pp, 16 * k);
+                }
+            }
+            const uint32_t tile = (uint32_t)(sl.ralloc / 8) * C::kGroupBytes;
+            // the index warp reused this slot, so chunk seq - kNS (and all before it) retired
+            if (tailk < seq - (C::kNS - 1)) tailk = seq - (C::kNS - 1);
+            if (tailv < seq - (C::kNS - 1)) tailv = seq - (C::kNS - 1);
+            // FIFO byte rings: chunks [tail, seq) occupy the cyclic span [start(tail), head); a tile
+            // goes at head, or at 0 if it does not fit before the end; retire the oldest until free.
+            auto alloc = [&](uint32_t& head, int32_t& tail, const int2* reg, uint32_t cap, int bar_base) -> uint32_t {
+                if (tile == 0) return head;  // zero-byte chunks (empty row windows) sit at head
+                for (;;) {
+                    const bool wrap = head + tile > cap;
+                    const uint32_t off = wrap ? 0u : head;
+                    bool ok = true;
+                    if (tail != seq) {
+                        const uint32_t ts = (uint32_t)reg[tail % C::kNS].x;
+                        ok = ts < head ? (!wrap || off + tile <= ts) : (!wrap && off + tile <= ts);
+                        if (ts == head) ok = false;  // full
+                    }
+                    if (ok) {
+                        head = off + tile;
+                        return off;
+                    }
+                    mbar_wait(bar(bar_base + tail % C::kNS), (tail / C::kNS) & 1);
+                    ++tail;
+                }
+            };
+            const uint32_t offk = alloc(headk, tailk, regk, (uint32_t)C::kRingK, B::kempty(0));
+            const uint32_t offv = alloc(headv, tailv, regv, (uint32_t)C::kRingV, B::empty(0));
+            lap(2);
+            __syncwarp();
+            if (lane == 0) {
+                regk[s] = make_int2((int)offk, (int)(offk + tile));
+                regv[s] = make_int2((int)offv, (int)(offv + tile));
+                sl.ring_off = (int)offk;
+                sl.pad = (int)offv;
+            }
+            __syncwarp();
+            lap(3);
+            if (lane == 0) mbar_arrive(bar(B::rfull(s)));  // ring space assigned: loaders may gather
+            ++seq;
+        }
+        __syncwarp();
+    } else if (warp >= C::kLoader0 && warp < C::kSoftmax0) {
+        // ===== loader warps: gather the K and V rows of each chunk (Alg.1 l.8) ===================
+        // Lane l of a warp copies 16-byte piece (l % pieces) of one gathered row straight into the
+        // 128B-swizzled UMMA layout; the rows of a chunk are dealt round-robin to the warps.
+        // Each lane arrives on the chunk's K/V barriers when its own copies have landed.
+        constexpr int kPieces = D * 2 / 16;
+        constexpr int kRowsPerOp = 32 / kPieces;
+        const int lw = warp - C::kLoader0;
+        const int piece = lane % kPieces, rsub = lane / kPieces;
+        const int pnl = piece >> 3, cc = piece & 7;
+        const int64_t ldb = (int64_t)H * D * 2;
         int32_t seq = 0;
         for (;;) {
             const int s = seq % C::kNS;
-            const uint32_t ph = (seq / C::kNS) & 1;
-            mbar_wait(bar(B::kfull(s)), ph);
-            const ChunkDesc dsc = descs[s];
-            if (dsc.rows < 0) break;
-            const int b = seq & 1;
-            if (dsc.flags & 1) mbar_wait(bar(B::qfull(dsc.qslot)), (dsc.flags >> 2) & 1);
-            tc_fence_after();
-            const uint32_t kt = sb + C::oRing + dsc.ring_off;
-            const uint32_t qt = sb + C::oQ + dsc.qslot * C::kQBytes;
-            if (lane == 0) {
-                if (dsc.rows > 0) {
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint64_t a = smem_desc_sw128(kt + (kk >> 2) * 1024 + (kk & 3) * 32, 16, C::kGroupBytes);
-                        const uint64_t bq = smem_desc_sw128(qt + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-                        mma_f16_ss(tmem + b * 16, a, bq, idesc1, kk > 0 ? 1u : 0u);
-                    }
-                }
-                mma_commit(bar(B::sfull(b)));
-                if (dsc.flags & 2) mma_commit(bar(B::qempty(dsc.qslot)));
+            mbar_wait(bar(B::rfull(s)), (seq / C::kNS) & 1);
+            const Slot& sl = slots[s];
+            const int rows = sl.rows;
+            const uint32_t kfb = bar(B::kfull(s)), vfb = bar(B::vfull(s));
+            if (rows < 0) {
+                mbar_arrive(kfb);
+                mbar_arrive(vfb);
+                break;
             }
-            __syncwarp();
-            mbar_wait(bar(B::pfull(b)), (seq >> 1) & 1);
-            mbar_wait(bar(B::vfull(s)), ph);
-            tc_fence_after();
-            if (lane == 0) {
-                if (dsc.rows > 0) {
-                    const uint32_t vt = kt + (uint32_t)(dsc.ralloc / 8) * C::kGroupBytes;
-                    const uint32_t pt = sb + C::oP + b * C::kPBytes;
-                    const int nsteps = (dsc.rows + 15) >> 4;
-                    for (int st = 0; st < nsteps; ++st) {
-                        const uint64_t a = smem_desc_sw128(vt + st * 2 * C::kGroupBytes, 1024, C::kGroupBytes);
-                        const uint64_t bp = smem_desc_sw128(pt + (st >> 2) * 2048 + (st & 3) * 32, 16, 1024);
-                        mma_f16_ss(tmem + 32 + b * 16, a, bp, idesc2, st > 0 ? 1u : 0u);
-                    }
+            const int h = sl.head;
+            const uint32_t kt = sb + C::oRing + sl.ring_off + pnl * 1024;
+            const uint32_t vt = sb + C::oRingV + sl.pad + pnl * 1024;
+            const uint8_t* kbase = Kg + (int64_t)h * D * 2 + piece * 16;
+            const uint8_t* vbase = Vg + (int64_t)h * D * 2 + piece * 16;
+            const int ops = (rows + kRowsPerOp - 1) / kRowsPerOp;
+#pragma unroll 2
+            for (int t = lw; t < ops; t += C::kLoaderWarps) {
+                const int r = t * kRowsPerOp + rsub;
+                if (r < rows) {
+                    const int64_t j = sl.cols[r];
+                    const uint32_t o = (uint32_t)(r >> 3) * C::kGroupBytes + (uint32_t)(r & 7) * 128 +
+                                       (uint32_t)((cc ^ (r & 7)) << 4);
+                    cp_async_16(kt + o, kbase + j * ldb);
+                    cp_async_16(vt + o, vbase + j * ldb);
                 }
-                mma_commit(bar(B::ofull(b)));
-                mma_commit(bar(B::empty(s)));
             }
-            __syncwarp();
+            cp_async_mbar_arrive(kfb);
+            cp_async_mbar_arrive(vfb);
+            if (lw == 0 && lane == 0) stamp(seq, 1);
             ++seq;
         }
-    } else {
-        // ===== softmax / correction / epilogue (warps 2..5) =======================================
+    } else if (warp == 1) {
+        // ===== MMA issuer (one thread, event loop) ====================================================
+        // MMA1(c) as soon as K_c (and Q) landed and S buffer c&1 is free (MMA2(c-2) issued);
+        // MMA2(c) as soon as P_c is written and V_c landed.  Both in chunk order.
+        if (lane == 0) {
+            constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+            constexpr uint32_t idesc1 = idesc_f16(fmt, 0, 0, 128, 16);  // S^T = K_c . Q_w^T
+            constexpr uint32_t idesc2 = idesc_f16(fmt, 1, 1, D, 16);    // O^T = V_c^T . P^T (A, B MN-major)
+            int32_t n1 = 0, n2 = 0, stop_at = 0x7FFFFFFF;
+            const uint64_t t0 = globaltimer_ns();
+            uint64_t idle_since = 0;
+            while (n2 < stop_at) {
+                bool progressed = false;
+                if (n1 < stop_at && n1 < n2 + C::kSB) {
+                    const int s = n1 % C::kNS;
+                    if (mbar_test(bar(B::kfull(s)), (n1 / C::kNS) & 1)) {
+                        const Slot& sl = slots[s];
+                        if (sl.rows < 0) {
+                            stop_at = n1;
+                            progressed = true;
+                        } else if (!(sl.flags & 1) || mbar_test(bar(B::qfull(sl.qslot)), (sl.flags >> 2) & 1)) {
+                            fence_proxy_async_smem();  // cp.async (generic proxy) data -> tensor core
+                            tc_fence_after();
+                            const int b = n1 % C::kSB;
+                            const uint32_t kt = sb + C::oRing + sl.ring_off;
+                            const uint32_t qt = sb + C::oQ + sl.qslot * C::kQBytes;
+                            if (sl.rows > 0) {
+#pragma unroll
+                                for (int kk = 0; kk < D / 16; ++kk) {
+                                    const uint64_t a = smem_desc_sw128(kt + (kk >> 2) * 1024 + (kk & 3) * 32, 16, C::kGroupBytes);
+                                    const uint64_t bq = smem_desc_sw128(qt + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
+                                    mma_f16_ss(tmem + b * 16, a, bq, idesc1, kk > 0 ? 1u : 0u);
+                                }
+                            }
+                            mma_commit(bar(B::sfull(b)));
+                            mma_commit(bar(B::kempty(s)));
+                            if (sl.flags & 2) mma_commit(bar(B::qempty(sl.qslot)));
+                            stamp(n1, 2);
+                            lap(1);
+                            ++n1;
+                            progressed = true;
+                        }
+                    }
+                }
+                if (n2 < n1) {
+                    const int s = n2 % C::kNS, b = n2 % C::kSB;
+                    if (mbar_test(bar(B::pfull(b)), (n2 / C::kSB) & 1) && mbar_test(bar(B::vfull(s)), (n2 / C::kNS) & 1)) {
+                        fence_proxy_async_smem();
+                        tc_fence_after();
+                        const Slot& sl = slots[s];
+                        if (sl.rows > 0) {
+                            const uint32_t vt = sb + C::oRingV + sl.pad;
+                            const uint32_t pt = sb + C::oP + b * C::kPBytes;
+                            const int nsteps = (sl.rows + 15) >> 4;
+                            for (int st = 0; st < nsteps; ++st) {
+                                const uint64_t a = smem_desc_sw128(vt + st * 2 * C::kGroupBytes, 1024, C::kGroupBytes);
+                                const uint64_t bp = smem_desc_sw32(pt + st * 512, 4096, 256);
+                                mma_f16_ss(tmem + 16 * C::kSB + b * 16, a, bp, idesc2, st > 0 ? 1u : 0u);
+                            }
+                        }
+                        mma_commit(bar(B::ofull(b)));
+                        mma_commit(bar(B::empty(s)));
+                        stamp(n2, 5);
+                        lap(2);
+                        ++n2;
+                        progressed = true;
+                    }
+                }
+                // watchdog for the polling loop (the blocking waits have their own)
+                if (progressed) {
+                    idle_since = 0;
+                } else {
+                    lap(n1 < stop_at && n1 >= n2 + C::kSB ? 3 : (n2 < n1 ? 4 : 0));
+                    const uint64_t now = globaltimer_ns();
+                    if (idle_since == 0) idle_since = now;
+                    else if (now - idle_since > 20000000000ull) __trap();
+                }
+            }
+            (void)t0;
+            prof_flush(12);
+        }
+        __syncwarp();
+    } else if (warp < C::kCorr0) {
+        // ===== softmax warpgroup =====================================================
         const int q = warp & 3;          // TMEM lane quadrant this warp may access
         const int p = 32 * q + lane;     // compacted column of the chunk (S^T lane)
         const uint32_t tl = (uint32_t)(32 * q) << 16;
         float* red = reinterpret_cast<float*>(smem + C::oRed);
         float* lred = reinterpret_cast<float*>(smem + C::oLred);
-        float m[16], l[16], oacc[16];
+        // Running row max starts at a finite floor instead of -inf so that every exponent below
+        // is well defined without branches: alpha = 2^(m_old - m_new) is 0 at a row's first
+        // entries and 1 while the row is still empty; masked scores are -inf and give p = 0.
+        constexpr float kMFloor = -8.5e37f;
+        float m[16], l[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) { m[i] = -INFINITY; l[i] = 0.f; oacc[i] = 0.f; }
-        int32_t seq = 0;
+        for (int i = 0; i < 16; ++i) { m[i] = kMFloor; l[i] = 0.f; }
+        int32_t seq = 0, item = 0;
         for (;;) {
             const int s = seq % C::kNS;
+            const int b = seq % C::kSB;
+            const uint32_t bph = (seq / C::kSB) & 1;
             mbar_wait(bar(B::kfull(s)), (seq / C::kNS) & 1);
-            const ChunkDesc dsc = descs[s];
-            if (dsc.rows < 0) break;
-            if (dsc.flags & 1) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) { m[i] = -INFINITY; l[i] = 0.f; oacc[i] = 0.f; }
+            if (p == 0) lap(0);
+            const Slot& sl = slots[s];
+            const int rows = sl.rows;
+            if (rows < 0) {  // forward the stop to the correction group
+                mbar_wait(bar(B::pempty(b)), bph ^ 1);
+                if (p == 0) corr[b].rows = -1;
+                mbar_arrive(bar(B::pfull(b)));
+                if (p == 0) prof_flush(18);
+                break;
             }
-            const uint32_t mask = p < dsc.rows ? (uint32_t)__ldg(masks + dsc.col_base + p) : 0u;
-            const int b = seq & 1;
-            mbar_wait(bar(B::sfull(b)), (seq >> 1) & 1);
+            const int flags = sl.flags;
+            if (flags & 1) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) { m[i] = kMFloor; l[i] = 0.f; }
+            }
+            const uint32_t mask = p < rows ? (uint32_t)sl.masks[p] : 0u;
+            const int rw = sl.rw, hd = sl.head;
+            mbar_wait(bar(B::sfull(b)), bph);
             tc_fence_after();
+            uint64_t t_s = 0;
+            if (kDiag && p == 0) { t_s = globaltimer_ns(); lap(1); }
             float x[16];
             tmem_ld_32x32b_x16(tmem + tl + b * 16, x);
 #pragma unroll
             for (int i = 0; i < 16; ++i) x[i] = ((mask >> i) & 1u) ? x[i] * scale_log2 : -INFINITY;  // Alg.1 l.14
-            // chunk row max (Alg.1 l.16)
+            // chunk row max (Alg.1 l.16): warp butterfly + 4-warp combine
             const float rm = rowreduce16(x, lane, OpMax());
             if (!(lane & 1)) red[(b * 4 + q) * 16 + ((lane >> 1) & 15)] = rm;
+            if (p == 0) lap(2);
             named_bar_sync(1, 128);
-            float alpha[16];
+            // P_b / corr_b are free once the correction group consumed chunk seq - kSB
+            mbar_wait(bar(B::pempty(b)), bph ^ 1);
+            if (p == 0) lap(3);
             const float4* r4 = reinterpret_cast<const float4*>(red + b * 64);
+            // P^T is the MN-major B operand of MMA2 with a 32-byte swizzle: compacted column p
+            // owns one 32-byte row (its 16 query rows), 8 rows per 256-byte atom, the two 16-byte
+            // halves swapped when bit 2 of p is set.
+            uint4* prow = reinterpret_cast<uint4*>(smem + C::oP + b * C::kPBytes + (p >> 3) * 256 + (p & 7) * 32);
+            const int sw = (p >> 2) & 1;
+            float av[16], pv[16];
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
                 const float4 w0 = r4[g], w1 = r4[4 + g], w2 = r4[8 + g], w3 = r4[12 + g];
-                const float c0 = fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x));
-                const float c1 = fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y));
-                const float c2 = fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z));
-                const float c3 = fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w));
-                const float cm[4] = {c0, c1, c2, c3};
+                const float cm[4] = {fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x)), fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y)),
+                                     fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z)), fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w))};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int i = 4 * g + e;
                     const float mn = fmaxf(m[i], cm[e]);
-                    alpha[i] = mn == -INFINITY ? 1.f : ex2(m[i] - mn);  // e^{m_o - m_i}, 1 if still empty
+                    av[i] = ex2(m[i] - mn);  // e^{m_o - m_i} (l.18, l.21)
                     m[i] = mn;
+                    pv[i] = ex2(x[i] - mn);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
+                    l[i] = fmaf(l[i], av[i], pv[i]);  // l_o (l.18)
                 }
             }
-            // E_i = e^{S_i - m_i} (l.17), l_o update (l.18), E -> input dtype in SMEM (l.19)
-            uint8_t* pt = smem + C::oP + b * C::kPBytes + (p >> 6) * 2048;
-            const uint32_t cchunk = (uint32_t)(p & 63) >> 3, cin = (uint32_t)(p & 7) * 2;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float pv = ((mask >> i) & 1u) ? ex2(x[i] - m[i]) : 0.f;
-                l[i] = l[i] * alpha[i] + pv;
-                *reinterpret_cast<uint16_t*>(pt + i * 128 + ((cchunk ^ (uint32_t)(i & 7)) << 4) + cin) = to_bits<T>(pv);
+            if (p == 0) lap(6);
+            if (p < C::kMaxRows) {  // E cast to the input dtype into SMEM (l.19): two 16-byte stores
+                const uint4 lo = make_uint4(pack2<T>(pv[0], pv[1]), pack2<T>(pv[2], pv[3]), pack2<T>(pv[4], pv[5]),
+                                            pack2<T>(pv[6], pv[7]));
+                const uint4 hi = make_uint4(pack2<T>(pv[8], pv[9]), pack2<T>(pv[10], pv[11]), pack2<T>(pv[12], pv[13]),
+                                            pack2<T>(pv[14], pv[15]));
+                prow[sw] = lo;
+                prow[sw ^ 1] = hi;
             }
+            if (p == 0) {
+                float4* a4 = reinterpret_cast<float4*>(corr[b].alpha);
+                a4[0] = make_float4(av[0], av[1], av[2], av[3]);
+                a4[1] = make_float4(av[4], av[5], av[6], av[7]);
+                a4[2] = make_float4(av[8], av[9], av[10], av[11]);
+                a4[3] = make_float4(av[12], av[13], av[14], av[15]);
+                reinterpret_cast<int4*>(&corr[b].rows)[0] = make_int4(rows, flags, rw, hd);
+                if (kDiag) {
+                    corr[b].t_s = t_s;
+                    corr[b].t_p = globaltimer_ns();
+                }
+            }
+            if (p == 0) lap(7);
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(bar(B::pfull(b)));
-            // O_i = diag(alpha) O_i + E_i V_j (l.21-22): the chunk's O^T arrives in TMEM
-            mbar_wait(bar(B::ofull(b)), (seq >> 1) & 1);
-            tc_fence_after();
-            if (dsc.rows > 0) {
-                float ov[16];
-                tmem_ld_32x32b_x16(tmem + tl + 32 + b * 16, ov);
+            if (p == 0) lap(4);
+            if (flags & 2) {
+                // l_o partial sums of the item (l.18) -> correction group
+                const int ib = item & 1;
+                const float rl = rowreduce16(l, lane, OpAdd());
+                mbar_wait(bar(B::lempty(ib)), ((item >> 1) & 1) ^ 1);
+                if (!(lane & 1)) lred[(ib * 4 + q) * 16 + ((lane >> 1) & 15)] = rl;
+                mbar_arrive(bar(B::lfull(ib)));
+                if (p == 0) lap(5);
+                ++item;
+            }
+            ++seq;
+        }
+    } else {
+        // ===== correction / epilogue warpgroup =======================================
+        const int q = warp & 3;
+        const uint32_t tl = (uint32_t)(32 * q) << 16;
+        const float* lred = reinterpret_cast<const float*>(smem + C::oLred);
+        float oacc[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) oacc[i] = oacc[i] * alpha[i] + ov[i];
+        for (int i = 0; i < 16; ++i) oacc[i] = 0.f;
+        int32_t seq = 0, item = 0;
+        for (;;) {
+            const int b = seq % C::kSB;
+            const uint32_t bph = (seq / C::kSB) & 1;
+            mbar_wait(bar(B::pfull(b)), bph);
+            const bool lead = lane == 0 && q == 0;
+            if (lead) lap(0);
+            const int4 info = reinterpret_cast<const int4*>(&corr[b].rows)[0];
+            const int rows = info.x, flags = info.y, rw = info.z, hd = info.w;
+            if (rows < 0) {
+                if (lead) prof_flush(24);
+                break;
+            }
+            // O_i = diag(alpha) O_i + E_i V_j (l.21-22): the chunk's O^T arrives in TMEM
+            mbar_wait(bar(B::ofull(b)), bph);
+            tc_fence_after();
+            if (lead) {
+                if (kDiag && trace != nullptr && seq < trace_chunks) {
+                    trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 3] = corr[b].t_s;
+                    trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 4] = corr[b].t_p;
+                }
+                stamp(seq, 6);
+                lap(1);
+            }
+            const float4* a4 = reinterpret_cast<const float4*>(corr[b].alpha);
+            if (rows > 0) {
+                float ov[16];
+                tmem_ld_32x32b_x16(tmem + tl + 16 * C::kSB + b * 16, ov);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float4 a = a4[g];
+                    oacc[4 * g] = oacc[4 * g] * a.x + ov[4 * g];
+                    oacc[4 * g + 1] = oacc[4 * g + 1] * a.y + ov[4 * g + 1];
+                    oacc[4 * g + 2] = oacc[4 * g + 2] * a.z + ov[4 * g + 2];
+                    oacc[4 * g + 3] = oacc[4 * g + 3] * a.w + ov[4 * g + 3];
+                }
+            } else {
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float4 a = a4[g];
+                    oacc[4 * g] *= a.x; oacc[4 * g + 1] *= a.y; oacc[4 * g + 2] *= a.z; oacc[4 * g + 3] *= a.w;
+                }
             }
             tc_fence_before();
-            if (dsc.flags & 2) {
-                // l_o = sum over the 128 column partials; O_i = diag(l_o)^-1 O_i (l.24)
-                const float rl = rowreduce16(l, lane, OpAdd());
-                if (!(lane & 1)) lred[q * 16 + ((lane >> 1) & 15)] = rl;
-                named_bar_sync(2, 128);
+            mbar_arrive(bar(B::pempty(b)));
+            if (lead) lap(2);
+            if (flags & 2) {
+                // O_i = diag(l_o)^-1 O_i (l.24)
+                const int ib = item & 1;
+                mbar_wait(bar(B::lfull(ib)), (item >> 1) & 1);
+                if (lead) lap(3);
+                const float4* l4 = reinterpret_cast<const float4*>(lred + ib * 64);
+                float inv[16];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float4 a = l4[g], b4 = l4[4 + g], c = l4[8 + g], e = l4[12 + g];
+                    const float lt[4] = {(a.x + b4.x) + (c.x + e.x), (a.y + b4.y) + (c.y + e.y),
+                                         (a.z + b4.z) + (c.z + e.z), (a.w + b4.w) + (c.w + e.w)};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) inv[4 * g + u] = lt[u] > 0.f ? rcp_approx(lt[u]) : 0.f;  // empty row -> 0
+                }
+                mbar_arrive(bar(B::lempty(ib)));
+                const int nvalid = min(16, n_rows - 16 * rw);  // ragged last window (reading c14)
                 const bool has = D == 128 || lane < 16;
-                const int f = D == 128 ? p : 16 * q + lane;  // O^T lane -> feature (M = 64 layout)
+                const int f = D == 128 ? 32 * q + lane : 16 * q + lane;  // O^T lane -> feature (M = 64 layout)
                 if (has) {
                     const int64_t ld = (int64_t)H * D;
-                    float* out = O + (int64_t)16 * dsc.rw * ld + (int64_t)dsc.head * D + f;
+                    float* out = O + (int64_t)16 * rw * ld + (int64_t)hd * D + f;
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        if (16 * dsc.rw + i < n_rows) {
-                            const float lt = (lred[i] + lred[16 + i]) + (lred[32 + i] + lred[48 + i]);
-                            out[(int64_t)i * ld] = lt > 0.f ? oacc[i] * (1.f / lt) : 0.f;
-                        }
-                    }
+                    for (int i = 0; i < 16; ++i)
+                        if (i < nvalid) out[(int64_t)i * ld] = oacc[i] * inv[i];
                 }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) oacc[i] = 0.f;
+                if (lead) { stamp(seq, 7); lap(4); }
+                ++item;
             }
             ++seq;
         }
@@ -436,7 +707,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<64>(tmem);
+        tmem_dealloc<32 * C::kSB>(tmem);
     }
 }
 
@@ -503,16 +774,23 @@ f3s_status launch(const AttnArgs& a) {
     static std::once_flag attr_once;
     cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [&] {
-        attr_err = cudaFuncSetAttribute(k_f3s_sm100<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        attr_err = cudaFuncSetAttribute(k_f3s_sm100<D, T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(k_f3s_sm100<D, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     });
     F3S_CUDA_TRY(attr_err);
     const int32_t n_items = (int32_t)((int64_t)p.num_rw * a.heads);
-    const int grid = (int)std::min<int64_t>(n_items, (int64_t)sms * C::kCtasPerSm);
+    const int grid = a.grid_override > 0 ? a.grid_override : (int)std::min<int64_t>(n_items, (int64_t)sms * C::kCtasPerSm);
+    // compacted columns per chunk: smaller chunks keep more tiles in flight in the ring
+    int chunk_rows = 128;
+    if (const char* env = getenv("F3S_CHUNK_ROWS")) chunk_rows = std::max(16, std::min(128, atoi(env) / 16 * 16));
     int32_t* counter = p.counters + (g_call.fetch_add(1) % kNumCounterSlots);
     F3S_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int32_t), a.stream));
-    k_f3s_sm100<D, T><<<grid, C::kThreads, C::kSmemBytes, a.stream>>>(
-        mq, mk, mv, p.rw_ptr, p.cols, p.masks, a.lpt ? p.rw_order : p.rw_natural, counter, n_items, a.heads,
-        p.n_rows, a.O, a.scale * 1.4426950408889634f);
+    auto kern = a.trace ? k_f3s_sm100<D, T, true> : k_f3s_sm100<D, T, false>;
+    kern<<<grid, C::kThreads, C::kSmemBytes, a.stream>>>(
+        mq, mk, mv, a.lpt ? p.meta_lpt : p.meta_nat, p.kcols, p.kmasks, counter, n_items, a.heads, p.n_rows,
+        chunk_rows, static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.O,
+        a.scale * 1.4426950408889634f, a.trace, a.trace_chunks);
     count_launch();
     F3S_CUDA_TRY(cudaGetLastError());
     return F3S_OK;

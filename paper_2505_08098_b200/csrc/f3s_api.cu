@@ -44,11 +44,15 @@ static f3s_status check_attention_args(f3s_plan_t plan, const void* Q, const voi
 }
 
 static f3s_status run_attention(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
-                                int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, cudaStream_t stream) {
+                                int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, cudaStream_t stream,
+                                uint64_t* trace = nullptr, int32_t trace_chunks = 0, int32_t grid = 0) {
     f3s_status st = check_attention_args(plan, Q, K, V, O, scale, heads, d, dtype, true);
     if (st != F3S_OK) return st;
     AttnArgs a{reinterpret_cast<const Plan*>(plan), Q, K, V, O, scale, heads, d, dtype,
                variant != F3S_VARIANT_NO_REORDER, stream};
+    a.trace = trace;
+    a.trace_chunks = trace_chunks;
+    a.grid_override = grid;
     if (a.plan->n_rows == 0) return F3S_OK;
     switch (variant) {
         case F3S_VARIANT_DEFAULT:
@@ -106,6 +110,10 @@ f3s_status f3s_plan_destroy(f3s_plan_t plan) {
     cudaFree(p->rw_order);
     cudaFree(p->rw_natural);
     cudaFree(p->counters);
+    cudaFree(p->kcols);
+    cudaFree(p->kmasks);
+    cudaFree(p->meta_lpt);
+    cudaFree(p->meta_nat);
     cudaFree(p->staging);
     delete p;
     return F3S_OK;
@@ -151,6 +159,18 @@ f3s_status f3s_attention_ex(f3s_plan_t plan, const void* Q, const void* K, const
                             int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, cudaStream_t stream) {
     try {
         return run_attention(plan, Q, K, V, O, scale, heads, d, dtype, variant, stream);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_trace(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
+                               int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, uint64_t* trace,
+                               int32_t trace_chunks, int32_t grid, cudaStream_t stream) {
+    if (trace_chunks < 0 || grid < 0) { set_error("bad trace arguments"); return F3S_ERR_INVALID_VALUE; }
+    try {
+        return run_attention(plan, Q, K, V, O, scale, heads, d, dtype, variant, stream, trace, trace_chunks, grid);
     } catch (...) {
         set_error("internal error");
         return F3S_ERR_INTERNAL;

@@ -23,6 +23,14 @@ struct Plan {
     uint16_t* masks = nullptr;    // [W]
     int32_t* rw_order = nullptr;  // [R]  LPT order
     int32_t* rw_natural = nullptr;  // [R] identity order (ablation)
+    // kernel layout (derived from the canonical arrays): every window's columns start at a
+    // multiple of 8 entries so a chunk's ids/masks are 16-byte aligned for cp.async.bulk;
+    // the padding repeats the window's last column with mask 0.
+    int64_t total_cols8 = 0;
+    int32_t* kcols = nullptr;     // [W8]
+    uint16_t* kmasks = nullptr;   // [W8]
+    int4* meta_lpt = nullptr;     // [R] {k, start8, width, 0} in LPT order
+    int4* meta_nat = nullptr;     // [R] same, natural order (no-reorder ablation)
     int32_t* counters = nullptr;  // work-queue counters, kNumCounterSlots
     // e2e staging buffers for f3s_attention_host
     std::mutex staging_mu;
@@ -51,6 +59,9 @@ struct AttnArgs {
     f3s_dtype dtype;
     bool lpt;
     cudaStream_t stream;
+    uint64_t* trace = nullptr;  // F3S_TRACE buffer [grid][trace_chunks][8] (diagnostics)
+    int32_t trace_chunks = 0;
+    int32_t grid_override = 0;
 };
 
 f3s_status launch_attention_sm100(const AttnArgs& a);

@@ -23,7 +23,6 @@ struct DevBuf {
     ~DevBuf() { if (p) cudaFree(p); }
     cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
     template <class T> T* as() const { return static_cast<T*>(p); }
-    void* release() { void* q = p; p = nullptr; return q; }
 };
 
 int bits_for(int64_t max_value) {  // bits needed to hold values in [0, max_value]
@@ -94,6 +93,32 @@ __global__ void k_order_extract(const uint64_t* __restrict__ okeys, int32_t R, i
         order[k] = (int32_t)(okeys[k] & 0xFFFFFFFFu);
 }
 
+__global__ void k_width8(const int32_t* __restrict__ rw_ptr, int32_t R, int32_t* __restrict__ w8) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= R; k += (int64_t)gridDim.x * blockDim.x)
+        w8[k] = k < R ? ((rw_ptr[k + 1] - rw_ptr[k] + 7) & ~7) : 0;
+}
+
+// kernel layout: one warp per row window copies its columns/masks to an 8-aligned start and
+// pads to a multiple of 8 with the last column (mask 0); plus the per-window meta records.
+__global__ void k_kernel_layout(const int32_t* __restrict__ rw_ptr, const int32_t* __restrict__ rw_ptr8,
+                                const int32_t* __restrict__ cols, const uint16_t* __restrict__ masks,
+                                const int32_t* __restrict__ order, int32_t R, int32_t* __restrict__ kcols,
+                                uint16_t* __restrict__ kmasks, int4* __restrict__ meta_lpt, int4* __restrict__ meta_nat) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = warp; k < R; k += nwarps) {
+        const int32_t b = rw_ptr[k], w = rw_ptr[k + 1] - b, b8 = rw_ptr8[k], w8 = rw_ptr8[k + 1] - b8;
+        for (int32_t p = lane; p < w8; p += 32) {
+            kcols[b8 + p] = cols[b + min(p, w - 1)];
+            kmasks[b8 + p] = p < w ? masks[b + p] : (uint16_t)0;
+        }
+        if (lane == 0) meta_nat[k] = make_int4((int)k, b8, w, 0);
+        const int32_t ko = order[k];
+        if (lane == 1) meta_lpt[k] = make_int4(ko, rw_ptr8[ko], rw_ptr[ko + 1] - rw_ptr[ko], 0);
+    }
+}
+
 int grid_for(int64_t n, int block) {
     int64_t g = (n + block - 1) / block;
     return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
@@ -112,7 +137,8 @@ f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_
     if (!plan) return F3S_ERR_OUT_OF_MEMORY;
     struct Guard { Plan*& p; bool ok = false; ~Guard() { if (!ok && p) {
         cudaFree(p->rw_ptr); cudaFree(p->cols); cudaFree(p->masks); cudaFree(p->rw_order);
-        cudaFree(p->rw_natural); cudaFree(p->counters); delete p; p = nullptr; } } } guard{plan};
+        cudaFree(p->rw_natural); cudaFree(p->counters); cudaFree(p->kcols); cudaFree(p->kmasks);
+        cudaFree(p->meta_lpt); cudaFree(p->meta_nat); delete p; p = nullptr; } } } guard{plan};
     F3S_CUDA_TRY(cudaGetDevice(&plan->device));
     const int32_t R = (n_rows + kRowsPerWindow - 1) / kRowsPerWindow;
     plan->n_rows = n_rows;
@@ -231,11 +257,25 @@ f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_
         count_launch();
         F3S_CUDA_TRY(cudaGetLastError());
     }
-    F3S_CUDA_TRY(cudaEventRecord(ev1, stream));
+    // 8-aligned window starts of the kernel layout
+    DevBuf w8, rw8, t4;
+    F3S_CUDA_TRY(w8.alloc(sizeof(int32_t) * (size_t)(R + 1)));
+    F3S_CUDA_TRY(rw8.alloc(sizeof(int32_t) * (size_t)(R + 1)));
+    k_width8<<<grid_for(R + 1, 256), 256, 0, stream>>>(plan->rw_ptr, R, w8.as<int32_t>());
+    count_launch();
+    {
+        size_t tb = 0;
+        F3S_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, w8.as<int32_t>(), rw8.as<int32_t>(), R + 1, stream));
+        F3S_CUDA_TRY(t4.alloc(tb));
+        F3S_CUDA_TRY(cub::DeviceScan::ExclusiveSum(t4.p, tb, w8.as<int32_t>(), rw8.as<int32_t>(), R + 1, stream));
+        count_launch();
+    }
 
     // ---- 4. statistics (sync #3) --------------------------------------------------------------
     std::vector<int32_t> h_rw(R + 1);
     unsigned long long h_pop = 0;
+    int32_t h_w8 = 0;
+    F3S_CUDA_TRY(cudaMemcpyAsync(&h_w8, rw8.as<int32_t>() + R, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
     F3S_CUDA_TRY(cudaMemcpyAsync(h_rw.data(), plan->rw_ptr, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToHost, stream));
     F3S_CUDA_TRY(cudaMemcpyAsync(&h_pop, d_pop, sizeof(h_pop), cudaMemcpyDeviceToHost, stream));
     F3S_CUDA_TRY(cudaStreamSynchronize(stream));
@@ -249,9 +289,23 @@ f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_
     plan->total_tcb8 = tcb;
     plan->max_width = maxw;
     plan->nnz = (int64_t)h_pop;  // deduplicated nnz = total mask popcount
+    plan->total_cols8 = h_w8;
+    F3S_CUDA_TRY(cudaMalloc(&plan->kcols, sizeof(int32_t) * std::max<int64_t>(h_w8, 8)));
+    F3S_CUDA_TRY(cudaMalloc(&plan->kmasks, sizeof(uint16_t) * std::max<int64_t>(h_w8, 8)));
+    F3S_CUDA_TRY(cudaMalloc(&plan->meta_lpt, sizeof(int4) * std::max(R, 1)));
+    F3S_CUDA_TRY(cudaMalloc(&plan->meta_nat, sizeof(int4) * std::max(R, 1)));
+    if (R > 0) {
+        k_kernel_layout<<<grid_for((int64_t)R * 32, 256), 256, 0, stream>>>(
+            plan->rw_ptr, rw8.as<int32_t>(), plan->cols, plan->masks, plan->rw_order, R, plan->kcols, plan->kmasks,
+            plan->meta_lpt, plan->meta_nat);
+        count_launch();
+        F3S_CUDA_TRY(cudaGetLastError());
+    }
+    F3S_CUDA_TRY(cudaEventRecord(ev1, stream));
+    F3S_CUDA_TRY(cudaStreamSynchronize(stream));  // the plan is complete when f3s_plan returns
     F3S_CUDA_TRY(cudaEventElapsedTime(&plan->build_ms, ev0, ev1));
-    plan->device_bytes = (int64_t)sizeof(int32_t) * (2 * R + 1 + R + kNumCounterSlots) +
-                         (int64_t)(sizeof(int32_t) + sizeof(uint16_t)) * std::max<int64_t>(W, 1);
+    plan->device_bytes = (int64_t)sizeof(int32_t) * (2 * R + 1 + R + kNumCounterSlots) + (int64_t)sizeof(int4) * 2 * R +
+                         (int64_t)(sizeof(int32_t) + sizeof(uint16_t)) * (std::max<int64_t>(W, 1) + h_w8);
     guard.ok = true;
     *out = plan;
     return F3S_OK;

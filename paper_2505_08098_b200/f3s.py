@@ -43,6 +43,7 @@ _lib.f3s_plan_get_info.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
 _lib.f3s_plan_export.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.f3s_attention.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_trace.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]
 _lib.f3s_attention_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_partition_rows.argtypes = [_vp, _i32, _i32, _vp]
 _lib.f3s_partition_at.argtypes = [_vp, _i32, _vp, _i32, _i32, _vp]
@@ -51,11 +52,12 @@ _lib.f3s_status_string.restype = ctypes.c_char_p
 _lib.f3s_last_error.restype = ctypes.c_char_p
 _lib.f3s_launch_count.restype = _i64
 for _name in ("f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export",
-              "f3s_attention", "f3s_attention_ex", "f3s_attention_host", "f3s_partition_rows", "f3s_partition_at"):
+              "f3s_attention", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows",
+              "f3s_partition_at"):
     getattr(_lib, _name).restype = _i32
 
 EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export",
-            "f3s_attention", "f3s_attention_ex", "f3s_attention_host", "f3s_partition_rows", "f3s_partition_at",
+            "f3s_attention", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows", "f3s_partition_at",
             "f3s_status_string", "f3s_last_error", "f3s_launch_count"]
 
 
@@ -160,6 +162,21 @@ def attention_raw(p: Plan, q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, scale
     """Pointer-level call (no torch); used by bench loops and CUDA-graph capture."""
     _check(_lib.f3s_attention_ex(p.handle, q_ptr, k_ptr, v_ptr, o_ptr, float(scale), heads, d, dtype, variant, stream),
            "f3s_attention")
+
+
+def attention_trace(p: Plan, Q, K, V, O, *, scale: float, trace_chunks: int = 4096, grid: int = 0,
+                    variant: str | int = "default", stream=None):
+    """Run the default kernel with F3S_TRACE on; returns uint64 [grid, trace_chunks, 8] globaltimer stamps."""
+    import torch
+    import math
+    H, d = Q.shape[1], Q.shape[2]
+    g = grid or torch.cuda.get_device_properties(Q.device).multi_processor_count * 2  # upper bound on the grid
+    tr = torch.zeros((g, max(trace_chunks, 8), 8), dtype=torch.int64, device=Q.device)
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    _check(_lib.f3s_attention_trace(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), O.data_ptr(), float(scale), H, d,
+                                    _dtype_code(Q), v, tr.data_ptr(), trace_chunks, grid, _stream(stream)),
+           "f3s_attention_trace")
+    return tr
 
 
 def attention_host(p: Plan, Q, K, V, O, *, scale: float, heads: int, d: int, dtype: int, stream=None) -> None:

@@ -1,0 +1,42 @@
+"""F3S_TRACE profile mode: per-CTA ns spent per pipeline phase, summed per role."""
+import argparse, os, sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+NAMES = {0: "index: wait slot", 1: "index: queue fetch", 2: "index: issue",
+         8: "prod: wait ids", 9: "prod: wait Q slot", 10: "prod: wait ring", 11: "prod: issue",
+         16: "mma: idle", 17: "mma: MMA1", 18: "mma: MMA2", 19: "mma: S-buffer blocked", 20: "mma: wait P/V",
+         24: "smax: wait K", 25: "smax: wait S", 26: "smax: S->max", 27: "smax: bar+pempty", 28: "smax: fence+arrive",
+         29: "smax: l", 30: "smax: exp loop", 31: "smax: P/alpha stores",
+         32: "corr: wait P", 33: "corr: wait O", 34: "corr: fold", 35: "corr: wait l", 36: "corr: store"}
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="arxiv")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    import torch
+    from f3s_inputs import configs
+    from paper_2505_08098_b200 import f3s
+    w = configs.get(a.config)
+    csr = w.graph()
+    Qb, Kb, Vb = w.qkv(csr)
+    dev = lambda b: torch.from_numpy(b.view(np.int16)).cuda().view(torch.float16)
+    p = f3s.plan(torch.from_numpy(csr.row_ptr).cuda(), torch.from_numpy(csr.col_idx).cuda(), csr.n_rows)
+    Q, K, V = dev(Qb), dev(Kb), dev(Vb)
+    O = torch.empty(Q.shape, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        f3s.attention(p, Q, K, V, O, scale=w.scale)
+    tr = f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=0)
+    tr = tr[: tr.shape[0] // 2 if False else tr.shape[0]]
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(); f3s.attention(p, Q, K, V, O, scale=w.scale); e.record(); torch.cuda.synchronize()
+    tr = tr.view(-1)[: tr.shape[0] * 64].view(tr.shape[0], 64).cpu().numpy()
+    print(f"{a.config}: kernel {s.elapsed_time(e):.3f} ms (no diag)")
+    tot = tr.astype(np.float64).mean(0) / 1e3
+    for k, nm in NAMES.items():
+        print(f"  {nm:24s} {tot[k]:9.1f} us/CTA")
+    if a.out:
+        np.save(a.out, tr)
+
+if __name__ == "__main__":
+    main()
