@@ -146,13 +146,16 @@ def cpu_oracle_sample(w, csr, Qb, Kb, Vb, target_s: float, seed: int = 7):
     per_row = dt / m
     m = int(min(n, max(m, target_s / per_row)))
     rows = np.sort(rng.choice(n, size=m, replace=False)).astype(np.int32)
+    # a small workload is repeated until ~target_s of CPU work has been timed
+    reps = max(1, int(round(target_s / max(per_row * m, 1e-3)))) if m == n else 1
     t0 = time.perf_counter()
-    ref = oracle.attention(csr.row_ptr, csr.col_idx, Qb, Kb, Vb, scale=w.scale, dtype=w.dtype, rows=rows)
+    for _ in range(reps):
+        ref = oracle.attention(csr.row_ptr, csr.col_idx, Qb, Kb, Vb, scale=w.scale, dtype=w.dtype, rows=rows)
     dt = time.perf_counter() - t0
     # useful flops counted on the deduplicated support (4 * nnz * d * H)
     nnz_s = int(deg[rows].sum())
-    gflops = 4.0 * nnz_s * w.d * w.H / dt / 1e9
-    return gflops, dt, rows, nnz_s, oracle.num_threads(), ref
+    gflops = 4.0 * nnz_s * reps * w.d * w.H / dt / 1e9
+    return gflops, dt, rows, nnz_s, oracle.num_threads(), ref, reps
 
 
 def reference_arm(args, rank: int):
@@ -253,16 +256,17 @@ def main():
     else:
         shard = f3sdist.make_shard(csr.row_ptr, csr.col_idx, rank, world, device=dev,
                                    graph_ptr=csr.graph_ptr if batched else None)
+        spec = shard.spec
         plan = shard.plan
-        row_b, row_e = shard.row_begin, shard.row_end
+        row_b, row_e = spec.row_begin, spec.row_end
         Q = dev_tensor(Qb[row_b:row_e])
-        if batched:
+        if batched:  # whole graphs per rank: own K/V rows, no collective
             K = dev_tensor(Kb[row_b:row_e])
             V = dev_tensor(Vb[row_b:row_e])
             K_sh = V_sh = None
-        else:
-            S = shard.shard_rows
-            lo, hi = min(rank * S, csr.n_cols), min((rank + 1) * S, csr.n_cols)
+        else:  # equal padded K/V shards, replicated by one all-gather each (NCCL over NVLink)
+            S = spec.kv_rows
+            lo, hi = f3sdist.kv_slice(spec, csr.n_cols)
             K_sh = torch.zeros((S, H, d), dtype=tdt, device=dev)
             V_sh = torch.zeros((S, H, d), dtype=tdt, device=dev)
             K_sh[:hi - lo] = dev_tensor(Kb[lo:hi])
@@ -362,7 +366,7 @@ def main():
             Qh = torch.from_numpy(np.ascontiguousarray(Qb[row_b:row_e]).view(np.int16)).pin_memory()
             S = K.shape[0] // world if K_sh is not None else 0
             if K_sh is not None:
-                lo, hi = min(rank * S, csr.n_cols), min((rank + 1) * S, csr.n_cols)
+                lo, hi = f3sdist.kv_slice(spec, csr.n_cols)
                 Kh = torch.zeros((S, H, d), dtype=torch.int16).pin_memory()
                 Vh = torch.zeros((S, H, d), dtype=torch.int16).pin_memory()
                 Kh[:hi - lo] = torch.from_numpy(Kb[lo:hi].view(np.int16))
@@ -403,9 +407,10 @@ def main():
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        gf, secs, rows, nnz_s, cores, ref = cpu_oracle_sample(w, csr, Qb, Kb, Vb, args.cpu_seconds)
+        gf, secs, rows, nnz_s, cores, ref, reps = cpu_oracle_sample(w, csr, Qb, Kb, Vb, args.cpu_seconds)
         cpu = {"value": round(gf, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{len(rows)} seeded random rows of {csr.n_rows} ({nnz_s} of {nnz_total} nnz), {secs:.1f} s fp64"}
+               "sample": f"{len(rows)} seeded random rows of {csr.n_rows} ({nnz_s} of {nnz_total} nnz) x {reps} "
+                         f"pass(es), {secs:.1f} s fp64 on {cores} threads"}
         Og = O[torch.from_numpy(rows).to(dev).long()].double().cpu().numpy()
         diff = Og - ref
         nr = np.linalg.norm(ref)

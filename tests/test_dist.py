@@ -1,0 +1,152 @@
+"""Multi-GPU orchestration (paper_2505_08098_b200.dist): host-side sharding, K/V all-gather layout
+over a world_size-2 gloo process group on CPU, and (GPU) bitwise equality of row-sharded results
+with the single-GPU call."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import f3s_inputs as fi
+from helpers import make_qkv
+
+
+@pytest.fixture(scope="module")
+def dist_mod():
+    from paper_2505_08098_b200 import build
+    build()
+    from paper_2505_08098_b200 import dist
+    return dist
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shard_specs_cover_rows(dist_mod, world):
+    g = fi.chung_lu(5000, 30000, gamma=2.3, max_deg=800, seed=5)
+    specs = [dist_mod.shard_spec(g.row_ptr, g.col_idx, r, world) for r in range(world)]
+    assert specs[0].row_begin == 0 and specs[-1].row_end == g.n_rows
+    for a, b in zip(specs, specs[1:]):
+        assert a.row_end == b.row_begin
+    for s in specs:
+        assert s.row_begin % 16 == 0
+        # the local CSR is exactly the global rows
+        for r in range(s.row_begin, s.row_end, 97):
+            lr = r - s.row_begin
+            assert np.array_equal(s.col_idx[s.row_ptr[lr]:s.row_ptr[lr + 1]], g.col_idx[g.row_ptr[r]:g.row_ptr[r + 1]])
+        lo, hi = dist_mod.kv_slice(s, g.n_rows)
+        assert hi - lo <= s.kv_rows
+    # K/V shards tile [0, n) in rank order
+    assert sum(min(s.kv_rows, max(0, g.n_rows - s.kv_begin)) for s in specs) == g.n_rows
+
+
+def test_batched_specs_are_graph_aligned(dist_mod):
+    g = fi.molecules(400, seed=7)
+    for world in (2, 4):
+        specs = [dist_mod.shard_spec(g.row_ptr, g.col_idx, r, world, g.graph_ptr) for r in range(world)]
+        for s in specs:
+            assert s.row_begin in set(g.graph_ptr.tolist())
+            assert len(s.col_idx) == 0 or (s.col_idx.min() >= 0 and s.col_idx.max() < s.n_cols)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as tdist
+
+    import oracle
+    from paper_2505_08098_b200 import dist as f3sdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = fi.chung_lu(3000, 15000, gamma=2.4, max_deg=500, seed=11)
+        n, H, d = g.n_rows, 2, 64
+        Qb, Kb, Vb = make_qkv(n, n, H, d, "fp16", seed=11)
+        spec = f3sdist.shard_spec(g.row_ptr, g.col_idx, rank, world)
+        lo, hi = f3sdist.kv_slice(spec, n)
+        S = spec.kv_rows
+        f16 = lambda b: torch.from_numpy(np.ascontiguousarray(b).view(np.float16))
+        Ks = torch.zeros((S, H, d), dtype=torch.float16)
+        Vs = torch.zeros((S, H, d), dtype=torch.float16)
+        Ks[:hi - lo] = f16(Kb[lo:hi])
+        Vs[:hi - lo] = f16(Vb[lo:hi])
+        Kf = torch.empty((world * S, H, d), dtype=torch.float16)
+        Vf = torch.empty((world * S, H, d), dtype=torch.float16)
+        f3sdist.allgather_kv(Ks, Vs, Kf, Vf)
+        Kfull = Kf.numpy().view(np.uint16)[:n]
+        Vfull = Vf.numpy().view(np.uint16)[:n]
+        ok_kv = bool(np.array_equal(Kfull, Kb) and np.array_equal(Vfull, Vb))
+        # the rank's rows, computed from its local CSR and the gathered K/V, equal the global rows
+        O_loc = oracle.attention(spec.row_ptr, spec.col_idx, Qb[spec.row_begin:spec.row_end], Kfull, Vfull,
+                                 scale=0.125, n_cols=n)
+        O_ref = oracle.attention(g.row_ptr, g.col_idx, Qb, Kb, Vb, scale=0.125,
+                                 rows=np.arange(spec.row_begin, spec.row_end, dtype=np.int32))
+        q.put((rank, ok_kv, bool(np.array_equal(O_loc, O_ref)), spec.row_begin, spec.row_end))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_gloo_world2_allgather_and_rows(dist_mod, oracle_mod):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    res.sort()
+    assert [r[1] for r in res] == [True, True], "K/V all-gather layout"
+    assert [r[2] for r in res] == [True, True], "sharded rows != global rows"
+    assert res[0][4] == res[1][3]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_row_shards_bitwise_equal_single_gpu(dist_mod, world):
+    import torch
+
+    from helpers import csr_to_dev, to_dev
+    from paper_2505_08098_b200 import f3s
+    g = fi.chung_lu(20000, 150000, gamma=2.2, max_deg=3000, seed=21)
+    n, H, d = g.n_rows, 4, 64
+    Qb, Kb, Vb = make_qkv(n, n, H, d, "fp16", seed=21)
+    Q, K, V = to_dev(Qb, "fp16"), to_dev(Kb, "fp16"), to_dev(Vb, "fp16")
+    rp, ci = csr_to_dev(g)
+    O1 = f3s.attention(f3s.plan(rp, ci, n), Q, K, V, scale=0.125)
+    parts = []
+    for r in range(world):
+        sh = dist_mod.make_shard(g.row_ptr, g.col_idx, r, world)
+        s = sh.spec
+        Ol = dist_mod.attention(sh, Q[s.row_begin:s.row_end].contiguous(), K, V,
+                                torch.empty((s.row_end - s.row_begin, H, d), dtype=torch.float32, device="cuda"),
+                                scale=0.125)
+        parts.append(Ol)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts), O1)
+
+
+@pytest.mark.gpu
+def test_batched_graph_shards(dist_mod, oracle_mod):
+    import torch
+
+    from helpers import assert_close, to_dev
+    g = fi.molecules(600, seed=9)
+    n, H, d = g.n_rows, 8, 64
+    Qb, Kb, Vb = make_qkv(n, n, H, d, "fp16", seed=9)
+    ref = oracle_mod.attention(g.row_ptr, g.col_idx, Qb, Kb, Vb, scale=0.125)
+    outs = []
+    for r in range(4):
+        sh = dist_mod.make_shard(g.row_ptr, g.col_idx, r, 4, graph_ptr=g.graph_ptr)
+        s = sh.spec
+        Ol = dist_mod.attention(sh, to_dev(Qb[s.row_begin:s.row_end], "fp16"), to_dev(Kb[s.row_begin:s.row_end], "fp16"),
+                                to_dev(Vb[s.row_begin:s.row_end], "fp16"),
+                                torch.empty((s.row_end - s.row_begin, H, d), dtype=torch.float32, device="cuda"),
+                                scale=0.125)
+        outs.append(Ol.cpu().numpy())
+    assert_close(np.concatenate(outs), ref)

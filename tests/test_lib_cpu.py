@@ -33,9 +33,12 @@ def test_exports_every_declared_symbol(f3s):
 def test_sass_is_blackwell_native(f3s):
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", f3s.LIB_PATH], capture_output=True, text=True).stdout
-    assert "UTCHMMA" in out          # tcgen05.mma
-    assert "UTMALDG.2D.GATHER4" in out  # TMA tile::gather4
-    assert "LDTM" in out             # tcgen05.ld
+    assert "UTCHMMA" in out          # tcgen05.mma (both contractions)
+    assert "UTMALDG.2D" in out       # TMA tile load (Q tiles)
+    assert "UBLKCP" in out           # cp.async.bulk (column ids / masks into chunk slots)
+    assert "LDGSTS" in out           # cp.async gathers of K/V rows
+    assert "LDTM" in out             # tcgen05.ld (S^T and O^T out of TMEM)
+    assert "HMMA" not in out         # no legacy mma.sync path
 
 
 def test_status_strings(f3s):
