@@ -38,7 +38,7 @@ def test_sass_is_blackwell_native(f3s):
     assert "UBLKCP" in out           # cp.async.bulk (column ids / masks into chunk slots)
     assert "LDGSTS" in out           # cp.async gathers of K/V rows
     assert "LDTM" in out             # tcgen05.ld (S^T and O^T out of TMEM)
-    assert "HMMA" not in out         # no legacy mma.sync path
+    assert re.search(r"\s HMMA", out) is None  # no legacy mma.sync path (UTCHMMA is tcgen05)
 
 
 def test_status_strings(f3s):

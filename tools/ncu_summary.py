@@ -25,7 +25,8 @@ KEYS = {
     "smsp__inst_executed.sum": "instructions",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
 }
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9, "second": 1}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9,
+         "second": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1}
 
 
 def main():
@@ -47,7 +48,7 @@ def main():
                 continue
             out[KEYS[h]] = x * SCALE.get(u, 1) if u in SCALE else x
             if u in SCALE:
-                out[KEYS[h] + "_unit"] = "s" if "second" in u else "bytes"
+                out[KEYS[h] + "_unit"] = "bytes" if "byte" in u else "s"
         if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
             try:
                 stalls[h.replace("smsp__pcsamp_warps_issue_stalled_", "")] = float(v.replace(",", ""))
