@@ -162,7 +162,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
             int32_t* __restrict__ counter, int32_t n_items, int32_t H, int32_t n_rows, int32_t chunk_rows,
             const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float* __restrict__ O, float scale_log2,
-            uint64_t* __restrict__ trace, int32_t trace_chunks) {
+            uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt) {
     using C = Cfg<D>;
     using B = Bars<D>;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -181,6 +181,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     // profile mode (trace_chunks == 0): each role accumulates ns spent per phase in registers
     // and writes trace[cta][32] once at the end (no stores on the hot path)
     const bool prof = kDiag && trace != nullptr && trace_chunks == 0;
+    // expt (f3s_attention_trace only; results are wrong): bit0 no exp work in the softmax,
+    // bit1 no MMA2, bit2 no MMA1, bit3 no K/V gathers.  0 in every real call.
     uint64_t pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint64_t pt0 = prof ? globaltimer_ns() : 0;
     auto lap = [&](int k) {  // charge the time since the previous lap to counter k
@@ -403,7 +405,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const uint32_t vt = sb + C::oRingV + sl.pad + pnl * 1024;
             const uint8_t* kbase = Kg + (int64_t)h * D * 2 + piece * 16;
             const uint8_t* vbase = Vg + (int64_t)h * D * 2 + piece * 16;
-            const int ops = (rows + kRowsPerOp - 1) / kRowsPerOp;
+            const int ops = (expt & 8) ? 0 : (rows + kRowsPerOp - 1) / kRowsPerOp;
 #pragma unroll 2
             for (int t = lw; t < ops; t += C::kLoaderWarps) {
                 const int r = t * kRowsPerOp + rsub;
@@ -446,7 +448,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                             const int b = n1 % C::kSB;
                             const uint32_t kt = sb + C::oRing + sl.ring_off;
                             const uint32_t qt = sb + C::oQ + sl.qslot * C::kQBytes;
-                            if (sl.rows > 0) {
+                            if (sl.rows > 0 && !(expt & 4)) {
 #pragma unroll
                                 for (int kk = 0; kk < D / 16; ++kk) {
                                     const uint64_t a = smem_desc_sw128(kt + (kk >> 2) * 1024 + (kk & 3) * 32, 16, C::kGroupBytes);
@@ -470,7 +472,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         fence_proxy_async_smem();
                         tc_fence_after();
                         const Slot& sl = slots[s];
-                        if (sl.rows > 0) {
+                        if (sl.rows > 0 && !(expt & 2)) {
                             const uint32_t vt = sb + C::oRingV + sl.pad;
                             const uint32_t pt = sb + C::oP + b * C::kPBytes;
                             const int nsteps = (sl.rows + 15) >> 4;
@@ -571,9 +573,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 for (int e = 0; e < 4; ++e) {
                     const int i = 4 * g + e;
                     const float mn = fmaxf(m[i], cm[e]);
-                    av[i] = ex2(m[i] - mn);  // e^{m_o - m_i} (l.18, l.21)
+                    av[i] = (expt & 1) ? 1.f : ex2(m[i] - mn);  // e^{m_o - m_i} (l.18, l.21)
                     m[i] = mn;
-                    pv[i] = ex2(x[i] - mn);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
+                    pv[i] = (expt & 1) ? x[i] : ex2(x[i] - mn);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
                     l[i] = fmaf(l[i], av[i], pv[i]);  // l_o (l.18)
                 }
             }
@@ -790,7 +792,7 @@ f3s_status launch(const AttnArgs& a) {
     kern<<<grid, C::kThreads, C::kSmemBytes, a.stream>>>(
         mq, mk, mv, a.lpt ? p.meta_lpt : p.meta_nat, p.kcols, p.kmasks, counter, n_items, a.heads, p.n_rows,
         chunk_rows, static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.O,
-        a.scale * 1.4426950408889634f, a.trace, a.trace_chunks);
+        a.scale * 1.4426950408889634f, a.trace, a.trace_chunks, a.expt);
     count_launch();
     F3S_CUDA_TRY(cudaGetLastError());
     return F3S_OK;

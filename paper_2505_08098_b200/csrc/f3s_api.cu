@@ -50,8 +50,9 @@ static f3s_status run_attention(f3s_plan_t plan, const void* Q, const void* K, c
     if (st != F3S_OK) return st;
     AttnArgs a{reinterpret_cast<const Plan*>(plan), Q, K, V, O, scale, heads, d, dtype,
                variant != F3S_VARIANT_NO_REORDER, stream};
-    a.trace = trace;
-    a.trace_chunks = trace_chunks;
+    a.trace = trace_chunks < 0 ? nullptr : trace;
+    a.trace_chunks = trace_chunks < 0 ? 0 : trace_chunks;
+    a.expt = trace_chunks < 0 ? -trace_chunks : 0;
     a.grid_override = grid;
     if (a.plan->n_rows == 0) return F3S_OK;
     switch (variant) {
@@ -168,7 +169,7 @@ f3s_status f3s_attention_ex(f3s_plan_t plan, const void* Q, const void* K, const
 f3s_status f3s_attention_trace(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
                                int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, uint64_t* trace,
                                int32_t trace_chunks, int32_t grid, cudaStream_t stream) {
-    if (trace_chunks < 0 || grid < 0) { set_error("bad trace arguments"); return F3S_ERR_INVALID_VALUE; }
+    if (grid < 0) { set_error("bad trace arguments"); return F3S_ERR_INVALID_VALUE; }  // trace_chunks < 0: experiments
     try {
         return run_attention(plan, Q, K, V, O, scale, heads, d, dtype, variant, stream, trace, trace_chunks, grid);
     } catch (...) {

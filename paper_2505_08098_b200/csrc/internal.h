@@ -62,6 +62,7 @@ struct AttnArgs {
     uint64_t* trace = nullptr;  // F3S_TRACE buffer [grid][trace_chunks][8] (diagnostics)
     int32_t trace_chunks = 0;
     int32_t grid_override = 0;
+    int32_t expt = 0;           // sensitivity experiments (diagnostics only)
 };
 
 f3s_status launch_attention_sm100(const AttnArgs& a);

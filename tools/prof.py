@@ -27,16 +27,20 @@ def main():
     for _ in range(3):
         f3s.attention(p, Q, K, V, O, scale=w.scale)
     tr = f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=0)
-    tr = tr[: tr.shape[0] // 2 if False else tr.shape[0]]
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(); f3s.attention(p, Q, K, V, O, scale=w.scale); e.record(); torch.cuda.synchronize()
     tr = tr.view(-1)[: tr.shape[0] * 64].view(tr.shape[0], 64).cpu().numpy()
+    tr = tr[tr.any(1)]
     print(f"{a.config}: kernel {s.elapsed_time(e):.3f} ms (no diag)")
     tot = tr.astype(np.float64).mean(0) / 1e3
     for k, nm in NAMES.items():
         print(f"  {nm:24s} {tot[k]:9.1f} us/CTA")
     if a.out:
         np.save(a.out, tr)
+    for ex, nm in [(1, "no softmax exp"), (2, "no MMA2"), (4, "no MMA1"), (6, "no MMAs"), (8, "no gathers"), (9, "no gathers+exp"), (14, "no gathers, no MMAs")]:
+        f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=-ex)
+        s.record(); f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=-ex); e.record(); torch.cuda.synchronize()
+        print(f"  experiment {ex:2d} ({nm:22s}): {s.elapsed_time(e):.3f} ms")
 
 if __name__ == "__main__":
     main()
