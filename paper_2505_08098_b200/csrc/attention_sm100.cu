@@ -71,8 +71,12 @@ struct Cfg {
     static constexpr int oTmem = oBar + kNumBars * 8;
     static constexpr int kSmemBytes = oTmem + 16;
     static constexpr int kCtasPerSm = 1;
-    static constexpr int kLoaderWarps = 8;           // cp.async gather warps (memory-level parallelism)
-    static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps, kCorr0 = kSoftmax0 + 4;
+    static constexpr int kLoaderWarps = 5;           // cp.async gather warps (20 warps in all: 5 per SMSP keeps 96 registers)
+    // two softmax warpgroups take alternate work items: one warpgroup's chunk is a long chain of
+    // dependent short-latency steps (measured: issue-active ~17% of its cycles), so a second
+    // independent chain doubles the softmax throughput
+    static constexpr int kSoftmaxWGs = 2;
+    static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps, kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
     static constexpr int kThreads = 32 * (kCorr0 + 4);  // control, MMA, index, loaders, softmax, correction
     static constexpr int kBatch = 8;                 // items fetched per queue round trip
     static_assert(kRingK >= (kMaxRows / 8) * kGroupBytes && kRingV >= (kMaxRows / 8) * kGroupBytes,
@@ -179,22 +183,23 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             trace[((size_t)blockIdx.x * trace_chunks + c) * 8 + ev] = globaltimer_ns();
     };
     // profile mode (trace_chunks == 0): each role accumulates ns spent per phase in registers
-    // and writes trace[cta][32] once at the end (no stores on the hot path)
+    // (SM cycles) and writes trace[cta][64] once at the end (no stores on the hot path)
     const bool prof = kDiag && trace != nullptr && trace_chunks == 0;
     // expt (f3s_attention_trace only; results are wrong): bit0 no exp work in the softmax,
-    // bit1 no MMA2, bit2 no MMA1, bit3 no K/V gathers.  0 in every real call.
-    uint64_t pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint64_t pt0 = prof ? globaltimer_ns() : 0;
-    auto lap = [&](int k) {  // charge the time since the previous lap to counter k
+    // bit1 no MMA2, bit2 no MMA1, bit3 no K/V gathers, bit4 consumer-side proxy fence before the
+    // MMAs, bit5 no S load / row max in the softmax, bit6 no O stores.  0 in every real call.
+    uint32_t pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t pt0 = prof ? (uint32_t)clock() : 0;  // SM cycles (cheap to read, unlike globaltimer)
+    auto lap = [&](int k) {  // charge the cycles since the previous lap to counter k
         if (prof) {
-            const uint64_t t = globaltimer_ns();
+            const uint32_t t = (uint32_t)clock();
             pc[k] += t - pt0;
             pt0 = t;
         }
     };
     auto prof_flush = [&](int base) {  // base in units of roles: 8 counters each
         if (prof)
-            for (int k = 0; k < 8; ++k) trace[(size_t)blockIdx.x * 64 + base * 8 / 6 + k] = pc[k];
+            for (int k = 0; k < 8; ++k) trace[(size_t)blockIdx.x * 64 + base * 8 / 6 + k] = (uint64_t)pc[k];
     };
 
     // ---- setup -------------------------------------------------------------------------------
@@ -423,43 +428,53 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             ++seq;
         }
     } else if (warp == 1) {
-        // ===== MMA issuer (one thread, event loop) ====================================================
-        // MMA1(c) as soon as K_c (and Q) landed and S buffer c&1 is free (MMA2(c-2) issued);
-        // MMA2(c) as soon as P_c is written and V_c landed.  Both in chunk order.
-        if (lane == 0) {
+        // ===== MMA issuer (whole warp, one elected lane issues; event loop) ===========================
+        // MMA1(c) as soon as K_c (and Q) landed and one of the kSB S buffers is free;
+        // MMA2(c) as soon as P_c is written and V_c landed.  Both in chunk order.  All lanes run
+        // the loop on warp-uniform values so the tcgen05 instructions are issued without a
+        // lane-divergent waterfall (sm100.cuh: mma_f16_ss_warp).  The cp.async-written K/V tiles
+        // need no proxy fence here (the mbarrier completion of cp.async orders them, as in
+        // CUTLASS's SM100 cp.async mainloop); P is fenced by its writers before pfull.
+        {
             constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
             constexpr uint32_t idesc1 = idesc_f16(fmt, 0, 0, 128, 16);  // S^T = K_c . Q_w^T
             constexpr uint32_t idesc2 = idesc_f16(fmt, 1, 1, D, 16);    // O^T = V_c^T . P^T (A, B MN-major)
+            // descriptor templates at address 0; adding (addr >> 4) sets the start address
+            // (shared addresses < 256 KB fit the 14-bit field, so the add never carries)
+            const uint64_t dK = smem_desc_sw128(0, 16, C::kGroupBytes);
+            const uint64_t dQ = smem_desc_sw128(0, 16, 1024);
+            const uint64_t dV = smem_desc_sw128(0, 1024, C::kGroupBytes);
+            const uint64_t dP = smem_desc_sw32(0, 4096, 256);
+            const bool fence_k = (expt & 16) != 0;  // diagnostics: consumer-side proxy fence
             int32_t n1 = 0, n2 = 0, stop_at = 0x7FFFFFFF;
-            const uint64_t t0 = globaltimer_ns();
             uint64_t idle_since = 0;
+            uint32_t idle_polls = 0;
             while (n2 < stop_at) {
                 bool progressed = false;
                 if (n1 < stop_at && n1 < n2 + C::kSB) {
                     const int s = n1 % C::kNS;
                     if (mbar_test(bar(B::kfull(s)), (n1 / C::kNS) & 1)) {
                         const Slot& sl = slots[s];
-                        if (sl.rows < 0) {
+                        const int rows = sl.rows, flags = sl.flags, qslot = sl.qslot, roff = sl.ring_off;
+                        if (rows < 0) {
                             stop_at = n1;
                             progressed = true;
-                        } else if (!(sl.flags & 1) || mbar_test(bar(B::qfull(sl.qslot)), (sl.flags >> 2) & 1)) {
-                            fence_proxy_async_smem();  // cp.async (generic proxy) data -> tensor core
+                        } else if (!(flags & 1) || mbar_test(bar(B::qfull(qslot)), (flags >> 2) & 1)) {
+                            if (fence_k) fence_proxy_async_smem();
                             tc_fence_after();
                             const int b = n1 % C::kSB;
-                            const uint32_t kt = sb + C::oRing + sl.ring_off;
-                            const uint32_t qt = sb + C::oQ + sl.qslot * C::kQBytes;
-                            if (sl.rows > 0 && !(expt & 4)) {
+                            const uint64_t a0 = dK + ((sb + C::oRing + roff) >> 4);
+                            const uint64_t b0 = dQ + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
+                            if (rows > 0 && !(expt & 4)) {
 #pragma unroll
-                                for (int kk = 0; kk < D / 16; ++kk) {
-                                    const uint64_t a = smem_desc_sw128(kt + (kk >> 2) * 1024 + (kk & 3) * 32, 16, C::kGroupBytes);
-                                    const uint64_t bq = smem_desc_sw128(qt + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-                                    mma_f16_ss(tmem + b * 16, a, bq, idesc1, kk > 0 ? 1u : 0u);
-                                }
+                                for (int kk = 0; kk < D / 16; ++kk)
+                                    mma_f16_ss_warp(tmem + b * 16, a0 + (((kk >> 2) * 1024 + (kk & 3) * 32) >> 4),
+                                                    b0 + (((kk >> 2) * 2048 + (kk & 3) * 32) >> 4), idesc1, kk > 0 ? 1u : 0u);
                             }
-                            mma_commit(bar(B::sfull(b)));
-                            mma_commit(bar(B::kempty(s)));
-                            if (sl.flags & 2) mma_commit(bar(B::qempty(sl.qslot)));
-                            stamp(n1, 2);
+                            mma_commit_warp(bar(B::sfull(b)));
+                            mma_commit_warp(bar(B::kempty(s)));
+                            if (flags & 2) mma_commit_warp(bar(B::qempty(qslot)));
+                            if (lane == 0) stamp(n1, 2);
                             lap(1);
                             ++n1;
                             progressed = true;
@@ -469,22 +484,20 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 if (n2 < n1) {
                     const int s = n2 % C::kNS, b = n2 % C::kSB;
                     if (mbar_test(bar(B::pfull(b)), (n2 / C::kSB) & 1) && mbar_test(bar(B::vfull(s)), (n2 / C::kNS) & 1)) {
-                        fence_proxy_async_smem();
+                        if (fence_k) fence_proxy_async_smem();
                         tc_fence_after();
-                        const Slot& sl = slots[s];
-                        if (sl.rows > 0 && !(expt & 2)) {
-                            const uint32_t vt = sb + C::oRingV + sl.pad;
-                            const uint32_t pt = sb + C::oP + b * C::kPBytes;
-                            const int nsteps = (sl.rows + 15) >> 4;
-                            for (int st = 0; st < nsteps; ++st) {
-                                const uint64_t a = smem_desc_sw128(vt + st * 2 * C::kGroupBytes, 1024, C::kGroupBytes);
-                                const uint64_t bp = smem_desc_sw32(pt + st * 512, 4096, 256);
-                                mma_f16_ss(tmem + 16 * C::kSB + b * 16, a, bp, idesc2, st > 0 ? 1u : 0u);
-                            }
+                        const int rows = slots[s].rows;
+                        if (rows > 0 && !(expt & 2)) {
+                            const uint64_t a0 = dV + ((sb + C::oRingV + slots[s].pad) >> 4);
+                            const uint64_t b0 = dP + ((sb + C::oP + b * C::kPBytes) >> 4);
+                            const int nsteps = (rows + 15) >> 4;
+                            for (int st = 0; st < nsteps; ++st)
+                                mma_f16_ss_warp(tmem + 16 * C::kSB + b * 16, a0 + ((st * 2 * C::kGroupBytes) >> 4),
+                                                b0 + ((st * 512) >> 4), idesc2, st > 0 ? 1u : 0u);
                         }
-                        mma_commit(bar(B::ofull(b)));
-                        mma_commit(bar(B::empty(s)));
-                        stamp(n2, 5);
+                        mma_commit_warp(bar(B::ofull(b)));
+                        mma_commit_warp(bar(B::empty(s)));
+                        if (lane == 0) stamp(n2, 5);
                         lap(2);
                         ++n2;
                         progressed = true;
@@ -493,21 +506,24 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 // watchdog for the polling loop (the blocking waits have their own)
                 if (progressed) {
                     idle_since = 0;
+                    idle_polls = 0;
                 } else {
                     lap(n1 < stop_at && n1 >= n2 + C::kSB ? 3 : (n2 < n1 ? 4 : 0));
-                    const uint64_t now = globaltimer_ns();
-                    if (idle_since == 0) idle_since = now;
-                    else if (now - idle_since > 20000000000ull) __trap();
+                    if ((++idle_polls & 1023) == 0) {  // read the (slow) global timer rarely
+                        const uint64_t now = globaltimer_ns();
+                        if (idle_since == 0) idle_since = now;
+                        else if (now - idle_since > 20000000000ull) __trap();
+                    }
                 }
             }
-            (void)t0;
-            prof_flush(12);
+            if (lane == 0) prof_flush(12);
         }
         __syncwarp();
     } else if (warp < C::kCorr0) {
         // ===== softmax warpgroup =====================================================
         const int q = warp & 3;          // TMEM lane quadrant this warp may access
         const int p = 32 * q + lane;     // compacted column of the chunk (S^T lane)
+        const int wg = (warp - C::kSoftmax0) >> 2;  // this warpgroup owns the items with index % 2 == wg
         const uint32_t tl = (uint32_t)(32 * q) << 16;
         float* red = reinterpret_cast<float*>(smem + C::oRed);
         float* lred = reinterpret_cast<float*>(smem + C::oLred);
@@ -518,7 +534,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         float m[16], l[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) { m[i] = kMFloor; l[i] = 0.f; }
-        int32_t seq = 0, item = 0;
+        int32_t seq = 0, item = -1;  // item: index of the current chunk's work item in queue order
         for (;;) {
             const int s = seq % C::kNS;
             const int b = seq % C::kSB;
@@ -527,17 +543,20 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (p == 0) lap(0);
             const Slot& sl = slots[s];
             const int rows = sl.rows;
-            if (rows < 0) {  // forward the stop to the correction group
-                mbar_wait(bar(B::pempty(b)), bph ^ 1);
-                if (p == 0) corr[b].rows = -1;
-                mbar_arrive(bar(B::pfull(b)));
-                if (p == 0) prof_flush(18);
+            if (rows < 0) {  // warpgroup 0 forwards the stop to the correction group
+                if (wg == 0) {
+                    mbar_wait(bar(B::pempty(b)), bph ^ 1);
+                    if (p == 0) corr[b].rows = -1;
+                    mbar_arrive(bar(B::pfull(b)));
+                    if (p == 0) prof_flush(18);
+                }
                 break;
             }
             const int flags = sl.flags;
-            if (flags & 1) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) { m[i] = kMFloor; l[i] = 0.f; }
+            if (flags & 1) ++item;
+            if ((item & 1) != wg) {  // the other warpgroup's item
+                ++seq;
+                continue;
             }
             const uint32_t mask = p < rows ? (uint32_t)sl.masks[p] : 0u;
             const int rw = sl.rw, hd = sl.head;
@@ -546,14 +565,19 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             uint64_t t_s = 0;
             if (kDiag && p == 0) { t_s = globaltimer_ns(); lap(1); }
             float x[16];
-            tmem_ld_32x32b_x16(tmem + tl + b * 16, x);
+            if (expt & 32) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) x[i] = 0.f;
+            } else {
+                tmem_ld_32x32b_x16(tmem + tl + b * 16, x);
+            }
 #pragma unroll
             for (int i = 0; i < 16; ++i) x[i] = ((mask >> i) & 1u) ? x[i] * scale_log2 : -INFINITY;  // Alg.1 l.14
             // chunk row max (Alg.1 l.16): warp butterfly + 4-warp combine
-            const float rm = rowreduce16(x, lane, OpMax());
+            const float rm = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
             if (!(lane & 1)) red[(b * 4 + q) * 16 + ((lane >> 1) & 15)] = rm;
             if (p == 0) lap(2);
-            named_bar_sync(1, 128);
+            named_bar_sync(1 + wg, 128);
             // P_b / corr_b are free once the correction group consumed chunk seq - kSB
             mbar_wait(bar(B::pempty(b)), bph ^ 1);
             if (p == 0) lap(3);
@@ -564,18 +588,30 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             uint4* prow = reinterpret_cast<uint4*>(smem + C::oP + b * C::kPBytes + (p >> 3) * 256 + (p & 7) * 32);
             const int sw = (p >> 2) & 1;
             float av[16], pv[16];
+            float cm[16];  // chunk row max (4-warp combine)
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
                 const float4 w0 = r4[g], w1 = r4[4 + g], w2 = r4[8 + g], w3 = r4[12 + g];
-                const float cm[4] = {fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x)), fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y)),
-                                     fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z)), fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w))};
+                cm[4 * g] = fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x));
+                cm[4 * g + 1] = fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y));
+                cm[4 * g + 2] = fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z));
+                cm[4 * g + 3] = fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w));
+            }
+            if (flags & 1) {  // item's first chunk: m_o = floor, l_o = 0, nothing to rescale (alpha = 0)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int i = 4 * g + e;
-                    const float mn = fmaxf(m[i], cm[e]);
+                for (int i = 0; i < 16; ++i) {
+                    m[i] = fmaxf(kMFloor, cm[i]);
+                    pv[i] = (expt & 1) ? x[i] : ex2(x[i] - m[i]);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
+                    l[i] = pv[i];
+                    av[i] = 0.f;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float mn = fmaxf(m[i], cm[i]);
                     av[i] = (expt & 1) ? 1.f : ex2(m[i] - mn);  // e^{m_o - m_i} (l.18, l.21)
                     m[i] = mn;
-                    pv[i] = (expt & 1) ? x[i] : ex2(x[i] - mn);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
+                    pv[i] = (expt & 1) ? x[i] : ex2(x[i] - mn);
                     l[i] = fmaf(l[i], av[i], pv[i]);  // l_o (l.18)
                 }
             }
@@ -613,7 +649,6 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 if (!(lane & 1)) lred[(ib * 4 + q) * 16 + ((lane >> 1) & 15)] = rl;
                 mbar_arrive(bar(B::lfull(ib)));
                 if (p == 0) lap(5);
-                ++item;
             }
             ++seq;
         }
@@ -690,7 +725,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const int nvalid = min(16, n_rows - 16 * rw);  // ragged last window (reading c14)
                 const bool has = D == 128 || lane < 16;
                 const int f = D == 128 ? 32 * q + lane : 16 * q + lane;  // O^T lane -> feature (M = 64 layout)
-                if (has) {
+                if (has && !(expt & 64)) {
                     const int64_t ld = (int64_t)H * D;
                     float* out = O + (int64_t)16 * rw * ld + (int64_t)hd * D + f;
 #pragma unroll

@@ -1,4 +1,5 @@
-"""F3S_TRACE profile mode: per-CTA ns spent per pipeline phase, summed per role."""
+"""F3S_TRACE profile mode: per-CTA SM cycles spent per pipeline phase, summed per role (printed as us at
+the measured SM clock)."""
 import argparse, os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -26,18 +27,21 @@ def main():
     O = torch.empty(Q.shape, dtype=torch.float32, device="cuda")
     for _ in range(3):
         f3s.attention(p, Q, K, V, O, scale=w.scale)
-    tr = f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=0)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tr = f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=0)
+    s.record(); tr = f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=0); e.record(); torch.cuda.synchronize()
+    print(f"{a.config}: profile-mode kernel {s.elapsed_time(e):.3f} ms")
     s.record(); f3s.attention(p, Q, K, V, O, scale=w.scale); e.record(); torch.cuda.synchronize()
     tr = tr.view(-1)[: tr.shape[0] * 64].view(tr.shape[0], 64).cpu().numpy()
     tr = tr[tr.any(1)]
     print(f"{a.config}: kernel {s.elapsed_time(e):.3f} ms (no diag)")
-    tot = tr.astype(np.float64).mean(0) / 1e3
+    ghz = float(os.environ.get("F3S_SM_GHZ", "1.92"))
+    tot = tr.astype(np.float64).mean(0) / 1e3 / ghz
     for k, nm in NAMES.items():
         print(f"  {nm:24s} {tot[k]:9.1f} us/CTA")
     if a.out:
         np.save(a.out, tr)
-    for ex, nm in [(1, "no softmax exp"), (2, "no MMA2"), (4, "no MMA1"), (6, "no MMAs"), (8, "no gathers"), (9, "no gathers+exp"), (14, "no gathers, no MMAs")]:
+    for ex, nm in [(1, "no softmax exp"), (2, "no MMA2"), (4, "no MMA1"), (6, "no MMAs"), (8, "no gathers"), (9, "no gathers+exp"), (14, "no gathers, no MMAs"), (16, "consumer proxy fence"), (32, "no S ld/max"), (33, "no S ld/max/exp"), (64, "no O stores"), (46, "skeleton: 2+4+8+32"), (110, "skeleton+no O stores")]:
         f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=-ex)
         s.record(); f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=-ex); e.record(); torch.cuda.synchronize()
         print(f"  experiment {ex:2d} ({nm:22s}): {s.elapsed_time(e):.3f} ms")
