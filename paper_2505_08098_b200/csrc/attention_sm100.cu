@@ -51,22 +51,26 @@ struct Cfg {
     static constexpr int kRingK = D == 128 ? 64 * 1024 : 64 * 1024;
     static constexpr int kRingV = D == 128 ? 80 * 1024 : 88 * 1024;
     static constexpr int kRingBytes = kRingK + kRingV;
-    static constexpr int kNS = 24;                   // chunk slots (ids, masks, descriptor, barriers)
-    static constexpr int kNQ = D == 128 ? 8 : 16;    // Q tile slots (items in flight per CTA)
+    static constexpr int kNS = D == 128 ? 20 : 22;   // chunk slots (ids, masks, descriptor, barriers)
+    static constexpr int kNQ = D == 128 ? 6 : 12;    // Q tile slots (items in flight per CTA)
     static constexpr int kQBytes = 16 * D * 2;
     static constexpr int kPBytes = 16 * kMaxRows * 2;
     static constexpr int kSB = 4;                    // S/P/O buffers in flight (TMEM and SMEM)
+    static constexpr int kNO = 2;                    // O staging tiles (16 x D fp32) for the TMA store
+    static constexpr int kOBytes = 16 * D * 4;
     static constexpr int kSlotBytes = 32 + 128 * 4 + 128 * 2;  // sizeof(Slot)
     static constexpr int oRing = 0;                  // K ring, then V ring
     static constexpr int oRingV = kRingK;
     static constexpr int oQ = oRing + kRingBytes;
     static constexpr int oP = oQ + kNQ * kQBytes;
-    static constexpr int oSlot = oP + kSB * kPBytes;
+    static constexpr int oOst = oP + kSB * kPBytes;
+    static constexpr int oSlot = oOst + kNO * kOBytes;
     static constexpr int oRed = oSlot + kNS * kSlotBytes;  // float [kSB][4][16] chunk row-max partials
-    static constexpr int oLred = oRed + kSB * 4 * 16 * 4;  // float [2][4][16] row-sum partials per item
-    static constexpr int oCorr = oLred + 2 * 4 * 16 * 4;   // CorrSlot [kSB]
+    static constexpr int kLB = 8;                    // row-sum hand-off buffers (items in flight, even)
+    static constexpr int oLred = oRed + kSB * 4 * 16 * 4;  // float [kLB][4][16] row-sum partials per item
+    static constexpr int oCorr = oLred + kLB * 4 * 16 * 4; // CorrSlot [kSB]
     static constexpr int oReg = oCorr + kSB * 96;          // int2 [2][kNS] ring regions (K, V)
-    static constexpr int kNumBars = 6 * kNS + 2 * kNQ + 4 * kSB + 4;
+    static constexpr int kNumBars = 6 * kNS + 2 * kNQ + 4 * kSB + 2 * kLB;
     static constexpr int oBar = oReg + 2 * kNS * 8;
     static constexpr int oTmem = oBar + kNumBars * 8;
     static constexpr int kSmemBytes = oTmem + 16;
@@ -101,9 +105,9 @@ template <int D> struct Bars {
     __host__ __device__ static constexpr int ofull(int b) { return kB0 + 2 * C::kSB + b; }
     __host__ __device__ static constexpr int pempty(int b) { return kB0 + 3 * C::kSB + b; }
     __host__ __device__ static constexpr int lfull(int b) { return kB0 + 4 * C::kSB + b; }
-    __host__ __device__ static constexpr int lempty(int b) { return kB0 + 4 * C::kSB + 2 + b; }
-    __host__ __device__ static constexpr int rfull(int s) { return kB0 + 4 * C::kSB + 4 + s; }
-    __host__ __device__ static constexpr int kempty(int s) { return kB0 + 4 * C::kSB + 4 + C::kNS + s; }
+    __host__ __device__ static constexpr int lempty(int b) { return kB0 + 4 * C::kSB + C::kLB + b; }
+    __host__ __device__ static constexpr int rfull(int s) { return kB0 + 4 * C::kSB + 2 * C::kLB + s; }
+    __host__ __device__ static constexpr int kempty(int s) { return kB0 + 4 * C::kSB + 2 * C::kLB + C::kNS + s; }
 };
 
 // One chunk of one work item: written by the index warp (ids/masks by cp.async.bulk), the
@@ -162,11 +166,11 @@ template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, f
 template <int D, typename T, bool kDiag>
 __global__ void __launch_bounds__(Cfg<D>::kThreads, Cfg<D>::kCtasPerSm)
 k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-            const __grid_constant__ CUtensorMap tmV, const int4* __restrict__ meta,
+            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const int4* __restrict__ meta,
             const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
             int32_t* __restrict__ counter, int32_t n_items, int32_t H, int32_t n_rows, int32_t chunk_rows,
             const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float* __restrict__ O, float scale_log2,
-            uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt) {
+            uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt, uint32_t mma_sleep_ns) {
     using C = Cfg<D>;
     using B = Bars<D>;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -226,7 +230,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             mbar_init(bar(B::ofull(b)), 1);
             mbar_init(bar(B::pempty(b)), 128);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < C::kLB; ++b) {
             mbar_init(bar(B::lfull(b)), 128);
             mbar_init(bar(B::lempty(b)), 128);
         }
@@ -236,6 +240,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         tma_prefetch_desc(&tmQ);
         tma_prefetch_desc(&tmK);
         tma_prefetch_desc(&tmV);
+        tma_prefetch_desc(&tmO);
     }
     if (warp == 1) {
         tmem_alloc<32 * C::kSB>(sb + C::oTmem);
@@ -509,6 +514,13 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     idle_polls = 0;
                 } else {
                     lap(n1 < stop_at && n1 >= n2 + C::kSB ? 3 : (n2 < n1 ? 4 : 0));
+                    // sleep on the event most likely next (P of the oldest chunk, else the next K
+                    // tile) rather than spin: the spinning warp would take issue slots from the
+                    // softmax warps of its SM sub-partition
+                    if (mma_sleep_ns > 0) {
+                        if (n2 < n1) mbar_try_wait_hint(bar(B::pfull(n2 % C::kSB)), (n2 / C::kSB) & 1, mma_sleep_ns);
+                        else if (n1 < stop_at) mbar_try_wait_hint(bar(B::kfull(n1 % C::kNS)), (n1 / C::kNS) & 1, mma_sleep_ns);
+                    }
                     if ((++idle_polls & 1023) == 0) {  // read the (slow) global timer rarely
                         const uint64_t now = globaltimer_ns();
                         if (idle_since == 0) idle_since = now;
@@ -643,9 +655,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (p == 0) lap(4);
             if (flags & 2) {
                 // l_o partial sums of the item (l.18) -> correction group
-                const int ib = item & 1;
+                const int ib = item % C::kLB;
                 const float rl = rowreduce16(l, lane, OpAdd());
-                mbar_wait(bar(B::lempty(ib)), ((item >> 1) & 1) ^ 1);
+                mbar_wait(bar(B::lempty(ib)), ((item / C::kLB) & 1) ^ 1);
                 if (!(lane & 1)) lred[(ib * 4 + q) * 16 + ((lane >> 1) & 15)] = rl;
                 mbar_arrive(bar(B::lfull(ib)));
                 if (p == 0) lap(5);
@@ -708,8 +720,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (lead) lap(2);
             if (flags & 2) {
                 // O_i = diag(l_o)^-1 O_i (l.24)
-                const int ib = item & 1;
-                mbar_wait(bar(B::lfull(ib)), (item >> 1) & 1);
+                const int ib = item % C::kLB;
+                mbar_wait(bar(B::lfull(ib)), (item / C::kLB) & 1);
                 if (lead) lap(3);
                 const float4* l4 = reinterpret_cast<const float4*>(lred + ib * 64);
                 float inv[16];
@@ -722,15 +734,23 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     for (int u = 0; u < 4; ++u) inv[4 * g + u] = lt[u] > 0.f ? rcp_approx(lt[u]) : 0.f;  // empty row -> 0
                 }
                 mbar_arrive(bar(B::lempty(ib)));
-                const int nvalid = min(16, n_rows - 16 * rw);  // ragged last window (reading c14)
+                // O tile [16 x D] fp32 staged in shared memory and written by one TMA store (rows
+                // past n_rows of a ragged last window are clipped by the tensor map, reading c14)
+                const int ob = item % C::kNO;
+                float* ost = reinterpret_cast<float*>(smem + C::oOst + ob * C::kOBytes);
+                if (threadIdx.x == 32 * C::kCorr0) bulk_wait_group_read<C::kNO - 1>();  // staging tile ob free
+                named_bar_sync(3, 128);
                 const bool has = D == 128 || lane < 16;
                 const int f = D == 128 ? 32 * q + lane : 16 * q + lane;  // O^T lane -> feature (M = 64 layout)
-                if (has && !(expt & 64)) {
-                    const int64_t ld = (int64_t)H * D;
-                    float* out = O + (int64_t)16 * rw * ld + (int64_t)hd * D + f;
+                if (has) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (i < nvalid) out[(int64_t)i * ld] = oacc[i] * inv[i];
+                    for (int i = 0; i < 16; ++i) ost[i * D + f] = oacc[i] * inv[i];
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(3, 128);
+                if (threadIdx.x == 32 * C::kCorr0) {
+                    if (!(expt & 64)) tma_store_2d(&tmO, sb + C::oOst + ob * C::kOBytes, hd * D, 16 * rw);
+                    bulk_commit_group();
                 }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) oacc[i] = 0.f;
@@ -739,6 +759,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             ++seq;
         }
+        if (threadIdx.x == 32 * C::kCorr0) bulk_wait_group<0>();
     }
     tc_fence_before();
     __syncthreads();
@@ -766,21 +787,28 @@ EncodeTiledFn get_encode() {
     return fn;
 }
 
-f3s_status make_map(CUtensorMap* map, const void* base, f3s_dtype dtype, int64_t inner, int64_t rows, uint32_t box_rows) {
+// 2-D tensor map over a row-major [rows, inner] matrix; 16-bit elements use 64-element (128-byte)
+// boxes with the 128-byte swizzle of the UMMA tiles, fp32 (O) a dense unswizzled box_inner-wide box
+f3s_status make_map(CUtensorMap* map, const void* base, CUtensorMapDataType type, int64_t inner, int64_t rows,
+                    uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz) {
     EncodeTiledFn enc = get_encode();
     if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return F3S_ERR_CUDA; }
+    const int esz = type == CU_TENSOR_MAP_DATA_TYPE_FLOAT32 ? 4 : 2;
     cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)inner * 2};
-    cuuint32_t box[2] = {64, box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)inner * esz};
+    cuuint32_t box[2] = {box_inner, box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, dtype == F3S_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
-                     const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(map, type, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
         return F3S_ERR_CUDA;
     }
     return F3S_OK;
+}
+f3s_status make_map(CUtensorMap* map, const void* base, f3s_dtype dtype, int64_t inner, int64_t rows, uint32_t box_rows) {
+    return make_map(map, base, dtype == F3S_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                    inner, rows, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 std::atomic<uint32_t> g_call{0};
@@ -794,11 +822,14 @@ f3s_status launch(const AttnArgs& a) {
         F3S_CUDA_TRY(cudaMemsetAsync(a.O, 0, (size_t)out_bytes, a.stream));
         return F3S_OK;
     }
-    CUtensorMap mq, mk, mv;
+    CUtensorMap mq, mk, mv, mo;
     f3s_status st;
     if ((st = make_map(&mq, a.Q, a.dtype, (int64_t)a.heads * D, p.n_rows, 16)) != F3S_OK) return st;
     if ((st = make_map(&mk, a.K, a.dtype, (int64_t)a.heads * D, p.n_cols, 1)) != F3S_OK) return st;
     if ((st = make_map(&mv, a.V, a.dtype, (int64_t)a.heads * D, p.n_cols, 1)) != F3S_OK) return st;
+    if ((st = make_map(&mo, a.O, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (int64_t)a.heads * D, p.n_rows, D, 16,
+                       CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK)
+        return st;
 
     static int num_sms[64] = {0};
     const int dev = p.device;
@@ -821,13 +852,14 @@ f3s_status launch(const AttnArgs& a) {
     // compacted columns per chunk: smaller chunks keep more tiles in flight in the ring
     int chunk_rows = 128;
     if (const char* env = getenv("F3S_CHUNK_ROWS")) chunk_rows = std::max(16, std::min(128, atoi(env) / 16 * 16));
+    static uint32_t mma_sleep_ns = getenv("F3S_MMA_SLEEP") ? (uint32_t)atoi(getenv("F3S_MMA_SLEEP")) : 0u;
     int32_t* counter = p.counters + (g_call.fetch_add(1) % kNumCounterSlots);
     F3S_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int32_t), a.stream));
     auto kern = a.trace ? k_f3s_sm100<D, T, true> : k_f3s_sm100<D, T, false>;
     kern<<<grid, C::kThreads, C::kSmemBytes, a.stream>>>(
-        mq, mk, mv, a.lpt ? p.meta_lpt : p.meta_nat, p.kcols, p.kmasks, counter, n_items, a.heads, p.n_rows,
+        mq, mk, mv, mo, a.lpt ? p.meta_lpt : p.meta_nat, p.kcols, p.kmasks, counter, n_items, a.heads, p.n_rows,
         chunk_rows, static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.O,
-        a.scale * 1.4426950408889634f, a.trace, a.trace_chunks, a.expt);
+        a.scale * 1.4426950408889634f, a.trace, a.trace_chunks, a.expt, mma_sleep_ns);
     count_launch();
     F3S_CUDA_TRY(cudaGetLastError());
     return F3S_OK;

@@ -35,6 +35,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint (ns): the thread sleeps until the phase completes or the
+// hint expires, instead of spinning on the issue slots its SM sub-partition shares
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(ns)
+        : "memory");
+    return ok != 0;
+}
 // non-blocking probe (never suspends the thread): for polling several barriers in one loop
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
     uint32_t ok;
@@ -51,11 +62,15 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     return t;
 }
 // Blocking wait with a watchdog: a pipeline bug traps (launch failure) instead of hanging the GPU.
+// try_wait without a hint returns after a short system time limit; the (slow) global timer is
+// read only every 64 retries.  (Suspending with a long hint was measured slower: the wake-up
+// latency lands on the pipeline's critical path.)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = globaltimer_ns();
+    uint32_t n = 0;
     while (!mbar_try_wait(bar, parity)) {
-        if (globaltimer_ns() - t0 > 20000000000ull) __trap();
+        if ((++n & 63) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
     }
 }
 
@@ -83,6 +98,22 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const void* tmap, uint
         " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;"
         ::"r"(dst), "l"(tmap), "r"(bar), "r"(x), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(policy)
         : "memory");
+}
+// TMA tile store shared -> global (bulk-group completion); out-of-bounds box rows are clipped
+__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int32_t x, int32_t y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                 ::"l"(tmap), "r"(src), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N committed bulk groups of this thread still READ shared memory
+template <int N>
+__device__ __forceinline__ void bulk_wait_group_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_group() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 // 16-byte asynchronous copy global -> shared, cached in L2 only (LDGSTS)
 __device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src) {
