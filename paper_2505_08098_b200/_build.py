@@ -23,25 +23,33 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), variant: str = "") -> str:
+    """variant/defines: experiment builds libf3s_<variant>.so with extra -D flags (selected at run
+    time by F3S_LIB_VARIANT; diagnostics only, the product library is libf3s.so)."""
+    lib = LIB if not variant else os.path.join(HERE, f"libf3s_{variant}.so")
+    if not force and not variant and not _stale():
         return LIB
     objs = []
-    build_dir = os.path.join(HERE, "build")
+    build_dir = os.path.join(HERE, "build" + (f"_{variant}" if variant else ""))
     os.makedirs(build_dir, exist_ok=True)
     for src in SOURCES:
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
+               os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     import sys
-    print(build(force=True, verbose="-v" in sys.argv))
+    args = [a for a in sys.argv[1:] if a != "-v"]
+    if args:  # python _build.py VARIANT DEF1=1 DEF2=3 ...
+        print(build(force=True, verbose="-v" in sys.argv, variant=args[0], defines=args[1:]))
+    else:
+        print(build(force=True, verbose="-v" in sys.argv))

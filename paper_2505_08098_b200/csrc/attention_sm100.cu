@@ -567,6 +567,15 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int flags = sl.flags;
             if (flags & 1) ++item;
             if ((item & 1) != wg) {  // the other warpgroup's item
+                // still observe the phase of the shared S^T buffer b: a warpgroup that skipped kSB
+                // or more chunks could otherwise take phase k-1 of sfull(b) for phase k+1.  Free of
+                // cost: MMA1 completes in chunk order, so this warpgroup's next chunk waits longer.
+                // (pempty cannot alias: MMA1(seq) is issued only after MMA2(seq - kSB), i.e. after
+                // the correction group consumed chunk seq - 2 kSB.)
+#ifndef F3S_SKIP_SFULL
+#define F3S_SKIP_SFULL 1
+#endif
+                if (F3S_SKIP_SFULL) mbar_wait(bar(B::sfull(b)), bph);
                 ++seq;
                 continue;
             }
@@ -576,17 +585,24 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             tc_fence_after();
             uint64_t t_s = 0;
             if (kDiag && p == 0) { t_s = globaltimer_ns(); lap(1); }
+            // MMA2 reads P^T columns [0, ralloc): a warp whose 32 columns all lie beyond has no
+            // score to load, no P to write and contributes -inf to the row max and 0 to l
+            // (warp-uniform; most chunks of small row windows use one or two of the four warps)
+#ifndef F3S_ACT
+#define F3S_ACT 0
+#endif
+            const bool act = !F3S_ACT || 32 * q < sl.ralloc;
             float x[16];
-            if (expt & 32) {
+            if ((expt & 32) || !act) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) x[i] = 0.f;
+                for (int i = 0; i < 16; ++i) x[i] = (expt & 32) ? 0.f : -INFINITY;
             } else {
                 tmem_ld_32x32b_x16(tmem + tl + b * 16, x);
-            }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) x[i] = ((mask >> i) & 1u) ? x[i] * scale_log2 : -INFINITY;  // Alg.1 l.14
+                for (int i = 0; i < 16; ++i) x[i] = ((mask >> i) & 1u) ? x[i] * scale_log2 : -INFINITY;  // Alg.1 l.14
+            }
             // chunk row max (Alg.1 l.16): warp butterfly + 4-warp combine
-            const float rm = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
+            const float rm = ((expt & 32) || !act) ? ((expt & 32) ? 0.f : -INFINITY) : rowreduce16(x, lane, OpMax());
             if (!(lane & 1)) red[(b * 4 + q) * 16 + ((lane >> 1) & 15)] = rm;
             if (p == 0) lap(2);
             named_bar_sync(1 + wg, 128);
@@ -613,7 +629,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     m[i] = fmaxf(kMFloor, cm[i]);
-                    pv[i] = (expt & 1) ? x[i] : ex2(x[i] - m[i]);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
+                    pv[i] = ((expt & 1) || !act) ? 0.f : ex2(x[i] - m[i]);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
                     l[i] = pv[i];
                     av[i] = 0.f;
                 }
@@ -623,12 +639,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     const float mn = fmaxf(m[i], cm[i]);
                     av[i] = (expt & 1) ? 1.f : ex2(m[i] - mn);  // e^{m_o - m_i} (l.18, l.21)
                     m[i] = mn;
-                    pv[i] = (expt & 1) ? x[i] : ex2(x[i] - mn);
+                    pv[i] = ((expt & 1) || !act) ? 0.f : ex2(x[i] - mn);
                     l[i] = fmaf(l[i], av[i], pv[i]);  // l_o (l.18)
                 }
             }
             if (p == 0) lap(6);
-            if (p < C::kMaxRows) {  // E cast to the input dtype into SMEM (l.19): two 16-byte stores
+            if (act) {  // E cast to the input dtype into SMEM (l.19): two 16-byte stores
                 const uint4 lo = make_uint4(pack2<T>(pv[0], pv[1]), pack2<T>(pv[2], pv[3]), pack2<T>(pv[4], pv[5]),
                                             pack2<T>(pv[6], pv[7]));
                 const uint4 hi = make_uint4(pack2<T>(pv[8], pv[9]), pack2<T>(pv[10], pv[11]), pack2<T>(pv[12], pv[13]),

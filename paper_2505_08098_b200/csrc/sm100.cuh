@@ -62,15 +62,16 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     return t;
 }
 // Blocking wait with a watchdog: a pipeline bug traps (launch failure) instead of hanging the GPU.
-// try_wait without a hint returns after a short system time limit; the (slow) global timer is
-// read only every 64 retries.  (Suspending with a long hint was measured slower: the wake-up
-// latency lands on the pipeline's critical path.)
+// The global-timer read between retries doubles as a back-off: measured, both a tighter spin and
+// a long suspend hint in try_wait were slower (issue-slot pressure / wake-up latency).
+#ifndef F3S_WAIT_HINT_NS
+#define F3S_WAIT_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = globaltimer_ns();
-    uint32_t n = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        if ((++n & 63) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
+    while (!(F3S_WAIT_HINT_NS > 0 ? mbar_try_wait_hint(bar, parity, F3S_WAIT_HINT_NS) : mbar_try_wait(bar, parity))) {
+        if (globaltimer_ns() - t0 > 20000000000ull) __trap();
     }
 }
 
@@ -211,6 +212,19 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, float (&v)[16
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// inverse of tmem_ld_32x32b_x16; waits until the stores are complete (tcgen05.wait::st)
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+          "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])),
+          "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+          "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+          "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
 // ---- UMMA descriptors -------------------------------------------------------------------------------

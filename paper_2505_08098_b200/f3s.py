@@ -13,6 +13,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libf3s.so")
+if os.environ.get("F3S_LIB_VARIANT"):  # experiment builds (tools/, _build.py VARIANT ...)
+    LIB_PATH = os.path.join(_HERE, f"libf3s_{os.environ['F3S_LIB_VARIANT']}.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")

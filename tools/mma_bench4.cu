@@ -121,6 +121,19 @@ __global__ void k(int outer, unsigned long long* out, const int4* g) {
                 asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(base + ((r * 4096) & 65535)), "r"(it));
             ++it;
         }
+    } else if (STRESS == 3 || STRESS == 4) {
+        // mbarrier waiters that never succeed (phase 1 of bars[7] never completes), as the
+        // kernel's mbar_wait: try_wait + global-timer read per retry (3) or try_wait only (4)
+        const uint32_t b7 = (uint32_t)__cvta_generic_to_shared(&bars[7]);
+        uint64_t acc = 0;
+        while (!stop) {
+            uint32_t ok;
+            asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 1; selp.u32 %0,1,0,p;}"
+                         : "=r"(ok) : "r"(b7));
+            if (STRESS == 3) { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); acc += t + ok; }
+            else acc += ok;
+        }
+        if (acc == 12345) out[0] = acc;
     } else if (STRESS == 2) {
         const uint32_t base = sa + 131072 + (threadIdx.x - 32) * 16;
         size_t gi = (size_t)blockIdx.x * 4096 + threadIdx.x;
@@ -165,6 +178,10 @@ int main() {
     run(k<0, 1>, "4 MMA M128, st.shared stress", 288);
     run(k<3, 1>, "batched item, st.shared stress", 288);
     run(k<4, 1>, "arxiv chunk, st.shared stress", 288);
+    run(k<3, 3>, "batched item, 8 spinners (timer)", 288);
+    run(k<3, 3>, "batched item, 19 spinners (timer)", 640);
+    run(k<3, 4>, "batched item, 19 spinners (no timer)", 640);
+    run(k<4, 3>, "arxiv chunk, 19 spinners (timer)", 640);
     run(k<0, 2>, "4 MMA M128, cp.async stress", 288);
     run(k<3, 2>, "batched item, cp.async stress", 288);
     run(k<4, 2>, "arxiv chunk, cp.async stress", 288);
