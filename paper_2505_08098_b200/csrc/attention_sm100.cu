@@ -48,11 +48,18 @@ struct Cfg {
     static constexpr int kGroupBytes = 1024 * P;     // 8 gathered rows (one swizzle atom per panel)
     static constexpr int kMaxRows = 128;             // compacted columns per chunk at most (MMA1 M = 128)
     // K tiles live until MMA1 completes, V tiles until MMA2 completes: two FIFO rings
-    static constexpr int kRingK = D == 128 ? 64 * 1024 : 64 * 1024;
-    static constexpr int kRingV = D == 128 ? 80 * 1024 : 88 * 1024;
+    // (the F3S_* macros are experiment knobs for tools/variants.sh; the defaults are the product)
+#ifndef F3S_RINGV128_KB
+#define F3S_RINGV128_KB 88
+#endif
+#ifndef F3S_KNQ128
+#define F3S_KNQ128 4
+#endif
+    static constexpr int kRingK = 64 * 1024;
+    static constexpr int kRingV = D == 128 ? F3S_RINGV128_KB * 1024 : 88 * 1024;
     static constexpr int kRingBytes = kRingK + kRingV;
     static constexpr int kNS = D == 128 ? 20 : 22;   // chunk slots (ids, masks, descriptor, barriers)
-    static constexpr int kNQ = D == 128 ? 6 : 12;    // Q tile slots (items in flight per CTA)
+    static constexpr int kNQ = D == 128 ? F3S_KNQ128 : 12;  // Q tile slots (items in flight per CTA)
     static constexpr int kQBytes = 16 * D * 2;
     static constexpr int kPBytes = 16 * kMaxRows * 2;
     static constexpr int kSB = 4;                    // S/P/O buffers in flight (TMEM and SMEM)
@@ -69,18 +76,30 @@ struct Cfg {
     static constexpr int kLB = 8;                    // row-sum hand-off buffers (items in flight, even)
     static constexpr int oLred = oRed + kSB * 4 * 16 * 4;  // float [kLB][4][16] row-sum partials per item
     static constexpr int oCorr = oLred + kLB * 4 * 16 * 4; // CorrSlot [kSB]
-    static constexpr int oReg = oCorr + kSB * 96;          // int2 [2][kNS] ring regions (K, V)
-    static constexpr int kNumBars = 6 * kNS + 2 * kNQ + 4 * kSB + 2 * kLB;
+    static constexpr int oReg = oCorr + kSB * 128;          // int2 [2][kNS] ring regions (K, V)
+    static constexpr int kNumBars = 6 * kNS + 2 * kNQ + 5 * kSB + 2 * kLB;
     static constexpr int oBar = oReg + 2 * kNS * 8;
     static constexpr int oTmem = oBar + kNumBars * 8;
     static constexpr int kSmemBytes = oTmem + 16;
     static constexpr int kCtasPerSm = 1;
-    static constexpr int kLoaderWarps = 5;           // cp.async gather warps (20 warps in all: 5 per SMSP keeps 96 registers)
+#ifndef F3S_MMA2W
+#define F3S_MMA2W 1
+#endif
+    // kSplitMma: MMA1 and MMA2 are issued by two warps that each sleep on their own barriers
+    // (mbarrier try_wait wakes ~60 cycles after the arrive), instead of one warp polling four
+    // barriers with test_wait (~150 cycles each, measured reaction ~0.9-2.8 us)
+    static constexpr bool kSplitMma = F3S_MMA2W != 0;
+#ifndef F3S_LOADERS
+#define F3S_LOADERS (F3S_MMA2W ? 4 : 5)
+#endif
+    static constexpr int kLoaderWarps = F3S_LOADERS;  // cp.async gather warps (20 warps in all keeps 96 registers)
+    static constexpr int kMma2Warp = 3 + kLoaderWarps;  // (kSplitMma)
     // two softmax warpgroups take alternate work items: one warpgroup's chunk is a long chain of
     // dependent short-latency steps (measured: issue-active ~17% of its cycles), so a second
     // independent chain doubles the softmax throughput
     static constexpr int kSoftmaxWGs = 2;
-    static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps, kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
+    static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps + (kSplitMma ? 1 : 0),
+                         kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
     static constexpr int kThreads = 32 * (kCorr0 + 4);  // control, MMA, index, loaders, softmax, correction
     static constexpr int kBatch = 8;                 // items fetched per queue round trip
     static_assert(kRingK >= (kMaxRows / 8) * kGroupBytes && kRingV >= (kMaxRows / 8) * kGroupBytes,
@@ -108,6 +127,8 @@ template <int D> struct Bars {
     __host__ __device__ static constexpr int lempty(int b) { return kB0 + 4 * C::kSB + C::kLB + b; }
     __host__ __device__ static constexpr int rfull(int s) { return kB0 + 4 * C::kSB + 2 * C::kLB + s; }
     __host__ __device__ static constexpr int kempty(int s) { return kB0 + 4 * C::kSB + 2 * C::kLB + C::kNS + s; }
+    // S^T buffer b may be overwritten: MMA2 of its previous chunk issued (kSplitMma)
+    __host__ __device__ static constexpr int sfree(int b) { return kB0 + 4 * C::kSB + 2 * C::kLB + 2 * C::kNS + b; }
 };
 
 // One chunk of one work item: written by the index warp (ids/masks by cp.async.bulk), the
@@ -129,6 +150,7 @@ struct __align__(16) CorrSlot {
     float alpha[16];   // e^{m_old - m_new} per query row (Alg.1 l.21)
     int32_t rows, flags, rw, head;
     uint64_t t_s, t_p; // F3S_TRACE stamps of the softmax group (written out by the correction group)
+    uint64_t tq[4];    // diagnostics (F3S_TRACE_EV0 == 3): per-warp time just before the pfull arrive
 };
 
 // Transposing butterfly: 16 per-row values in each of 32 lanes -> lane l holds the
@@ -229,6 +251,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             mbar_init(bar(B::pfull(b)), 128);
             mbar_init(bar(B::ofull(b)), 1);
             mbar_init(bar(B::pempty(b)), 128);
+            mbar_init(bar(B::sfree(b)), 1);
         }
         for (int b = 0; b < C::kLB; ++b) {
             mbar_init(bar(B::lfull(b)), 128);
@@ -299,7 +322,10 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         } else {
                             mbar_arrive(fb);
                         }
-                        stamp(seq, 0);
+#ifndef F3S_TRACE_EV0
+#define F3S_TRACE_EV0 0
+#endif
+                        if (!F3S_TRACE_EV0) stamp(seq, 0);
                         lap(2);
                     }
                     ++seq;
@@ -387,7 +413,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             ++seq;
         }
         __syncwarp();
-    } else if (warp >= C::kLoader0 && warp < C::kSoftmax0) {
+    } else if (warp >= C::kLoader0 && warp < C::kLoader0 + C::kLoaderWarps) {
         // ===== loader warps: gather the K and V rows of each chunk (Alg.1 l.8) ===================
         // Lane l of a warp copies 16-byte piece (l % pieces) of one gathered row straight into the
         // 128B-swizzled UMMA layout; the rows of a chunk are dealt round-robin to the warps.
@@ -432,6 +458,70 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (lw == 0 && lane == 0) stamp(seq, 1);
             ++seq;
         }
+    } else if (C::kSplitMma && (warp == 1 || warp == C::kMma2Warp)) {
+        // ===== MMA issuers: warp 1 issues MMA1 (SDDMM), warp kMma2Warp MMA2 (SpMM) ====================
+        // Each walks the chunks in order and sleeps in try_wait on the barriers of its next
+        // instruction.  Whole warps run the loops on warp-uniform values; one elected lane issues
+        // (sm100.cuh: mma_f16_ss_warp).  The cp.async-written K/V tiles need no proxy fence here
+        // (the mbarrier completion of cp.async orders them, as in CUTLASS's SM100 cp.async
+        // mainloop); P is fenced by its writers before pfull.
+        constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+        if (warp == 1) {
+            constexpr uint32_t idesc1 = idesc_f16(fmt, 0, 0, 128, 16);  // S^T = K_c . Q_w^T
+            const uint64_t dK = smem_desc_sw128(0, 16, C::kGroupBytes);
+            const uint64_t dQ = smem_desc_sw128(0, 16, 1024);
+            for (int32_t n1 = 0;; ++n1) {
+                const int s = n1 % C::kNS, b = n1 % C::kSB;
+                mbar_wait(bar(B::kfull(s)), (n1 / C::kNS) & 1);  // K_c landed
+                const Slot& sl = slots[s];
+                const int rows = sl.rows, flags = sl.flags, qslot = sl.qslot, roff = sl.ring_off;
+                if (rows < 0) break;
+                mbar_wait(bar(B::sfree(b)), ((n1 / C::kSB) & 1) ^ 1);  // MMA2(n1 - kSB) issued
+                if (flags & 1) mbar_wait(bar(B::qfull(qslot)), (flags >> 2) & 1);
+                tc_fence_after();
+                const uint64_t a0 = dK + ((sb + C::oRing + roff) >> 4);
+                const uint64_t b0 = dQ + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
+                if (rows > 0 && !(expt & 4)) {
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        mma_f16_ss_warp(tmem + b * 16, a0 + (((kk >> 2) * 1024 + (kk & 3) * 32) >> 4),
+                                        b0 + (((kk >> 2) * 2048 + (kk & 3) * 32) >> 4), idesc1, kk > 0 ? 1u : 0u);
+                }
+                mma_commit_warp(bar(B::sfull(b)));
+                mma_commit_warp(bar(B::kempty(s)));
+                if (flags & 2) mma_commit_warp(bar(B::qempty(qslot)));
+                if (lane == 0 && F3S_TRACE_EV0 != 3) stamp(n1, 2);
+            }
+        } else {
+            constexpr uint32_t idesc2 = idesc_f16(fmt, 1, 1, D, 16);    // O^T = V_c^T . P^T (A, B MN-major)
+            const uint64_t dV = smem_desc_sw128(0, 1024, C::kGroupBytes);
+            const uint64_t dP = smem_desc_sw32(0, 4096, 256);
+            for (int32_t n2 = 0;; ++n2) {
+                const int s = n2 % C::kNS, b = n2 % C::kSB;
+                mbar_wait(bar(B::kfull(s)), (n2 / C::kNS) & 1);  // slot of chunk n2 filled
+                const int rows = slots[s].rows;
+                if (rows < 0) break;
+                mbar_wait(bar(B::pfull(b)), (n2 / C::kSB) & 1);  // P_c written
+                mbar_wait(bar(B::vfull(s)), (n2 / C::kNS) & 1);  // V_c landed
+                tc_fence_after();
+                if (rows > 0 && !(expt & 2)) {
+                    const uint64_t a0 = dV + ((sb + C::oRingV + slots[s].pad) >> 4);
+                    const uint64_t b0 = dP + ((sb + C::oP + b * C::kPBytes) >> 4);
+                    const int nsteps = (rows + 15) >> 4;
+                    for (int st = 0; st < nsteps; ++st)
+                        mma_f16_ss_warp(tmem + 16 * C::kSB + b * 16, a0 + ((st * 2 * C::kGroupBytes) >> 4),
+                                        b0 + ((st * 512) >> 4), idesc2, st > 0 ? 1u : 0u);
+                }
+                mma_commit_warp(bar(B::ofull(b)));
+                mma_commit_warp(bar(B::empty(s)));
+                if (lane == 0) {
+                    mbar_arrive(bar(B::sfree(b)));  // S^T_b was consumed by the softmax before P_c
+                    stamp(n2, 5);
+                }
+                __syncwarp();
+            }
+        }
+        __syncwarp();
     } else if (warp == 1) {
         // ===== MMA issuer (whole warp, one elected lane issues; event loop) ===========================
         // MMA1(c) as soon as K_c (and Q) landed and one of the kSB S buffers is free;
@@ -479,7 +569,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                             mma_commit_warp(bar(B::sfull(b)));
                             mma_commit_warp(bar(B::kempty(s)));
                             if (flags & 2) mma_commit_warp(bar(B::qempty(qslot)));
-                            if (lane == 0) stamp(n1, 2);
+                            if (lane == 0 && F3S_TRACE_EV0 != 3) stamp(n1, 2);
                             lap(1);
                             ++n1;
                             progressed = true;
@@ -488,6 +578,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
                 if (n2 < n1) {
                     const int s = n2 % C::kNS, b = n2 % C::kSB;
+                    if (F3S_TRACE_EV0 == 1 && kDiag && lane == 0 && trace != nullptr && n2 < trace_chunks &&
+                        trace[((size_t)blockIdx.x * trace_chunks + n2) * 8] == 0 && mbar_test(bar(B::pfull(b)), (n2 / C::kSB) & 1))
+                        stamp(n2, 0);  // diagnostics: when the MMA warp first sees P_n2 complete
+                    if (F3S_TRACE_EV0 == 2 && kDiag && lane == 0 && trace != nullptr && n2 < trace_chunks &&
+                        trace[((size_t)blockIdx.x * trace_chunks + n2) * 8] == 0 && mbar_test(bar(B::vfull(s)), (n2 / C::kNS) & 1))
+                        stamp(n2, 0);  // diagnostics: when the MMA warp first sees V_n2 landed
                     if (mbar_test(bar(B::pfull(b)), (n2 / C::kSB) & 1) && mbar_test(bar(B::vfull(s)), (n2 / C::kNS) & 1)) {
                         if (fence_k) fence_proxy_async_smem();
                         tc_fence_after();
@@ -665,8 +761,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
             }
             if (p == 0) lap(7);
-            fence_proxy_async_smem();
+#ifndef F3S_NOFENCE
+#define F3S_NOFENCE 0
+#endif
+            if (!F3S_NOFENCE) fence_proxy_async_smem();
             tc_fence_before();
+            if (F3S_TRACE_EV0 == 3 && kDiag && lane == 0) corr[b].tq[q] = globaltimer_ns();
             mbar_arrive(bar(B::pfull(b)));
             if (p == 0) lap(4);
             if (flags & 2) {
@@ -708,6 +808,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 if (kDiag && trace != nullptr && seq < trace_chunks) {
                     trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 3] = corr[b].t_s;
                     trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 4] = corr[b].t_p;
+                    if (F3S_TRACE_EV0 == 3) {
+                        trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 0] = corr[b].tq[3];
+                        trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 2] = corr[b].tq[1];
+                        trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 7] = corr[b].tq[2];
+                        trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 3] = corr[b].tq[0];
+                    }
                 }
                 stamp(seq, 6);
                 lap(1);
@@ -770,7 +876,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) oacc[i] = 0.f;
-                if (lead) { stamp(seq, 7); lap(4); }
+                if (lead) { if (F3S_TRACE_EV0 != 3) stamp(seq, 7); lap(4); }
                 ++item;
             }
             ++seq;
