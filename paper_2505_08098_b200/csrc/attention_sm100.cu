@@ -82,23 +82,19 @@ struct Cfg {
     static constexpr int oTmem = oBar + kNumBars * 8;
     static constexpr int kSmemBytes = oTmem + 16;
     static constexpr int kCtasPerSm = 1;
-#ifndef F3S_MMA2W
-#define F3S_MMA2W 1
-#endif
-    // kSplitMma: MMA1 and MMA2 are issued by two warps that each sleep on their own barriers
-    // (mbarrier try_wait wakes ~60 cycles after the arrive), instead of one warp polling four
-    // barriers with test_wait (~150 cycles each, measured reaction ~0.9-2.8 us)
-    static constexpr bool kSplitMma = F3S_MMA2W != 0;
+    // MMA1 and MMA2 are issued by two warps that each sleep on their own barriers (mbarrier
+    // try_wait wakes ~60 cycles after the arrive); one warp polling four barriers with test_wait
+    // (~150 cycles each) reacted 0.9-2.8 us late (measured)
 #ifndef F3S_LOADERS
-#define F3S_LOADERS (F3S_MMA2W ? 4 : 5)
+#define F3S_LOADERS 4
 #endif
     static constexpr int kLoaderWarps = F3S_LOADERS;  // cp.async gather warps (20 warps in all keeps 96 registers)
-    static constexpr int kMma2Warp = 3 + kLoaderWarps;  // (kSplitMma)
+    static constexpr int kMma2Warp = 3 + kLoaderWarps;
     // two softmax warpgroups take alternate work items: one warpgroup's chunk is a long chain of
     // dependent short-latency steps (measured: issue-active ~17% of its cycles), so a second
     // independent chain doubles the softmax throughput
     static constexpr int kSoftmaxWGs = 2;
-    static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps + (kSplitMma ? 1 : 0),
+    static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps + 1,
                          kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
     static constexpr int kThreads = 32 * (kCorr0 + 4);  // control, MMA, index, loaders, softmax, correction
     static constexpr int kBatch = 8;                 // items fetched per queue round trip
@@ -127,7 +123,8 @@ template <int D> struct Bars {
     __host__ __device__ static constexpr int lempty(int b) { return kB0 + 4 * C::kSB + C::kLB + b; }
     __host__ __device__ static constexpr int rfull(int s) { return kB0 + 4 * C::kSB + 2 * C::kLB + s; }
     __host__ __device__ static constexpr int kempty(int s) { return kB0 + 4 * C::kSB + 2 * C::kLB + C::kNS + s; }
-    // S^T buffer b may be overwritten: MMA2 of its previous chunk issued (kSplitMma)
+    // S^T buffer b may be overwritten by MMA1: both softmax warpgroups passed its previous chunk
+    // (the owner after the P-tile wait, the other in its skip path): 8 warp arrivals
     __host__ __device__ static constexpr int sfree(int b) { return kB0 + 4 * C::kSB + 2 * C::kLB + 2 * C::kNS + b; }
 };
 
@@ -251,7 +248,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             mbar_init(bar(B::pfull(b)), 128);
             mbar_init(bar(B::ofull(b)), 1);
             mbar_init(bar(B::pempty(b)), 128);
-            mbar_init(bar(B::sfree(b)), 1);
+            mbar_init(bar(B::sfree(b)), 8);
         }
         for (int b = 0; b < C::kLB; ++b) {
             mbar_init(bar(B::lfull(b)), 128);
@@ -325,7 +322,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #ifndef F3S_TRACE_EV0
 #define F3S_TRACE_EV0 0
 #endif
-                        if (!F3S_TRACE_EV0) stamp(seq, 0);
+                        if (F3S_TRACE_EV0 == 0) stamp(seq, 0);
                         lap(2);
                     }
                     ++seq;
@@ -458,7 +455,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (lw == 0 && lane == 0) stamp(seq, 1);
             ++seq;
         }
-    } else if (C::kSplitMma && (warp == 1 || warp == C::kMma2Warp)) {
+    } else if (warp == 1 || warp == C::kMma2Warp) {
         // ===== MMA issuers: warp 1 issues MMA1 (SDDMM), warp kMma2Warp MMA2 (SpMM) ====================
         // Each walks the chunks in order and sleeps in try_wait on the barriers of its next
         // instruction.  Whole warps run the loops on warp-uniform values; one elected lane issues
@@ -476,7 +473,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const Slot& sl = slots[s];
                 const int rows = sl.rows, flags = sl.flags, qslot = sl.qslot, roff = sl.ring_off;
                 if (rows < 0) break;
-                mbar_wait(bar(B::sfree(b)), ((n1 / C::kSB) & 1) ^ 1);  // MMA2(n1 - kSB) issued
+                mbar_wait(bar(B::sfree(b)), ((n1 / C::kSB) & 1) ^ 1);  // both warpgroups passed chunk n1 - kSB
                 if (flags & 1) mbar_wait(bar(B::qfull(qslot)), (flags >> 2) & 1);
                 tc_fence_after();
                 const uint64_t a0 = dK + ((sb + C::oRing + roff) >> 4);
@@ -502,7 +499,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const int rows = slots[s].rows;
                 if (rows < 0) break;
                 mbar_wait(bar(B::pfull(b)), (n2 / C::kSB) & 1);  // P_c written
+                if (F3S_TRACE_EV0 == 4 && lane == 0) stamp(n2, 0);
                 mbar_wait(bar(B::vfull(s)), (n2 / C::kNS) & 1);  // V_c landed
+                if (F3S_TRACE_EV0 == 4 && lane == 0) stamp(n2, 7);
                 tc_fence_after();
                 if (rows > 0 && !(expt & 2)) {
                     const uint64_t a0 = dV + ((sb + C::oRingV + slots[s].pad) >> 4);
@@ -514,117 +513,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
                 mma_commit_warp(bar(B::ofull(b)));
                 mma_commit_warp(bar(B::empty(s)));
-                if (lane == 0) {
-                    mbar_arrive(bar(B::sfree(b)));  // S^T_b was consumed by the softmax before P_c
-                    stamp(n2, 5);
-                }
+                if (lane == 0) stamp(n2, 5);
                 __syncwarp();
             }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        // ===== MMA issuer (whole warp, one elected lane issues; event loop) ===========================
-        // MMA1(c) as soon as K_c (and Q) landed and one of the kSB S buffers is free;
-        // MMA2(c) as soon as P_c is written and V_c landed.  Both in chunk order.  All lanes run
-        // the loop on warp-uniform values so the tcgen05 instructions are issued without a
-        // lane-divergent waterfall (sm100.cuh: mma_f16_ss_warp).  The cp.async-written K/V tiles
-        // need no proxy fence here (the mbarrier completion of cp.async orders them, as in
-        // CUTLASS's SM100 cp.async mainloop); P is fenced by its writers before pfull.
-        {
-            constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
-            constexpr uint32_t idesc1 = idesc_f16(fmt, 0, 0, 128, 16);  // S^T = K_c . Q_w^T
-            constexpr uint32_t idesc2 = idesc_f16(fmt, 1, 1, D, 16);    // O^T = V_c^T . P^T (A, B MN-major)
-            // descriptor templates at address 0; adding (addr >> 4) sets the start address
-            // (shared addresses < 256 KB fit the 14-bit field, so the add never carries)
-            const uint64_t dK = smem_desc_sw128(0, 16, C::kGroupBytes);
-            const uint64_t dQ = smem_desc_sw128(0, 16, 1024);
-            const uint64_t dV = smem_desc_sw128(0, 1024, C::kGroupBytes);
-            const uint64_t dP = smem_desc_sw32(0, 4096, 256);
-            const bool fence_k = (expt & 16) != 0;  // diagnostics: consumer-side proxy fence
-            int32_t n1 = 0, n2 = 0, stop_at = 0x7FFFFFFF;
-            uint64_t idle_since = 0;
-            uint32_t idle_polls = 0;
-            while (n2 < stop_at) {
-                bool progressed = false;
-                if (n1 < stop_at && n1 < n2 + C::kSB) {
-                    const int s = n1 % C::kNS;
-                    if (mbar_test(bar(B::kfull(s)), (n1 / C::kNS) & 1)) {
-                        const Slot& sl = slots[s];
-                        const int rows = sl.rows, flags = sl.flags, qslot = sl.qslot, roff = sl.ring_off;
-                        if (rows < 0) {
-                            stop_at = n1;
-                            progressed = true;
-                        } else if (!(flags & 1) || mbar_test(bar(B::qfull(qslot)), (flags >> 2) & 1)) {
-                            if (fence_k) fence_proxy_async_smem();
-                            tc_fence_after();
-                            const int b = n1 % C::kSB;
-                            const uint64_t a0 = dK + ((sb + C::oRing + roff) >> 4);
-                            const uint64_t b0 = dQ + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
-                            if (rows > 0 && !(expt & 4)) {
-#pragma unroll
-                                for (int kk = 0; kk < D / 16; ++kk)
-                                    mma_f16_ss_warp(tmem + b * 16, a0 + (((kk >> 2) * 1024 + (kk & 3) * 32) >> 4),
-                                                    b0 + (((kk >> 2) * 2048 + (kk & 3) * 32) >> 4), idesc1, kk > 0 ? 1u : 0u);
-                            }
-                            mma_commit_warp(bar(B::sfull(b)));
-                            mma_commit_warp(bar(B::kempty(s)));
-                            if (flags & 2) mma_commit_warp(bar(B::qempty(qslot)));
-                            if (lane == 0 && F3S_TRACE_EV0 != 3) stamp(n1, 2);
-                            lap(1);
-                            ++n1;
-                            progressed = true;
-                        }
-                    }
-                }
-                if (n2 < n1) {
-                    const int s = n2 % C::kNS, b = n2 % C::kSB;
-                    if (F3S_TRACE_EV0 == 1 && kDiag && lane == 0 && trace != nullptr && n2 < trace_chunks &&
-                        trace[((size_t)blockIdx.x * trace_chunks + n2) * 8] == 0 && mbar_test(bar(B::pfull(b)), (n2 / C::kSB) & 1))
-                        stamp(n2, 0);  // diagnostics: when the MMA warp first sees P_n2 complete
-                    if (F3S_TRACE_EV0 == 2 && kDiag && lane == 0 && trace != nullptr && n2 < trace_chunks &&
-                        trace[((size_t)blockIdx.x * trace_chunks + n2) * 8] == 0 && mbar_test(bar(B::vfull(s)), (n2 / C::kNS) & 1))
-                        stamp(n2, 0);  // diagnostics: when the MMA warp first sees V_n2 landed
-                    if (mbar_test(bar(B::pfull(b)), (n2 / C::kSB) & 1) && mbar_test(bar(B::vfull(s)), (n2 / C::kNS) & 1)) {
-                        if (fence_k) fence_proxy_async_smem();
-                        tc_fence_after();
-                        const int rows = slots[s].rows;
-                        if (rows > 0 && !(expt & 2)) {
-                            const uint64_t a0 = dV + ((sb + C::oRingV + slots[s].pad) >> 4);
-                            const uint64_t b0 = dP + ((sb + C::oP + b * C::kPBytes) >> 4);
-                            const int nsteps = (rows + 15) >> 4;
-                            for (int st = 0; st < nsteps; ++st)
-                                mma_f16_ss_warp(tmem + 16 * C::kSB + b * 16, a0 + ((st * 2 * C::kGroupBytes) >> 4),
-                                                b0 + ((st * 512) >> 4), idesc2, st > 0 ? 1u : 0u);
-                        }
-                        mma_commit_warp(bar(B::ofull(b)));
-                        mma_commit_warp(bar(B::empty(s)));
-                        if (lane == 0) stamp(n2, 5);
-                        lap(2);
-                        ++n2;
-                        progressed = true;
-                    }
-                }
-                // watchdog for the polling loop (the blocking waits have their own)
-                if (progressed) {
-                    idle_since = 0;
-                    idle_polls = 0;
-                } else {
-                    lap(n1 < stop_at && n1 >= n2 + C::kSB ? 3 : (n2 < n1 ? 4 : 0));
-                    // sleep on the event most likely next (P of the oldest chunk, else the next K
-                    // tile) rather than spin: the spinning warp would take issue slots from the
-                    // softmax warps of its SM sub-partition
-                    if (mma_sleep_ns > 0) {
-                        if (n2 < n1) mbar_try_wait_hint(bar(B::pfull(n2 % C::kSB)), (n2 / C::kSB) & 1, mma_sleep_ns);
-                        else if (n1 < stop_at) mbar_try_wait_hint(bar(B::kfull(n1 % C::kNS)), (n1 / C::kNS) & 1, mma_sleep_ns);
-                    }
-                    if ((++idle_polls & 1023) == 0) {  // read the (slow) global timer rarely
-                        const uint64_t now = globaltimer_ns();
-                        if (idle_since == 0) idle_since = now;
-                        else if (now - idle_since > 20000000000ull) __trap();
-                    }
-                }
-            }
-            if (lane == 0) prof_flush(12);
         }
         __syncwarp();
     } else if (warp < C::kCorr0) {
@@ -663,15 +554,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int flags = sl.flags;
             if (flags & 1) ++item;
             if ((item & 1) != wg) {  // the other warpgroup's item
-                // still observe the phase of the shared S^T buffer b: a warpgroup that skipped kSB
-                // or more chunks could otherwise take phase k-1 of sfull(b) for phase k+1.  Free of
-                // cost: MMA1 completes in chunk order, so this warpgroup's next chunk waits longer.
-                // (pempty cannot alias: MMA1(seq) is issued only after MMA2(seq - kSB), i.e. after
-                // the correction group consumed chunk seq - 2 kSB.)
-#ifndef F3S_SKIP_SFULL
-#define F3S_SKIP_SFULL 1
-#endif
-                if (F3S_SKIP_SFULL) mbar_wait(bar(B::sfull(b)), bph);
+                // Observe the phase of the shared S^T buffer b, then release it: MMA1 may refill
+                // buffer b only when both warpgroups passed this chunk, so neither can take phase
+                // k+1 of sfull(b) for phase k.  Free of cost: MMA1 completes in chunk order, so
+                // this warpgroup's next chunk waits longer anyway.
+                mbar_wait(bar(B::sfull(b)), bph);
+                if (lane == 0) mbar_arrive(bar(B::sfree(b)));
                 ++seq;
                 continue;
             }
@@ -704,6 +592,10 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             named_bar_sync(1 + wg, 128);
             // P_b / corr_b are free once the correction group consumed chunk seq - kSB
             mbar_wait(bar(B::pempty(b)), bph ^ 1);
+            // S^T_b was loaded above; releasing it only now (after the P-tile wait) also keeps the
+            // pempty phases exact: MMA1(seq + kSB) then implies the correction consumed seq - kSB
+            tc_fence_before();
+            if (lane == 0) mbar_arrive(bar(B::sfree(b)));
             if (p == 0) lap(3);
             const float4* r4 = reinterpret_cast<const float4*>(red + b * 64);
             // P^T is the MN-major B operand of MMA2 with a 32-byte swizzle: compacted column p
@@ -876,7 +768,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) oacc[i] = 0.f;
-                if (lead) { if (F3S_TRACE_EV0 != 3) stamp(seq, 7); lap(4); }
+                if (lead) { if (F3S_TRACE_EV0 < 3) stamp(seq, 7); lap(4); }
                 ++item;
             }
             ++seq;
