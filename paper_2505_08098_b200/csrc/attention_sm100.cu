@@ -752,19 +752,33 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 // past n_rows of a ragged last window are clipped by the tensor map, reading c14)
                 const int ob = item % C::kNO;
                 float* ost = reinterpret_cast<float*>(smem + C::oOst + ob * C::kOBytes);
-                if (threadIdx.x == 32 * C::kCorr0) bulk_wait_group_read<C::kNO - 1>();  // staging tile ob free
-                named_bar_sync(3, 128);
                 const bool has = D == 128 || lane < 16;
                 const int f = D == 128 ? 32 * q + lane : 16 * q + lane;  // O^T lane -> feature (M = 64 layout)
-                if (has) {
+#ifndef F3S_OSTG
+#define F3S_OSTG 0
+#endif
+                if (F3S_OSTG) {  // direct coalesced stores: lane = feature, one row per instruction
+                    const int nvalid = min(16, n_rows - 16 * rw);  // ragged last window (reading c14)
+                    if (has && !(expt & 64)) {
+                        const int64_t ld = (int64_t)H * D;
+                        float* out = O + (int64_t)16 * rw * ld + (int64_t)hd * D + f;
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) ost[i * D + f] = oacc[i] * inv[i];
-                }
-                fence_proxy_async_smem();
-                named_bar_sync(3, 128);
-                if (threadIdx.x == 32 * C::kCorr0) {
-                    if (!(expt & 64)) tma_store_2d(&tmO, sb + C::oOst + ob * C::kOBytes, hd * D, 16 * rw);
-                    bulk_commit_group();
+                        for (int i = 0; i < 16; ++i)
+                            if (i < nvalid) out[(int64_t)i * ld] = oacc[i] * inv[i];
+                    }
+                } else {
+                    if (threadIdx.x == 32 * C::kCorr0) bulk_wait_group_read<C::kNO - 1>();  // staging tile ob free
+                    named_bar_sync(3, 128);
+                    if (has) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) ost[i * D + f] = oacc[i] * inv[i];
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(3, 128);
+                    if (threadIdx.x == 32 * C::kCorr0) {
+                        if (!(expt & 64)) tma_store_2d(&tmO, sb + C::oOst + ob * C::kOBytes, hd * D, 16 * rw);
+                        bulk_commit_group();
+                    }
                 }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) oacc[i] = 0.f;
