@@ -61,6 +61,8 @@ typedef struct {
     int64_t device_bytes; /* device memory owned by the plan                                   */
     float build_ms;       /* device time of the plan build                                     */
     float reserved;
+    int32_t split_chunks; /* heavy-window split: pieces of at most this many 128-column chunks  */
+    int32_t split_groups; /* row windows that are split      */
 } f3s_plan_info;
 
 /*
@@ -106,6 +108,20 @@ f3s_status f3s_plan_get_info(f3s_plan_t plan, f3s_plan_info* info);
  * These arrays are independent of the kernel's tile size and are what the tests compare
  * bit-exactly with the oracle's block builder.
  */
+/*
+ * Heavy row-window split (load balance under degree skew; the paper's "assigning multiple
+ * thread blocks per row window").  f3s_attention (default variant) processes
+ * a row window of more than max_chunks 128-column chunks as pieces of max_chunks chunks on
+ * different CTAs; each piece leaves its partial (row max, row sum, unnormalised O) in a
+ * per-call scratch buffer and the CTA that completes a window's last piece merges all pieces
+ * in piece order (O = sum_p e^{m_p - M} O_p / sum_p e^{m_p - M} l_p), so results stay
+ * bitwise deterministic.  f3s_plan picks max(16, ceil(total chunks / (2 * SMs))); this call
+ * rebuilds the piece list with another bound (max_chunks <= 0: never split).  Host-synchronous;
+ * not to be called while attention calls on the plan are in flight.
+ * Errors: INVALID_VALUE (NULL plan), UNSUPPORTED (more than 65535 pieces per window), CUDA.
+ */
+f3s_status f3s_plan_set_split(f3s_plan_t plan, int32_t max_chunks);
+
 f3s_status f3s_plan_export(f3s_plan_t plan, int32_t* rw_ptr, int32_t* cols, uint16_t* masks, int32_t* rw_order);
 
 /*

@@ -75,8 +75,10 @@ struct Cfg {
     static constexpr int oRed = oSlot + kNS * kSlotBytes;  // float [kSB][4][16] chunk row-max partials
     static constexpr int kLB = 8;                    // row-sum hand-off buffers (items in flight, even)
     static constexpr int oLred = oRed + kSB * 4 * 16 * 4;  // float [kLB][4][16] row-sum partials per item
-    static constexpr int oCorr = oLred + kLB * 4 * 16 * 4; // CorrSlot [kSB]
-    static constexpr int oReg = oCorr + kSB * 128;          // int2 [2][kNS] ring regions (K, V)
+    static constexpr int oLm = oLred + kLB * 4 * 16 * 4;   // float [kLB][16] row max of a split piece
+    static constexpr int oCorr = oLm + kLB * 16 * 4;        // CorrSlot [kSB]
+    static constexpr int kCorrBytes = 128;                  // sizeof(CorrSlot)
+    static constexpr int oReg = oCorr + kSB * kCorrBytes;   // int2 [2][kNS] ring regions (K, V)
     static constexpr int kNumBars = 6 * kNS + 2 * kNQ + 5 * kSB + 2 * kLB;
     static constexpr int oBar = oReg + 2 * kNS * 8;
     static constexpr int oTmem = oBar + kNumBars * 8;
@@ -136,7 +138,8 @@ struct __align__(16) Slot {
     int32_t rows;      // valid compacted columns in this chunk (0 for an empty RW, -1 = stop)
     int32_t ring_off;  // byte offset of the K tile in the ring (V tile follows)
     int32_t qslot;
-    int32_t flags;     // bit0 first chunk of item, bit1 last chunk, bit2 Q-slot phase
+    int32_t flags;     // bit0 first chunk of item, bit1 last chunk, bit2 Q-slot phase, bits 8..31 split:
+                       // 0, or 1 + global piece index of a split row window (Plan::meta_sub)
     int32_t ralloc;    // rows allocated in the ring (multiple of 16)
     int32_t pad;       // byte offset of the V tile in the V ring
     int32_t cols[128];     // gathered row ids (tail repeats the last column)
@@ -149,6 +152,8 @@ struct __align__(16) CorrSlot {
     uint64_t t_s, t_p; // F3S_TRACE stamps of the softmax group (written out by the correction group)
     uint64_t tq[4];    // diagnostics (F3S_TRACE_EV0 == 3): per-warp time just before the pfull arrive
 };
+
+static_assert(sizeof(CorrSlot) == Cfg<64>::kCorrBytes && sizeof(Slot) == Cfg<64>::kSlotBytes, "layout");
 
 // Transposing butterfly: 16 per-row values in each of 32 lanes -> lane l holds the
 // reduction over the warp for row (l >> 1) & 15.  16 shuffles.
@@ -189,7 +194,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
             int32_t* __restrict__ counter, int32_t n_items, int32_t H, int32_t n_rows, int32_t chunk_rows,
             const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float* __restrict__ O, float scale_log2,
-            uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt, uint32_t mma_sleep_ns) {
+            uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt, uint32_t mma_sleep_ns,
+            float* __restrict__ scratch) {
     using C = Cfg<D>;
     using B = Bars<D>;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -292,6 +298,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const int32_t k = __shfl_sync(0xffffffffu, mt.x, b);
                 const int32_t cb8 = __shfl_sync(0xffffffffu, mt.y, b);
                 const int32_t w = __shfl_sync(0xffffffffu, mt.z, b);
+                const int32_t sp = __shfl_sync(0xffffffffu, mt.w, b);
                 if (itb >= n_items) { done = true; continue; }
                 const int32_t h = itb - (itb / H) * H;
                 const int nch = w > 0 ? (w + chunk_rows - 1) / chunk_rows : 1;
@@ -308,7 +315,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         sl.head = h;
                         sl.rows = rows;
                         sl.qslot = qs;
-                        sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2);
+                        sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2) | (sp << 8);
                         sl.ralloc = rows > 0 ? ((rows + 15) & ~15) : 0;
                         const uint32_t fb = bar(B::idxfull(s));
                         if (rows > 0) {
@@ -564,7 +571,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 continue;
             }
             const uint32_t mask = p < rows ? (uint32_t)sl.masks[p] : 0u;
-            const int rw = sl.rw, hd = sl.head;
+            const int rw = sl.rw, hd = sl.head, sp = flags >> 8;  // split piece (0: none)
             mbar_wait(bar(B::sfull(b)), bph);
             tc_fence_after();
             uint64_t t_s = 0;
@@ -667,6 +674,11 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const float rl = rowreduce16(l, lane, OpAdd());
                 mbar_wait(bar(B::lempty(ib)), ((item / C::kLB) & 1) ^ 1);
                 if (!(lane & 1)) lred[(ib * 4 + q) * 16 + ((lane >> 1) & 15)] = rl;
+                if (p == 0 && sp) {  // a piece of a split window also hands over its row max
+                    float4* m4 = reinterpret_cast<float4*>(smem + C::oLm + ib * 64);
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) m4[g] = make_float4(m[4 * g], m[4 * g + 1], m[4 * g + 2], m[4 * g + 3]);
+                }
                 mbar_arrive(bar(B::lfull(ib)));
                 if (p == 0) lap(5);
             }
@@ -689,6 +701,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (lead) lap(0);
             const int4 info = reinterpret_cast<const int4*>(&corr[b].rows)[0];
             const int rows = info.x, flags = info.y, rw = info.z, hd = info.w;
+            const int split = flags >> 8;
             if (rows < 0) {
                 if (lead) prof_flush(24);
                 break;
@@ -739,25 +752,58 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 if (lead) lap(3);
                 const float4* l4 = reinterpret_cast<const float4*>(lred + ib * 64);
                 float inv[16];
+                auto row_sum = [&](int g, float (&lt)[4]) {  // l_o of rows 4g..4g+3: the 4 warps' partials
+                    const float4 a = l4[g], b4 = l4[4 + g], c = l4[8 + g], e = l4[12 + g];
+                    lt[0] = (a.x + b4.x) + (c.x + e.x);
+                    lt[1] = (a.y + b4.y) + (c.y + e.y);
+                    lt[2] = (a.z + b4.z) + (c.z + e.z);
+                    lt[3] = (a.w + b4.w) + (c.w + e.w);
+                };
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    const float4 a = l4[g], b4 = l4[4 + g], c = l4[8 + g], e = l4[12 + g];
-                    const float lt[4] = {(a.x + b4.x) + (c.x + e.x), (a.y + b4.y) + (c.y + e.y),
-                                         (a.z + b4.z) + (c.z + e.z), (a.w + b4.w) + (c.w + e.w)};
+                    float lt[4];
+                    row_sum(g, lt);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) inv[4 * g + u] = lt[u] > 0.f ? rcp_approx(lt[u]) : 0.f;  // empty row -> 0
+                }
+                const bool has = D == 128 || lane < 16;
+                const int f = D == 128 ? 32 * q + lane : 16 * q + lane;  // O^T lane -> feature (M = 64 layout)
+                bool do_store = true;
+#ifndef F3S_SPLIT_CODE
+#define F3S_SPLIT_CODE 1
+#endif
+                if (F3S_SPLIT_CODE && split) {
+                    // piece of a split row window: leave (m, l, unnormalised O) in the scratch
+                    // record of its global piece; k_split_merge combines the pieces after the
+                    // kernel, in piece order (deterministic)
+                    const int64_t rec_floats = 32 + 16 * D;
+                    float* rec = scratch + ((int64_t)(split - 1) * H + hd) * rec_floats;
+                    if (lead) {
+                        const float* lm = reinterpret_cast<const float*>(smem + C::oLm + ib * 64);
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            float lt[4];
+                            row_sum(g, lt);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) { rec[4 * g + u] = lm[4 * g + u]; rec[16 + 4 * g + u] = lt[u]; }
+                        }
+                    }
+                    if (has) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) rec[32 + i * D + f] = oacc[i];
+                    }
+                    do_store = false;
                 }
                 mbar_arrive(bar(B::lempty(ib)));
                 // O tile [16 x D] fp32 staged in shared memory and written by one TMA store (rows
                 // past n_rows of a ragged last window are clipped by the tensor map, reading c14)
                 const int ob = item % C::kNO;
                 float* ost = reinterpret_cast<float*>(smem + C::oOst + ob * C::kOBytes);
-                const bool has = D == 128 || lane < 16;
-                const int f = D == 128 ? 32 * q + lane : 16 * q + lane;  // O^T lane -> feature (M = 64 layout)
 #ifndef F3S_OSTG
 #define F3S_OSTG 0
 #endif
-                if (F3S_OSTG) {  // direct coalesced stores: lane = feature, one row per instruction
+                if (!do_store) {
+                } else if (F3S_OSTG) {  // direct coalesced stores: lane = feature, one row per instruction
                     const int nvalid = min(16, n_rows - 16 * rw);  // ragged last window (reading c14)
                     if (has && !(expt & 64)) {
                         const int64_t ld = (int64_t)H * D;
@@ -794,6 +840,33 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<32 * C::kSB>(tmem);
+    }
+}
+
+// Merge of a split row window: pieces p = 0..np-1 of window k left
+// (m_p, l_p, O_p) for each of its 16 rows (m in log2 units, O unnormalised); in piece order,
+//   M = max_p m_p,  l = sum_p 2^(m_p - M) l_p,  O = sum_p 2^(m_p - M) O_p / l   (0 if l = 0)
+// which is the online-softmax rescaling of Alg.1 l.18/l.21 applied once per piece.
+template <int D>
+__global__ void __launch_bounds__(256) k_split_merge(const int4* __restrict__ ginfo, const float* __restrict__ scratch,
+                                                     float* __restrict__ O, int32_t H, int32_t n_rows) {
+    const int g = blockIdx.x / H, h = blockIdx.x - (blockIdx.x / H) * H;
+    const int4 gi = ginfo[g];
+    const int64_t rec_floats = 32 + 16 * D, stride = (int64_t)H * rec_floats;
+    const float* r0 = scratch + ((int64_t)gi.x * H + h) * rec_floats;
+    for (int e = threadIdx.x; e < 16 * D; e += blockDim.x) {
+        const int i = e / D, f = e - (e / D) * D;
+        float M = -INFINITY;
+        for (int j = 0; j < gi.y; ++j) M = fmaxf(M, r0[j * stride + i]);
+        float l = 0.f, acc = 0.f;
+        for (int j = 0; j < gi.y; ++j) {
+            const float* rj = r0 + j * stride;
+            const float w = exp2f(rj[i] - M);
+            l = fmaf(w, rj[16 + i], l);
+            acc = fmaf(w, rj[32 + i * D + f], acc);
+        }
+        const int64_t row = 16 * (int64_t)gi.z + i;
+        if (row < n_rows) O[(row * H + h) * D + f] = l > 0.f ? acc / l : 0.f;  // empty row -> 0 (reading c4)
     }
 }
 
@@ -875,7 +948,11 @@ f3s_status launch(const AttnArgs& a) {
             attr_err = cudaFuncSetAttribute(k_f3s_sm100<D, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     });
     F3S_CUDA_TRY(attr_err);
-    const int32_t n_items = (int32_t)((int64_t)p.num_rw * a.heads);
+    // default variant: the LPT list with heavy row windows split into pieces (Plan::meta_sub)
+    const bool split = a.lpt && p.n_groups > 0;
+    const int64_t n_items64 = (int64_t)(a.lpt ? p.n_sub : p.num_rw) * a.heads;
+    if (n_items64 > 0x7FFFFFFF) { set_error("too many work items"); return F3S_ERR_UNSUPPORTED; }
+    const int32_t n_items = (int32_t)n_items64;
     const int grid = a.grid_override > 0 ? a.grid_override : (int)std::min<int64_t>(n_items, (int64_t)sms * C::kCtasPerSm);
     // compacted columns per chunk: smaller chunks keep more tiles in flight in the ring
     int chunk_rows = 128;
@@ -884,12 +961,25 @@ f3s_status launch(const AttnArgs& a) {
     int32_t* counter = p.counters + (g_call.fetch_add(1) % kNumCounterSlots);
     F3S_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int32_t), a.stream));
     auto kern = a.trace ? k_f3s_sm100<D, T, true> : k_f3s_sm100<D, T, false>;
+    // split pieces: per-call scratch (a stream-ordered allocation, so concurrent calls on other
+    // streams never share it): one (m[16], l[16], O[16][D]) fp32 record per piece and head
+    float* scratch = nullptr;
+    if (split)
+        F3S_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                     sizeof(float) * (size_t)p.n_pieces * a.heads * (32 + 16 * D), a.stream));
     kern<<<grid, C::kThreads, C::kSmemBytes, a.stream>>>(
-        mq, mk, mv, mo, a.lpt ? p.meta_lpt : p.meta_nat, p.kcols, p.kmasks, counter, n_items, a.heads, p.n_rows,
-        chunk_rows, static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.O,
-        a.scale * 1.4426950408889634f, a.trace, a.trace_chunks, a.expt, mma_sleep_ns);
+        mq, mk, mv, mo, a.lpt ? p.meta_sub : p.meta_nat, p.kcols, p.kmasks, counter,
+        n_items, a.heads, p.n_rows, chunk_rows, static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.O,
+        a.scale * 1.4426950408889634f, a.trace, a.trace_chunks, a.expt, mma_sleep_ns, scratch);
     count_launch();
     F3S_CUDA_TRY(cudaGetLastError());
+    if (split) {
+        k_split_merge<D><<<(int)((int64_t)p.n_groups * a.heads), 256, 0, a.stream>>>(p.ginfo, scratch, a.O, a.heads,
+                                                                                     p.n_rows);
+        count_launch();
+        F3S_CUDA_TRY(cudaGetLastError());
+        F3S_CUDA_TRY(cudaFreeAsync(scratch, a.stream));
+    }
     return F3S_OK;
 }
 

@@ -115,9 +115,18 @@ f3s_status f3s_plan_destroy(f3s_plan_t plan) {
     cudaFree(p->kmasks);
     cudaFree(p->meta_lpt);
     cudaFree(p->meta_nat);
+    cudaFree(p->meta_sub);
+    cudaFree(p->ginfo);
     cudaFree(p->staging);
     delete p;
     return F3S_OK;
+}
+
+f3s_status f3s_plan_set_split(f3s_plan_t plan, int32_t max_chunks) {
+    if (!plan) { set_error("plan is NULL"); return F3S_ERR_INVALID_VALUE; }
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    F3S_CUDA_TRY(cudaSetDevice(p->device));
+    return build_split(p, max_chunks);
 }
 
 f3s_status f3s_plan_get_info(f3s_plan_t plan, f3s_plan_info* info) {
@@ -133,6 +142,8 @@ f3s_status f3s_plan_get_info(f3s_plan_t plan, f3s_plan_info* info) {
     info->total_tcb8 = p.total_tcb8;
     info->device_bytes = p.device_bytes;
     info->build_ms = p.build_ms;
+    info->split_chunks = p.split_chunks;
+    info->split_groups = p.n_groups;
     return F3S_OK;
 }
 

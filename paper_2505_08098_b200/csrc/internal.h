@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/f3s.h"
 
@@ -32,6 +33,15 @@ struct Plan {
     int4* meta_lpt = nullptr;     // [R] {k, start8, width, 0} in LPT order
     int4* meta_nat = nullptr;     // [R] same, natural order (no-reorder ablation)
     int32_t* counters = nullptr;  // work-queue counters, kNumCounterSlots
+    // heavy row-window split: the default kernel walks
+    // meta_sub, the LPT list with every window of more than split_chunks 128-column chunks cut
+    // into pieces of split_chunks chunks (meta_sub[i].w = 1 + global piece index, 0 for an
+    // unsplit window); each piece leaves (m, l, O) partials and k_split_merge combines the
+    // pieces of split window g, in piece order (ginfo[g] = {first global piece, pieces, k, 0})
+    int32_t split_chunks = 0, n_sub = 0, n_groups = 0, n_pieces = 0;
+    int4* meta_sub = nullptr;     // [n_sub]
+    int4* ginfo = nullptr;        // [n_groups]
+    std::vector<int32_t> h_rw, h_rw8, h_order;  // host copies used to (re)build meta_sub
     // e2e staging buffers for f3s_attention_host
     std::mutex staging_mu;
     void* staging = nullptr;
@@ -66,6 +76,9 @@ struct AttnArgs {
 };
 
 f3s_status launch_attention_sm100(const AttnArgs& a);
+// (re)build meta_sub / sinfo with pieces of at most `chunks` 128-column chunks (chunks <= 0: no split)
+f3s_status build_split(Plan* p, int32_t chunks);
+constexpr int kSplitChunkCols = 128;  // column granularity of the split (the kernel's chunk)
 f3s_status launch_attention_simt(const AttnArgs& a);
 
 }  // namespace f3s

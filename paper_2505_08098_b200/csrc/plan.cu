@@ -138,7 +138,7 @@ f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_
     struct Guard { Plan*& p; bool ok = false; ~Guard() { if (!ok && p) {
         cudaFree(p->rw_ptr); cudaFree(p->cols); cudaFree(p->masks); cudaFree(p->rw_order);
         cudaFree(p->rw_natural); cudaFree(p->counters); cudaFree(p->kcols); cudaFree(p->kmasks);
-        cudaFree(p->meta_lpt); cudaFree(p->meta_nat); delete p; p = nullptr; } } } guard{plan};
+        cudaFree(p->meta_lpt); cudaFree(p->meta_nat); cudaFree(p->meta_sub); cudaFree(p->ginfo); delete p; p = nullptr; } } } guard{plan};
     F3S_CUDA_TRY(cudaGetDevice(&plan->device));
     const int32_t R = (n_rows + kRowsPerWindow - 1) / kRowsPerWindow;
     plan->n_rows = n_rows;
@@ -301,6 +301,29 @@ f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_
         count_launch();
         F3S_CUDA_TRY(cudaGetLastError());
     }
+    // heavy-window split list (host: the widths are already here; the order is R ints)
+    plan->h_rw = std::move(h_rw);
+    plan->h_rw8.resize(R + 1);
+    plan->h_order.resize(R);
+    if (R > 0) {
+        F3S_CUDA_TRY(cudaMemcpyAsync(plan->h_rw8.data(), rw8.as<int32_t>(), sizeof(int32_t) * (R + 1),
+                                     cudaMemcpyDeviceToHost, stream));
+        F3S_CUDA_TRY(cudaMemcpyAsync(plan->h_order.data(), plan->rw_order, sizeof(int32_t) * R,
+                                     cudaMemcpyDeviceToHost, stream));
+    }
+    F3S_CUDA_TRY(cudaStreamSynchronize(stream));
+    {
+        // default: a window is split when it alone exceeds half of an SM's even share of all
+        // chunks (counted for one head; more heads only make the share larger)
+        int64_t chunks = 0;
+        for (int32_t k = 0; k < R; ++k)
+            chunks += std::max<int64_t>(1, (plan->h_rw[k + 1] - plan->h_rw[k] + kSplitChunkCols - 1) / kSplitChunkCols);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
+        const int64_t t = std::max<int64_t>(16, (chunks + 2 * sms - 1) / (2 * (int64_t)sms));
+        f3s_status st = build_split(plan, (int32_t)std::min<int64_t>(t, 0x7FFFFFFF));
+        if (st != F3S_OK) return st;
+    }
     F3S_CUDA_TRY(cudaEventRecord(ev1, stream));
     F3S_CUDA_TRY(cudaStreamSynchronize(stream));  // the plan is complete when f3s_plan returns
     F3S_CUDA_TRY(cudaEventElapsedTime(&plan->build_ms, ev0, ev1));
@@ -308,6 +331,44 @@ f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_
                          (int64_t)(sizeof(int32_t) + sizeof(uint16_t)) * (std::max<int64_t>(W, 1) + h_w8);
     guard.ok = true;
     *out = plan;
+    return F3S_OK;
+}
+
+f3s_status build_split(Plan* p, int32_t chunks) {
+    const int32_t R = p->num_rw;
+    std::vector<int4> meta, info;
+    meta.reserve(R);
+    int32_t groups = 0, pieces = 0;
+    for (int32_t i = 0; i < R; ++i) {
+        const int32_t k = p->h_order[i], w = p->h_rw[k + 1] - p->h_rw[k], b8 = p->h_rw8[k];
+        const int64_t nch = std::max<int64_t>(1, (w + kSplitChunkCols - 1) / kSplitChunkCols);
+        if (chunks <= 0 || nch <= chunks) {
+            meta.push_back(make_int4(k, b8, w, 0));
+            continue;
+        }
+        const int32_t np = (int32_t)((nch + chunks - 1) / chunks), step = chunks * kSplitChunkCols;
+        if ((int64_t)pieces + np >= (1 << 23)) { set_error("split: too many pieces"); return F3S_ERR_UNSUPPORTED; }
+        info.push_back(make_int4(pieces, np, k, 0));
+        for (int32_t j = 0; j < np; ++j) {
+            const int32_t c0 = j * step;
+            meta.push_back(make_int4(k, b8 + c0, std::min(step, w - c0), ++pieces));
+        }
+        ++groups;
+    }
+    cudaFree(p->meta_sub);
+    cudaFree(p->ginfo);
+    p->meta_sub = nullptr;
+    p->ginfo = nullptr;
+    F3S_CUDA_TRY(cudaMalloc(&p->meta_sub, sizeof(int4) * std::max<size_t>(meta.size(), 1)));
+    F3S_CUDA_TRY(cudaMalloc(&p->ginfo, sizeof(int4) * std::max<size_t>(info.size(), 1)));
+    if (!meta.empty())
+        F3S_CUDA_TRY(cudaMemcpy(p->meta_sub, meta.data(), sizeof(int4) * meta.size(), cudaMemcpyHostToDevice));
+    if (!info.empty())
+        F3S_CUDA_TRY(cudaMemcpy(p->ginfo, info.data(), sizeof(int4) * info.size(), cudaMemcpyHostToDevice));
+    p->split_chunks = chunks;
+    p->n_sub = (int32_t)meta.size();
+    p->n_groups = groups;
+    p->n_pieces = pieces;
     return F3S_OK;
 }
 

@@ -31,7 +31,7 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("n_rows", ctypes.c_int32), ("n_cols", ctypes.c_int32), ("num_rw", ctypes.c_int32),
                 ("max_width", ctypes.c_int32), ("nnz", ctypes.c_int64), ("total_cols", ctypes.c_int64),
                 ("total_tcb8", ctypes.c_int64), ("device_bytes", ctypes.c_int64), ("build_ms", ctypes.c_float),
-                ("reserved", ctypes.c_float)]
+                ("reserved", ctypes.c_float), ("split_chunks", ctypes.c_int32), ("split_groups", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -43,6 +43,7 @@ _lib.f3s_plan_rows.argtypes = [_vp, _vp, _i32, _i32, _vp, ctypes.POINTER(_vp)]
 _lib.f3s_plan_destroy.argtypes = [_vp]
 _lib.f3s_plan_get_info.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
 _lib.f3s_plan_export.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.f3s_plan_set_split.argtypes = [_vp, _i32]
 _lib.f3s_attention.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_trace.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]
@@ -53,12 +54,12 @@ _lib.f3s_status_string.argtypes = [_i32]
 _lib.f3s_status_string.restype = ctypes.c_char_p
 _lib.f3s_last_error.restype = ctypes.c_char_p
 _lib.f3s_launch_count.restype = _i64
-for _name in ("f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export",
+for _name in ("f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
               "f3s_attention", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows",
               "f3s_partition_at"):
     getattr(_lib, _name).restype = _i32
 
-EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export",
+EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
             "f3s_attention", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows", "f3s_partition_at",
             "f3s_status_string", "f3s_last_error", "f3s_launch_count"]
 
@@ -117,6 +118,11 @@ class Plan:
         _check(_lib.f3s_plan_export(self._h, rw_ptr.ctypes.data, cols.ctypes.data, masks.ctypes.data,
                                     order.ctypes.data), "f3s_plan_export")
         return rw_ptr, cols[:W], masks[:W], order[:R]
+
+    def set_split(self, max_chunks: int) -> None:
+        """f3s_plan_set_split: heavy row windows processed as pieces of <= max_chunks 128-column
+        chunks (0: never split)."""
+        _check(_lib.f3s_plan_set_split(self._h, int(max_chunks)), "f3s_plan_set_split")
 
     def destroy(self) -> None:
         if self._h:

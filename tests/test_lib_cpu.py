@@ -53,6 +53,7 @@ def test_host_argument_validation(f3s):
     st = f3s._lib.f3s_plan(None, None, 4, None, ctypes.byref(ctypes.c_void_p()))
     assert st == f3s.INVALID_VALUE
     assert b"NULL" in f3s._lib.f3s_last_error()
+    assert f3s._lib.f3s_plan_set_split(None, 4) == f3s.INVALID_VALUE
 
 
 def nnz_of_range(rp, b, e):
