@@ -38,7 +38,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="arxiv")
-    ap.add_argument("--variant", default="default", choices=["default", "no_reorder", "simt"])
+    ap.add_argument("--variant", default="default", choices=["default", "no_reorder", "simt", "one_head"])
     ap.add_argument("--dtype", default=None, choices=[None, "fp16", "bf16"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -147,7 +147,9 @@ f3s_status f3s_attention(f3s_plan_t plan, const void* Q, const void* K, const vo
 typedef enum {
     F3S_VARIANT_DEFAULT = 0, /* tcgen05 + TMA gather kernel, LPT-ordered persistent queue       */
     F3S_VARIANT_NO_REORDER = 1, /* same kernel, row windows in natural order */
-    F3S_VARIANT_SIMT = 2     /* CUDA-core reference kernel of the same dataflow (no tensor core) */
+    F3S_VARIANT_SIMT = 2,    /* CUDA-core reference kernel of the same dataflow (no tensor core) */
+    F3S_VARIANT_ONE_HEAD = 3 /* tcgen05 kernel with one head per chunk even where the default packs
+                                4 heads of windows <= 32 columns wide into one chunk (d = 64)   */
 } f3s_variant;
 
 f3s_status f3s_attention_ex(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,

@@ -42,8 +42,14 @@ namespace {
 
 using namespace sm100;
 
-template <int D>
+// HG = heads per chunk.  HG = 1: a chunk holds up to 128 compacted columns of one head.
+// HG = 4 (d = 64, every row window at most 32 columns wide, e.g. batched small graphs): a chunk
+// holds the window's columns for 4 heads, head g in tile rows / S^T lanes 32g .. 32g+31, so
+// softmax warp q works on head q alone (row max within the warp) and the per-chunk pipeline
+// cost is paid once per 4 heads.
+template <int D, int HG = 1>
 struct Cfg {
+    static_assert(HG == 1 || (HG == 4 && D == 64), "head groups: d = 64 only");
     static constexpr int P = D / 64;                 // 128-byte panels per gathered row of one head
     static constexpr int kGroupBytes = 1024 * P;     // 8 gathered rows (one swizzle atom per panel)
     static constexpr int kMaxRows = 128;             // compacted columns per chunk at most (MMA1 M = 128)
@@ -55,16 +61,18 @@ struct Cfg {
 #ifndef F3S_KNQ128
 #define F3S_KNQ128 4
 #endif
-    static constexpr int kRingK = 64 * 1024;
-    static constexpr int kRingV = D == 128 ? F3S_RINGV128_KB * 1024 : 88 * 1024;
+    static constexpr int kRingK = HG == 4 ? 48 * 1024 : 64 * 1024;
+    static constexpr int kRingV = HG == 4 ? 64 * 1024 : D == 128 ? F3S_RINGV128_KB * 1024 : 88 * 1024;
     static constexpr int kRingBytes = kRingK + kRingV;
     static constexpr int kNS = D == 128 ? 20 : 22;   // chunk slots (ids, masks, descriptor, barriers)
-    static constexpr int kNQ = D == 128 ? F3S_KNQ128 : 12;  // Q tile slots (items in flight per CTA)
-    static constexpr int kQBytes = 16 * D * 2;
+    static constexpr int kNQ = HG == 4 ? 6 : D == 128 ? F3S_KNQ128 : 12;  // Q tile slots (items in flight per CTA)
+    static constexpr int kQBytes = 16 * D * 2 * HG;  // HG head tiles of 16 x D
     static constexpr int kPBytes = 16 * kMaxRows * 2;
     static constexpr int kSB = 4;                    // S/P/O buffers in flight (TMEM and SMEM)
-    static constexpr int kNO = 2;                    // O staging tiles (16 x D fp32) for the TMA store
-    static constexpr int kOBytes = 16 * D * 4;
+    static constexpr int kNO = HG == 4 ? 1 : 2;      // O staging tiles (16 x HG*D fp32) for the TMA store
+    static constexpr int kOBytes = 16 * D * 4 * HG;
+    static constexpr int kTmemCols = HG == 4 ? 512 : 128;  // S^T and O^T: kSB x HG buffers of 16 columns each
+    static_assert(2 * 16 * kSB * HG <= kTmemCols, "TMEM columns");
     static constexpr int kSlotBytes = 32 + 128 * 4 + 128 * 2;  // sizeof(Slot)
     static constexpr int oRing = 0;                  // K ring, then V ring
     static constexpr int oRingV = kRingK;
@@ -108,8 +116,8 @@ struct Cfg {
     static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 };
 
-template <int D> struct Bars {
-    using C = Cfg<D>;
+template <int D, int HG> struct Bars {
+    using C = Cfg<D, HG>;
     __host__ __device__ static constexpr int idxfull(int s) { return s; }
     __host__ __device__ static constexpr int kfull(int s) { return C::kNS + s; }
     __host__ __device__ static constexpr int vfull(int s) { return 2 * C::kNS + s; }
@@ -187,8 +195,8 @@ template <typename T> __device__ __forceinline__ uint32_t pack2(float lo, float 
 template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) { return pack_f16x2(lo, hi); }
 template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) { return pack_bf16x2(lo, hi); }
 
-template <int D, typename T, bool kDiag>
-__global__ void __launch_bounds__(Cfg<D>::kThreads, Cfg<D>::kCtasPerSm)
+template <int D, typename T, bool kDiag, int HG>
+__global__ void __launch_bounds__(Cfg<D, HG>::kThreads, Cfg<D, HG>::kCtasPerSm)
 k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const int4* __restrict__ meta,
             const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
@@ -196,8 +204,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float* __restrict__ O, float scale_log2,
             uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt, uint32_t mma_sleep_ns,
             float* __restrict__ scratch) {
-    using C = Cfg<D>;
-    using B = Bars<D>;
+    using C = Cfg<D, HG>;
+    using B = Bars<D, HG>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sb = smem_u32(smem);
     if (sb & 1023) __trap();  // swizzled tiles need 1024-byte alignment
@@ -269,7 +277,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         tma_prefetch_desc(&tmO);
     }
     if (warp == 1) {
-        tmem_alloc<32 * C::kSB>(sb + C::oTmem);
+        tmem_alloc<C::kTmemCols>(sb + C::oTmem);
         tmem_relinquish();
     }
     fence_proxy_async_smem();
@@ -289,7 +297,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             int4 mt = make_int4(0, 0, 0, 0);
             if (lane < C::kBatch) {
                 it = atomicAdd(counter, 1);
-                if (it < n_items) mt = __ldg(meta + it / H);
+                if (it < n_items) mt = __ldg(meta + it / (H / HG));
             }
             __syncwarp();
             if (lane == 0) lap(1);
@@ -300,7 +308,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const int32_t w = __shfl_sync(0xffffffffu, mt.z, b);
                 const int32_t sp = __shfl_sync(0xffffffffu, mt.w, b);
                 if (itb >= n_items) { done = true; continue; }
-                const int32_t h = itb - (itb / H) * H;
+                const int32_t h = (itb - (itb / (H / HG)) * (H / HG)) * HG;  // (first) head
                 const int nch = w > 0 ? (w + chunk_rows - 1) / chunk_rows : 1;
                 const int qs = qseq % C::kNQ;
                 const int qph = (qseq / C::kNQ) & 1;
@@ -316,7 +324,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         sl.rows = rows;
                         sl.qslot = qs;
                         sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2) | (sp << 8);
-                        sl.ralloc = rows > 0 ? ((rows + 15) & ~15) : 0;
+                        sl.ralloc = rows > 0 ? (HG == 1 ? ((rows + 15) & ~15) : C::kMaxRows) : 0;
                         const uint32_t fb = bar(B::idxfull(s));
                         if (rows > 0) {
                             const uint32_t r8 = (uint32_t)((rows + 7) & ~7);
@@ -371,9 +379,11 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 if (lane == 0) {
                     mbar_arrive_expect_tx(bar(B::qfull(qs)), C::kQBytes);
 #pragma unroll
-                    for (int pp = 0; pp < C::P; ++pp)
-                        tma_load_2d(sb + C::oQ + qs * C::kQBytes + pp * 2048, &tmQ, bar(B::qfull(qs)),
-                                    h * D + 64 * pp, 16 * k);
+                    for (int g = 0; g < HG; ++g)
+#pragma unroll
+                        for (int pp = 0; pp < C::P; ++pp)
+                            tma_load_2d(sb + C::oQ + qs * C::kQBytes + g * 16 * D * 2 + pp * 2048, &tmQ,
+                                        bar(B::qfull(qs)), (h + g) * D + 64 * pp, 16 * k);
                 }
             }
             const uint32_t tile = (uint32_t)(sl.ralloc / 8) * C::kGroupBytes;
@@ -445,16 +455,19 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const uint32_t vt = sb + C::oRingV + sl.pad + pnl * 1024;
             const uint8_t* kbase = Kg + (int64_t)h * D * 2 + piece * 16;
             const uint8_t* vbase = Vg + (int64_t)h * D * 2 + piece * 16;
-            const int ops = (expt & 8) ? 0 : (rows + kRowsPerOp - 1) / kRowsPerOp;
+            // HG = 1: tile row r = compacted column r.  HG = 4: tile row 32g + r = column r of head h + g.
+            const int ops = (expt & 8) ? 0 : (HG == 1 ? (rows + kRowsPerOp - 1) / kRowsPerOp : C::kMaxRows / kRowsPerOp);
 #pragma unroll 2
             for (int t = lw; t < ops; t += C::kLoaderWarps) {
-                const int r = t * kRowsPerOp + rsub;
+                const int tr = t * kRowsPerOp + rsub;  // tile row
+                const int r = HG == 1 ? tr : (tr & 31);
                 if (r < rows) {
                     const int64_t j = sl.cols[r];
-                    const uint32_t o = (uint32_t)(r >> 3) * C::kGroupBytes + (uint32_t)(r & 7) * 128 +
-                                       (uint32_t)((cc ^ (r & 7)) << 4);
-                    cp_async_16(kt + o, kbase + j * ldb);
-                    cp_async_16(vt + o, vbase + j * ldb);
+                    const int64_t src = j * ldb + (HG == 1 ? 0 : (int64_t)(tr >> 5) * D * 2);
+                    const uint32_t o = (uint32_t)(tr >> 3) * C::kGroupBytes + (uint32_t)(tr & 7) * 128 +
+                                       (uint32_t)((cc ^ (tr & 7)) << 4);
+                    cp_async_16(kt + o, kbase + src);
+                    cp_async_16(vt + o, vbase + src);
                 }
             }
             cp_async_mbar_arrive(kfb);
@@ -486,10 +499,15 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const uint64_t a0 = dK + ((sb + C::oRing + roff) >> 4);
                 const uint64_t b0 = dQ + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
                 if (rows > 0 && !(expt & 4)) {
+                    // HG > 1: one M = 128 MMA group per head g against its own Q tile into its own
+                    // S^T buffer; only lanes 32g .. 32g+31 (head g's tile rows) are read back
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk)
-                        mma_f16_ss_warp(tmem + b * 16, a0 + (((kk >> 2) * 1024 + (kk & 3) * 32) >> 4),
-                                        b0 + (((kk >> 2) * 2048 + (kk & 3) * 32) >> 4), idesc1, kk > 0 ? 1u : 0u);
+                    for (int g = 0; g < HG; ++g)
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk)
+                            mma_f16_ss_warp(tmem + (b * HG + g) * 16, a0 + (((kk >> 2) * 1024 + (kk & 3) * 32) >> 4),
+                                            b0 + ((g * 16 * D * 2 + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4), idesc1,
+                                            kk > 0 ? 1u : 0u);
                 }
                 mma_commit_warp(bar(B::sfull(b)));
                 mma_commit_warp(bar(B::kempty(s)));
@@ -514,9 +532,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     const uint64_t a0 = dV + ((sb + C::oRingV + slots[s].pad) >> 4);
                     const uint64_t b0 = dP + ((sb + C::oP + b * C::kPBytes) >> 4);
                     const int nsteps = (rows + 15) >> 4;
-                    for (int st = 0; st < nsteps; ++st)
-                        mma_f16_ss_warp(tmem + 16 * C::kSB + b * 16, a0 + ((st * 2 * C::kGroupBytes) >> 4),
-                                        b0 + ((st * 512) >> 4), idesc2, st > 0 ? 1u : 0u);
+#pragma unroll
+                    for (int g = 0; g < HG; ++g)  // head g: tile rows / P^T columns 32g .. (HG > 1)
+                        for (int st = 0; st < nsteps; ++st)
+                            mma_f16_ss_warp(tmem + 16 * C::kSB * HG + (b * HG + g) * 16,
+                                            a0 + ((g * 4 * C::kGroupBytes + st * 2 * C::kGroupBytes) >> 4),
+                                            b0 + ((g * 1024 + st * 512) >> 4), idesc2, st > 0 ? 1u : 0u);
                 }
                 mma_commit_warp(bar(B::ofull(b)));
                 mma_commit_warp(bar(B::empty(s)));
@@ -570,7 +591,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 ++seq;
                 continue;
             }
-            const uint32_t mask = p < rows ? (uint32_t)sl.masks[p] : 0u;
+            // S^T lane p <-> compacted column p (HG = 1), or column `lane` of head q (HG = 4)
+            const int col = HG == 1 ? p : lane;
+            const uint32_t mask = col < rows ? (uint32_t)sl.masks[col] : 0u;
             const int rw = sl.rw, hd = sl.head, sp = flags >> 8;  // split piece (0: none)
             mbar_wait(bar(B::sfull(b)), bph);
             tc_fence_after();
@@ -588,15 +611,18 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                 for (int i = 0; i < 16; ++i) x[i] = (expt & 32) ? 0.f : -INFINITY;
             } else {
-                tmem_ld_32x32b_x16(tmem + tl + b * 16, x);
+                tmem_ld_32x32b_x16(tmem + tl + (b * HG + (HG > 1 ? q : 0)) * 16, x);
 #pragma unroll
                 for (int i = 0; i < 16; ++i) x[i] = ((mask >> i) & 1u) ? x[i] * scale_log2 : -INFINITY;  // Alg.1 l.14
             }
-            // chunk row max (Alg.1 l.16): warp butterfly + 4-warp combine
+            // chunk row max (Alg.1 l.16): warp butterfly (+ 4-warp combine when the chunk's columns
+            // span the four warps, HG = 1)
             const float rm = ((expt & 32) || !act) ? ((expt & 32) ? 0.f : -INFINITY) : rowreduce16(x, lane, OpMax());
-            if (!(lane & 1)) red[(b * 4 + q) * 16 + ((lane >> 1) & 15)] = rm;
-            if (p == 0) lap(2);
-            named_bar_sync(1 + wg, 128);
+            if (HG == 1) {
+                if (!(lane & 1)) red[(b * 4 + q) * 16 + ((lane >> 1) & 15)] = rm;
+                if (p == 0) lap(2);
+                named_bar_sync(1 + wg, 128);
+            }
             // P_b / corr_b are free once the correction group consumed chunk seq - kSB
             mbar_wait(bar(B::pempty(b)), bph ^ 1);
             // S^T_b was loaded above; releasing it only now (after the P-tile wait) also keeps the
@@ -611,14 +637,19 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             uint4* prow = reinterpret_cast<uint4*>(smem + C::oP + b * C::kPBytes + (p >> 3) * 256 + (p & 7) * 32);
             const int sw = (p >> 2) & 1;
             float av[16], pv[16];
-            float cm[16];  // chunk row max (4-warp combine)
+            float cm[16];  // chunk row max
+            if (HG == 1) {  // 4-warp combine
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                const float4 w0 = r4[g], w1 = r4[4 + g], w2 = r4[8 + g], w3 = r4[12 + g];
-                cm[4 * g] = fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x));
-                cm[4 * g + 1] = fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y));
-                cm[4 * g + 2] = fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z));
-                cm[4 * g + 3] = fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w));
+                for (int g = 0; g < 4; ++g) {
+                    const float4 w0 = r4[g], w1 = r4[4 + g], w2 = r4[8 + g], w3 = r4[12 + g];
+                    cm[4 * g] = fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x));
+                    cm[4 * g + 1] = fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y));
+                    cm[4 * g + 2] = fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z));
+                    cm[4 * g + 3] = fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w));
+                }
+            } else {  // the warp holds all columns of its head: lane 2i has row i's max
+#pragma unroll
+                for (int i = 0; i < 16; ++i) cm[i] = __shfl_sync(0xffffffffu, rm, 2 * i);
             }
             if (flags & 1) {  // item's first chunk: m_o = floor, l_o = 0, nothing to rescale (alpha = 0)
 #pragma unroll
@@ -722,6 +753,48 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
                 stamp(seq, 6);
                 lap(1);
+            }
+            if constexpr (HG > 1) {
+                // head groups: one chunk per item (every window <= 32 columns), so O_g = O^T_g / l_g
+                // for each head g of the group, staged as one [16 x HG*D] tile and stored by one TMA
+                const int ib = item % C::kLB;
+                mbar_wait(bar(B::lfull(ib)), (item / C::kLB) & 1);
+                float* ost = reinterpret_cast<float*>(smem + C::oOst);
+                if (lead) bulk_wait_group_read<0>();  // the previous item's store has read the tile
+                named_bar_sync(3, 128);
+                const bool has = lane < 16;           // O^T lane -> feature 16q + lane (M = 64 layout)
+                const int f = 16 * q + lane;
+#pragma unroll 1
+                for (int g = 0; g < HG; ++g) {
+                    float ov[16];
+                    tmem_ld_32x32b_x16(tmem + tl + 16 * C::kSB * HG + (b * HG + g) * 16, ov);
+                    const float4* l4 = reinterpret_cast<const float4*>(lred + (ib * 4 + g) * 16);  // head g's row sums
+                    if (has) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const float4 lv = l4[u];
+                            const float lt[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                const int i = 4 * u + v;  // empty row (l = 0) -> 0 (reading c4)
+                                ost[i * (HG * D) + g * D + f] = (rows > 0 && lt[v] > 0.f) ? ov[i] * rcp_approx(lt[v]) : 0.f;
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(bar(B::pempty(b)));
+                mbar_arrive(bar(B::lempty(ib)));
+                fence_proxy_async_smem();
+                named_bar_sync(3, 128);
+                if (lead) {
+                    if (!(expt & 64)) tma_store_2d(&tmO, sb + C::oOst, hd * D, 16 * rw);
+                    bulk_commit_group();
+                    if (F3S_TRACE_EV0 < 3) stamp(seq, 7);
+                }
+                ++item;
+                ++seq;
+                continue;
             }
             const float4* a4 = reinterpret_cast<const float4*>(corr[b].alpha);
             if (rows > 0) {
@@ -839,7 +912,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<32 * C::kSB>(tmem);
+        tmem_dealloc<C::kTmemCols>(tmem);
     }
 }
 
@@ -914,9 +987,9 @@ f3s_status make_map(CUtensorMap* map, const void* base, f3s_dtype dtype, int64_t
 
 std::atomic<uint32_t> g_call{0};
 
-template <int D, typename T>
+template <int D, typename T, int HG>
 f3s_status launch(const AttnArgs& a) {
-    using C = Cfg<D>;
+    using C = Cfg<D, HG>;
     const Plan& p = *a.plan;
     const int64_t out_bytes = (int64_t)p.n_rows * a.heads * D * 4;
     if (p.nnz == 0 || p.n_cols == 0) {  // every row is empty: O = 0 (reading c4)
@@ -928,7 +1001,7 @@ f3s_status launch(const AttnArgs& a) {
     if ((st = make_map(&mq, a.Q, a.dtype, (int64_t)a.heads * D, p.n_rows, 16)) != F3S_OK) return st;
     if ((st = make_map(&mk, a.K, a.dtype, (int64_t)a.heads * D, p.n_cols, 1)) != F3S_OK) return st;
     if ((st = make_map(&mv, a.V, a.dtype, (int64_t)a.heads * D, p.n_cols, 1)) != F3S_OK) return st;
-    if ((st = make_map(&mo, a.O, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (int64_t)a.heads * D, p.n_rows, D, 16,
+    if ((st = make_map(&mo, a.O, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (int64_t)a.heads * D, p.n_rows, D * HG, 16,
                        CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK)
         return st;
 
@@ -943,24 +1016,28 @@ f3s_status launch(const AttnArgs& a) {
     static std::once_flag attr_once;
     cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [&] {
-        attr_err = cudaFuncSetAttribute(k_f3s_sm100<D, T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        attr_err = cudaFuncSetAttribute(k_f3s_sm100<D, T, false, HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        C::kSmemBytes);
         if (attr_err == cudaSuccess)
-            attr_err = cudaFuncSetAttribute(k_f3s_sm100<D, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+            attr_err = cudaFuncSetAttribute(k_f3s_sm100<D, T, true, HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            C::kSmemBytes);
     });
     F3S_CUDA_TRY(attr_err);
     // default variant: the LPT list with heavy row windows split into pieces (Plan::meta_sub)
     const bool split = a.lpt && p.n_groups > 0;
-    const int64_t n_items64 = (int64_t)(a.lpt ? p.n_sub : p.num_rw) * a.heads;
+    if (split && HG > 1) { set_error("internal: head groups with split windows"); return F3S_ERR_INTERNAL; }
+    const int64_t n_items64 = (int64_t)(a.lpt ? p.n_sub : p.num_rw) * (a.heads / HG);
     if (n_items64 > 0x7FFFFFFF) { set_error("too many work items"); return F3S_ERR_UNSUPPORTED; }
     const int32_t n_items = (int32_t)n_items64;
     const int grid = a.grid_override > 0 ? a.grid_override : (int)std::min<int64_t>(n_items, (int64_t)sms * C::kCtasPerSm);
     // compacted columns per chunk: smaller chunks keep more tiles in flight in the ring
     int chunk_rows = 128;
-    if (const char* env = getenv("F3S_CHUNK_ROWS")) chunk_rows = std::max(16, std::min(128, atoi(env) / 16 * 16));
+    if (const char* env = getenv("F3S_CHUNK_ROWS"))
+        if (HG == 1) chunk_rows = std::max(16, std::min(128, atoi(env) / 16 * 16));  // (HG > 1: one chunk per item)
     static uint32_t mma_sleep_ns = getenv("F3S_MMA_SLEEP") ? (uint32_t)atoi(getenv("F3S_MMA_SLEEP")) : 0u;
     int32_t* counter = p.counters + (g_call.fetch_add(1) % kNumCounterSlots);
     F3S_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int32_t), a.stream));
-    auto kern = a.trace ? k_f3s_sm100<D, T, true> : k_f3s_sm100<D, T, false>;
+    auto kern = a.trace ? k_f3s_sm100<D, T, true, HG> : k_f3s_sm100<D, T, false, HG>;
     // split pieces: per-call scratch (a stream-ordered allocation, so concurrent calls on other
     // streams never share it): one (m[16], l[16], O[16][D]) fp32 record per piece and head
     float* scratch = nullptr;
@@ -986,8 +1063,17 @@ f3s_status launch(const AttnArgs& a) {
 }  // namespace
 
 f3s_status launch_attention_sm100(const AttnArgs& a) {
-    if (a.dtype == F3S_FP16) return a.d == 64 ? launch<64, __half>(a) : launch<128, __half>(a);
-    return a.d == 64 ? launch<64, __nv_bfloat16>(a) : launch<128, __nv_bfloat16>(a);
+    // head groups of 4 when every row window fits one 32-column block (d = 64): the per-chunk
+    // pipeline cost is shared by 4 heads (batched small graphs).  F3S_HG1=1 forces HG = 1.
+    static const bool hg1 = getenv("F3S_HG1") != nullptr;
+    const Plan& p = *a.plan;
+    const bool hg4 = !hg1 && !a.one_head && a.d == 64 && a.heads % 4 == 0 && p.max_width <= 32 && p.n_groups == 0;
+    if (a.dtype == F3S_FP16) {
+        if (hg4) return launch<64, __half, 4>(a);
+        return a.d == 64 ? launch<64, __half, 1>(a) : launch<128, __half, 1>(a);
+    }
+    if (hg4) return launch<64, __nv_bfloat16, 4>(a);
+    return a.d == 64 ? launch<64, __nv_bfloat16, 1>(a) : launch<128, __nv_bfloat16, 1>(a);
 }
 
 }  // namespace f3s

@@ -54,10 +54,12 @@ static f3s_status run_attention(f3s_plan_t plan, const void* Q, const void* K, c
     a.trace_chunks = trace_chunks < 0 ? 0 : trace_chunks;
     a.expt = trace_chunks < 0 ? -trace_chunks : 0;
     a.grid_override = grid;
+    a.one_head = variant == F3S_VARIANT_ONE_HEAD;
     if (a.plan->n_rows == 0) return F3S_OK;
     switch (variant) {
         case F3S_VARIANT_DEFAULT:
-        case F3S_VARIANT_NO_REORDER: return launch_attention_sm100(a);
+        case F3S_VARIANT_NO_REORDER:
+        case F3S_VARIANT_ONE_HEAD: return launch_attention_sm100(a);
         case F3S_VARIANT_SIMT: return launch_attention_simt(a);
         default: set_error("unknown variant"); return F3S_ERR_INVALID_VALUE;
     }

@@ -73,6 +73,7 @@ struct AttnArgs {
     int32_t trace_chunks = 0;
     int32_t grid_override = 0;
     int32_t expt = 0;           // sensitivity experiments (diagnostics only)
+    bool one_head = false;      // F3S_VARIANT_ONE_HEAD: no head groups
 };
 
 f3s_status launch_attention_sm100(const AttnArgs& a);

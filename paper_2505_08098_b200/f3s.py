@@ -23,8 +23,9 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 OK, INVALID_VALUE, INVALID_CSR, UNSUPPORTED, OUT_OF_MEMORY, CUDA, INTERNAL = range(7)
 FP16, BF16 = 0, 1
-VARIANT_DEFAULT, VARIANT_NO_REORDER, VARIANT_SIMT = 0, 1, 2
-VARIANTS = {"default": VARIANT_DEFAULT, "no_reorder": VARIANT_NO_REORDER, "simt": VARIANT_SIMT}
+VARIANT_DEFAULT, VARIANT_NO_REORDER, VARIANT_SIMT, VARIANT_ONE_HEAD = 0, 1, 2, 3
+VARIANTS = {"default": VARIANT_DEFAULT, "no_reorder": VARIANT_NO_REORDER, "simt": VARIANT_SIMT,
+            "one_head": VARIANT_ONE_HEAD}
 
 
 class PlanInfo(ctypes.Structure):
