@@ -224,7 +224,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     const bool prof = kDiag && trace != nullptr && trace_chunks == 0;
     // expt (f3s_attention_trace only; results are wrong): bit0 no exp work in the softmax,
     // bit1 no MMA2, bit2 no MMA1, bit3 no K/V gathers, bit4 consumer-side proxy fence before the
-    // MMAs, bit5 no S load / row max in the softmax, bit6 no O stores.  0 in every real call.
+    // MMAs, bit5 no S load / row max in the softmax, bit6 no O stores, bit7 no correction work.  0 in
+    // every real call.
     uint32_t pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t pt0 = prof ? (uint32_t)clock() : 0;  // SM cycles (cheap to read, unlike globaltimer)
     auto lap = [&](int k) {  // charge the cycles since the previous lap to counter k
@@ -797,6 +798,18 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 continue;
             }
             const float4* a4 = reinterpret_cast<const float4*>(corr[b].alpha);
+            if (expt & 128) {  // diagnostics: the correction group only keeps the barrier protocol
+                tc_fence_before();
+                mbar_arrive(bar(B::pempty(b)));
+                if (flags & 2) {
+                    const int ib = item % C::kLB;
+                    mbar_wait(bar(B::lfull(ib)), (item / C::kLB) & 1);
+                    mbar_arrive(bar(B::lempty(ib)));
+                    ++item;
+                }
+                ++seq;
+                continue;
+            }
             if (rows > 0) {
                 float ov[16];
                 tmem_ld_32x32b_x16(tmem + tl + 16 * C::kSB + b * 16, ov);

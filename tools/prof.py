@@ -41,7 +41,8 @@ def main():
         print(f"  {nm:24s} {tot[k]:9.1f} us/CTA")
     if a.out:
         np.save(a.out, tr)
-    for ex, nm in [(1, "no softmax exp"), (2, "no MMA2"), (4, "no MMA1"), (6, "no MMAs"), (8, "no gathers"), (9, "no gathers+exp"), (14, "no gathers, no MMAs"), (16, "consumer proxy fence"), (32, "no S ld/max"), (33, "no S ld/max/exp"), (64, "no O stores"), (46, "skeleton: 2+4+8+32"), (110, "skeleton+no O stores")]:
+    for ex, nm in [(1, "no softmax exp"), (2, "no MMA2"), (4, "no MMA1"), (6, "no MMAs"), (8, "no gathers"), (9, "no gathers+exp"), (14, "no gathers, no MMAs"), (16, "consumer proxy fence"), (32, "no S ld/max"), (33, "no S ld/max/exp"), (64, "no O stores"), (46, "skeleton: 2+4+8+32"), (110, "skeleton+no O stores"),
+                   (128, "no correction work"), (128 + 33, "no corr, no S ld/exp"), (128 + 46, "skeleton, no corr")]:
         f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=-ex)
         s.record(); f3s.attention_trace(p, Q, K, V, O, scale=w.scale, trace_chunks=-ex); e.record(); torch.cuda.synchronize()
         print(f"  experiment {ex:2d} ({nm:22s}): {s.elapsed_time(e):.3f} ms")
