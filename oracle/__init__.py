@@ -41,6 +41,8 @@ def _load():
         lib.oracle_attention.argtypes = [i32, i32, vp, vp, i32, i32, i32, vp, vp, vp, ctypes.c_double, vp, i32, vp, i32]
         lib.oracle_plan.argtypes = [i32, i32, vp, vp, pp, pp, pp, pp, ctypes.POINTER(i64)]
         lib.oracle_free.argtypes = [vp]
+        lib.oracle_attention_backward.argtypes = [i32, i32, vp, vp, i32, i32, vp, vp, vp, vp, ctypes.c_double, vp, vp, vp]
+        lib.oracle_attention_f64.argtypes = [i32, i32, vp, vp, i32, i32, vp, vp, vp, ctypes.c_double, vp]
         lib.oracle_num_threads.restype = i32
         _lib = lib
     return _lib
@@ -74,6 +76,38 @@ def attention(row_ptr, col_idx, Q, K, V, *, scale: float, dtype: str = "fp16", n
     if rc:
         raise ValueError(f"oracle_attention: invalid input (code {rc})")
     return out
+
+
+def attention_f64(row_ptr, col_idx, Q, K, V, *, scale: float) -> np.ndarray:
+    """Eq.1 on fp64 inputs Q [n, H, d], K, V [n_cols, H, d] (the function differentiated by
+    attention_backward)."""
+    lib = _load()
+    row_ptr = _c(row_ptr, np.int32)
+    col_idx = _c(col_idx, np.int32) if len(col_idx) else np.zeros(1, np.int32)
+    Q, K, V = _c(Q, np.float64), _c(K, np.float64), _c(V, np.float64)
+    n_rows, H, d = Q.shape
+    out = np.empty(Q.shape, np.float64)
+    rc = lib.oracle_attention_f64(n_rows, K.shape[0], row_ptr.ctypes.data, col_idx.ctypes.data, H, d, Q.ctypes.data,
+                                  K.ctypes.data, V.ctypes.data, float(scale), out.ctypes.data)
+    if rc:
+        raise ValueError(f"oracle_attention_f64: invalid input (code {rc})")
+    return out
+
+
+def attention_backward(row_ptr, col_idx, Q, K, V, dO, *, scale: float):
+    """fp64 (dQ, dK, dV) of Eq.1 for the given dO; all inputs fp64 arrays [rows, H, d]."""
+    lib = _load()
+    row_ptr = _c(row_ptr, np.int32)
+    col_idx = _c(col_idx, np.int32) if len(col_idx) else np.zeros(1, np.int32)
+    Q, K, V, dO = _c(Q, np.float64), _c(K, np.float64), _c(V, np.float64), _c(dO, np.float64)
+    n_rows, H, d = Q.shape
+    dQ, dK, dV = np.empty_like(Q), np.empty_like(K), np.empty_like(V)
+    rc = lib.oracle_attention_backward(n_rows, K.shape[0], row_ptr.ctypes.data, col_idx.ctypes.data, H, d,
+                                       Q.ctypes.data, K.ctypes.data, V.ctypes.data, dO.ctypes.data, float(scale),
+                                       dQ.ctypes.data, dK.ctypes.data, dV.ctypes.data)
+    if rc:
+        raise ValueError(f"oracle_attention_backward: invalid input (code {rc})")
+    return dQ, dK, dV
 
 
 @dataclass

@@ -22,8 +22,14 @@
  *                    sorted by TCB count ceil(w/8) descending, ties by index (P:402,
  *                    reading c13).
  *
+ *  oracle_attention_backward   dQ, dK, dV of Eq.1 for a given dO,
+ *                    the softmax Jacobian and the transposed SDDMM/SpMM written out, in fp64;
+ *                    oracle_attention_f64 is the same forward on fp64 inputs (its FD target).
+ *
  * Pins: tests/test_oracle.py (dense brute force, torch SDPA in fp64, closed forms,
- * invariants, SPEC worked examples).  No function here is "parity unpinned".
+ * invariants, SPEC worked examples), tests/test_oracle_backward.py (central finite
+ * differences, torch autograd of dense masked SDPA in fp64, closed forms).  No function here
+ * is "parity unpinned".
  */
 #include <math.h>
 #include <stdint.h>
@@ -139,6 +145,146 @@ int oracle_attention(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr, con
         free(qd);
         free(acc);
     }
+    return bad ? 2 : 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* backward ("SpMM and SDDMM operations in      */
+/* reverse order")                                                           */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * Gradients of O = softmax_row(scale * (Q K^T) (.) A) V (Eq.1, same readings c1-c4 as
+ * oracle_attention) with respect to Q, K and V, given dO = dL/dO; all values fp64 ([n, H, d]
+ * row-major; Q, dO, dQ have n_rows rows, K, V, dK, dV have n_cols rows).  Per row i and head h,
+ * with N_i the sorted unique neighbours (empty rows contribute nothing and get dQ_i = 0):
+ *   s_j  = scale * q_i . k_j,   p_j = exp(s_j - max s) / sum_t exp(s_t - max s)     (Eq.7)
+ *   dp_j = dO_i . v_j                                            (SDDMM of dO with V)
+ *   D_i  = sum_j p_j dp_j                                        (= dO_i . O_i)
+ *   ds_j = p_j (dp_j - D_i)                                      (softmax Jacobian)
+ *   dQ_i = scale * sum_j ds_j k_j                                (SpMM)
+ *   dK_j += scale * ds_j q_i,   dV_j += p_j dO_i                 (transposed SpMMs)
+ * Rows are visited in order, so the accumulation into dK / dV is deterministic.
+ * Returns 0, or 2 on an invalid CSR.
+ */
+int oracle_attention_backward(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr, const int32_t* col_idx,
+                              int32_t H, int32_t d, const double* Q, const double* K, const double* V,
+                              const double* dO, double scale, double* dQ, double* dK, double* dV) {
+    if (n_rows < 0 || n_cols < 0 || H < 1 || d < 1) return 1;
+    for (int32_t r = 0; r < n_rows; ++r)
+        if (row_ptr[r + 1] < row_ptr[r]) return 2;
+    memset(dQ, 0, (size_t)n_rows * H * d * sizeof(double));
+    memset(dK, 0, (size_t)n_cols * H * d * sizeof(double));
+    memset(dV, 0, (size_t)n_cols * H * d * sizeof(double));
+    int32_t cap = 0;
+    int32_t* nb = NULL;
+    double *p = NULL, *dp = NULL;
+    int bad = 0;
+    for (int32_t i = 0; i < n_rows && !bad; ++i) {
+        int32_t b = row_ptr[i], e = row_ptr[i + 1], deg = e - b;
+        if (deg > cap) {
+            cap = deg;
+            nb = (int32_t*)realloc(nb, (size_t)cap * sizeof(int32_t));
+            p = (double*)realloc(p, (size_t)cap * sizeof(double));
+            dp = (double*)realloc(dp, (size_t)cap * sizeof(double));
+        }
+        for (int32_t t = 0; t < deg; ++t) {
+            nb[t] = col_idx[b + t];
+            if (nb[t] < 0 || nb[t] >= n_cols) bad = 1;
+        }
+        if (bad) break;
+        qsort(nb, (size_t)deg, sizeof(int32_t), cmp_i32);
+        int32_t u = 0;
+        for (int32_t t = 0; t < deg; ++t)
+            if (u == 0 || nb[t] != nb[u - 1]) nb[u++] = nb[t];
+        for (int32_t h = 0; h < H; ++h) {
+            const double* qi = Q + ((size_t)i * H + h) * d;
+            const double* gi = dO + ((size_t)i * H + h) * d;
+            double m = -INFINITY, l = 0.0, Di = 0.0;
+            for (int32_t t = 0; t < u; ++t) {
+                const double* kj = K + ((size_t)nb[t] * H + h) * d;
+                const double* vj = V + ((size_t)nb[t] * H + h) * d;
+                double dot = 0.0, dv = 0.0;
+                for (int32_t k = 0; k < d; ++k) { dot += qi[k] * kj[k]; dv += gi[k] * vj[k]; }
+                p[t] = scale * dot;
+                dp[t] = dv;
+                if (p[t] > m) m = p[t];
+            }
+            for (int32_t t = 0; t < u; ++t) { p[t] = exp(p[t] - m); l += p[t]; }
+            for (int32_t t = 0; t < u; ++t) { p[t] /= l; Di += p[t] * dp[t]; }
+            double* dqi = dQ + ((size_t)i * H + h) * d;
+            for (int32_t t = 0; t < u; ++t) {
+                const double ds = p[t] * (dp[t] - Di);
+                const double* kj = K + ((size_t)nb[t] * H + h) * d;
+                double* dkj = dK + ((size_t)nb[t] * H + h) * d;
+                double* dvj = dV + ((size_t)nb[t] * H + h) * d;
+                for (int32_t k = 0; k < d; ++k) {
+                    dqi[k] += scale * ds * kj[k];
+                    dkj[k] += scale * ds * qi[k];
+                    dvj[k] += p[t] * gi[k];
+                }
+            }
+        }
+    }
+    free(nb);
+    free(p);
+    free(dp);
+    return bad ? 2 : 0;
+}
+
+/*
+ * The forward of Eq.1 on fp64 inputs (same definition as oracle_attention, which reads the
+ * exact fp16/bf16 values): the function whose derivative oracle_attention_backward is; used
+ * by the finite-difference pins of the backward.
+ */
+int oracle_attention_f64(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr, const int32_t* col_idx,
+                         int32_t H, int32_t d, const double* Q, const double* K, const double* V, double scale,
+                         double* O) {
+    if (n_rows < 0 || n_cols < 0 || H < 1 || d < 1) return 1;
+    int32_t cap = 0;
+    int32_t* nb = NULL;
+    double* w = NULL;
+    int bad = 0;
+    for (int32_t i = 0; i < n_rows && !bad; ++i) {
+        int32_t b = row_ptr[i], e = row_ptr[i + 1], deg = e - b;
+        if (deg < 0) { bad = 1; break; }
+        if (deg > cap) {
+            cap = deg;
+            nb = (int32_t*)realloc(nb, (size_t)cap * sizeof(int32_t));
+            w = (double*)realloc(w, (size_t)cap * sizeof(double));
+        }
+        for (int32_t t = 0; t < deg; ++t) {
+            nb[t] = col_idx[b + t];
+            if (nb[t] < 0 || nb[t] >= n_cols) bad = 1;
+        }
+        if (bad) break;
+        qsort(nb, (size_t)deg, sizeof(int32_t), cmp_i32);
+        int32_t u = 0;
+        for (int32_t t = 0; t < deg; ++t)
+            if (u == 0 || nb[t] != nb[u - 1]) nb[u++] = nb[t];
+        for (int32_t h = 0; h < H; ++h) {
+            double* out = O + ((size_t)i * H + h) * d;
+            for (int32_t k = 0; k < d; ++k) out[k] = 0.0;
+            if (u == 0) continue;
+            const double* qi = Q + ((size_t)i * H + h) * d;
+            double m = -INFINITY, l = 0.0;
+            for (int32_t t = 0; t < u; ++t) {
+                const double* kj = K + ((size_t)nb[t] * H + h) * d;
+                double dot = 0.0;
+                for (int32_t k = 0; k < d; ++k) dot += qi[k] * kj[k];
+                w[t] = scale * dot;
+                if (w[t] > m) m = w[t];
+            }
+            for (int32_t t = 0; t < u; ++t) { w[t] = exp(w[t] - m); l += w[t]; }
+            for (int32_t t = 0; t < u; ++t) {
+                const double* vj = V + ((size_t)nb[t] * H + h) * d;
+                for (int32_t k = 0; k < d; ++k) out[k] += w[t] * vj[k];
+            }
+            for (int32_t k = 0; k < d; ++k) out[k] /= l;
+        }
+    }
+    free(nb);
+    free(w);
     return bad ? 2 : 0;
 }
 
