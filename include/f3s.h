@@ -143,6 +143,26 @@ f3s_status f3s_plan_export(f3s_plan_t plan, int32_t* rw_ptr, int32_t* cols, uint
 f3s_status f3s_attention(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
                          int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
 
+/*
+ * Backward of f3s_attention ("SpMM and SDDMM operations in reverse order",
+ * PAPER.md:752): for O = softmax_row(scale * (Q K^T) (.) A) V and dO = dL/dO,
+ *   dp_ij = dO_i . v_j,  D_i = sum_j p_ij dp_ij,  ds_ij = p_ij (dp_ij - D_i),
+ *   dQ_i = scale sum_j ds_ij k_j,  dK_j = scale sum_i ds_ij q_i,  dV_j = sum_i p_ij dO_i,
+ * with p the exact fp32 softmax of Eq.1 (the forward's rounding of P to the input dtype is not
+ * differentiated).  Two deterministic passes (rows, then columns of A through a transposed index
+ * the plan builds on its first backward call); no atomics on the data.
+ *
+ *  Q, K, V   as for f3s_attention (device, [N, H, d] fp16/bf16, 16-byte aligned).
+ *  dO        device fp32 [n_rows, H, d];  dQ device fp32 [n_rows, H, d] (written);
+ *  dK, dV    device fp32 [n_cols, H, d] (written; for a row-shard plan (f3s_plan_rows) these are
+ *            the shard's partial sums, to be all-reduced by the caller).
+ * Asynchronous on `stream` (stream-ordered scratch of 8 * n_rows * H bytes).
+ * Errors: as f3s_attention; INVALID_VALUE for NULL dO/dK/dV.
+ */
+f3s_status f3s_attention_backward(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* dO,
+                                  float* dQ, float* dK, float* dV, float scale, int32_t heads, int32_t d,
+                                  f3s_dtype dtype, cudaStream_t stream);
+
 /* Kernel variants for ablations (bench.py --variant); f3s_attention uses F3S_VARIANT_DEFAULT. */
 typedef enum {
     F3S_VARIANT_DEFAULT = 0, /* tcgen05 + TMA gather kernel, LPT-ordered persistent queue       */

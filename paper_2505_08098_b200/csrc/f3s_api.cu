@@ -119,6 +119,8 @@ f3s_status f3s_plan_destroy(f3s_plan_t plan) {
     cudaFree(p->meta_nat);
     cudaFree(p->meta_sub);
     cudaFree(p->ginfo);
+    cudaFree(p->col_ptr);
+    cudaFree(p->col_rows);
     cudaFree(p->staging);
     delete p;
     return F3S_OK;
@@ -163,6 +165,25 @@ f3s_status f3s_attention(f3s_plan_t plan, const void* Q, const void* K, const vo
                          int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
     try {
         return run_attention(plan, Q, K, V, O, scale, heads, d, dtype, F3S_VARIANT_DEFAULT, stream);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_backward(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* dO,
+                                  float* dQ, float* dK, float* dV, float scale, int32_t heads, int32_t d,
+                                  f3s_dtype dtype, cudaStream_t stream) {
+    try {
+        f3s_status st = check_attention_args(plan, Q, K, V, dQ, scale, heads, d, dtype, true);
+        if (st != F3S_OK) return st;
+        Plan& p = *reinterpret_cast<Plan*>(plan);
+        if (p.n_rows > 0 && !dO) { set_error("dO is NULL"); return F3S_ERR_INVALID_VALUE; }
+        if (p.n_cols > 0 && (!dK || !dV)) { set_error("dK/dV is NULL"); return F3S_ERR_INVALID_VALUE; }
+        auto mis = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) != 0; };
+        if (mis(dO) || mis(dK) || mis(dV)) { set_error("dO/dK/dV must be 16-byte aligned"); return F3S_ERR_UNSUPPORTED; }
+        F3S_CUDA_TRY(cudaSetDevice(p.device));
+        return launch_attention_backward(p, Q, K, V, dO, dQ, dK, dV, scale, heads, d, dtype, stream);
     } catch (...) {
         set_error("internal error");
         return F3S_ERR_INTERNAL;

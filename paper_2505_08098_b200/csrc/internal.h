@@ -42,6 +42,10 @@ struct Plan {
     int4* meta_sub = nullptr;     // [n_sub]
     int4* ginfo = nullptr;        // [n_groups]
     std::vector<int32_t> h_rw, h_rw8, h_order;  // host copies used to (re)build meta_sub
+    // transposed index of A for the backward's column pass (built on the first backward call):
+    // col_rows[col_ptr[j] .. col_ptr[j+1]) = rows i with (i, j) in A, ascending
+    int32_t* col_ptr = nullptr;   // [n_cols + 1]
+    int32_t* col_rows = nullptr;  // [nnz]
     // e2e staging buffers for f3s_attention_host
     std::mutex staging_mu;
     void* staging = nullptr;
@@ -81,6 +85,9 @@ f3s_status launch_attention_sm100(const AttnArgs& a);
 f3s_status build_split(Plan* p, int32_t chunks);
 constexpr int kSplitChunkCols = 128;  // column granularity of the split (the kernel's chunk)
 f3s_status launch_attention_simt(const AttnArgs& a);
+f3s_status launch_attention_backward(Plan& p, const void* Q, const void* K, const void* V, const float* dO, float* dQ,
+                                     float* dK, float* dV, float scale, int heads, int d, f3s_dtype dtype,
+                                     cudaStream_t stream);
 
 }  // namespace f3s
 

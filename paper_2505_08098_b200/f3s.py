@@ -48,6 +48,7 @@ _lib.f3s_plan_set_split.argtypes = [_vp, _i32]
 _lib.f3s_attention.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_trace.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]
+_lib.f3s_attention_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_partition_rows.argtypes = [_vp, _i32, _i32, _vp]
 _lib.f3s_partition_at.argtypes = [_vp, _i32, _vp, _i32, _i32, _vp]
@@ -57,11 +58,12 @@ _lib.f3s_last_error.restype = ctypes.c_char_p
 _lib.f3s_launch_count.restype = _i64
 for _name in ("f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
               "f3s_attention", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows",
-              "f3s_partition_at"):
+              "f3s_partition_at", "f3s_attention_backward"):
     getattr(_lib, _name).restype = _i32
 
 EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
             "f3s_attention", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows", "f3s_partition_at",
+            "f3s_attention_backward",
             "f3s_status_string", "f3s_last_error", "f3s_launch_count"]
 
 
@@ -171,6 +173,20 @@ def attention_raw(p: Plan, q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, scale
     """Pointer-level call (no torch); used by bench loops and CUDA-graph capture."""
     _check(_lib.f3s_attention_ex(p.handle, q_ptr, k_ptr, v_ptr, o_ptr, float(scale), heads, d, dtype, variant, stream),
            "f3s_attention")
+
+
+def attention_backward(p: Plan, Q, K, V, dO, *, scale: float, stream=None):
+    """f3s_attention_backward: (dQ, dK, dV) fp32 device tensors for dO = dL/dO (fp32 [N, H, d])."""
+    import torch
+    assert dO.dtype == torch.float32 and dO.is_contiguous()
+    H, d = Q.shape[1], Q.shape[2]
+    dQ = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
+    dK = torch.empty(K.shape, dtype=torch.float32, device=K.device)
+    dV = torch.empty(V.shape, dtype=torch.float32, device=V.device)
+    _check(_lib.f3s_attention_backward(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), dO.data_ptr(),
+                                       dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(), float(scale), H, d,
+                                       _dtype_code(Q), _stream(stream)), "f3s_attention_backward")
+    return dQ, dK, dV
 
 
 def attention_trace(p: Plan, Q, K, V, O, *, scale: float, trace_chunks: int = 4096, grid: int = 0,

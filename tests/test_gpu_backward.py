@@ -1,0 +1,95 @@
+"""Backward of the fused 3S pass (f3s_attention_backward) against the fp64 oracle
+backward (pinned in test_oracle_backward.py) on the same seeded inputs: dQ, dK, dV element by
+element, plus determinism and row-shard additivity."""
+import numpy as np
+import pytest
+
+import f3s_inputs as fi
+from conftest import decode
+from helpers import csr_to_dev, errors, make_qkv, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def f3s():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2505_08098_b200 import f3s as mod
+    return mod
+
+
+def _close(got, ref):
+    # fp32 arithmetic on the exact inputs: the same bar as the forward, relative to the scale
+    max_abs, rel = errors(got, ref)
+    scale = max(1.0, float(np.max(np.abs(ref))))
+    assert np.all(np.isfinite(got)) and max_abs <= 1e-2 * scale and rel <= 5e-3, (max_abs, rel, scale)
+
+
+def _bwd(f3s, p, Qb, Kb, Vb, G, dtype, scale):
+    import torch
+    dO = torch.from_numpy(G.astype(np.float32)).cuda()
+    dQ, dK, dV = f3s.attention_backward(p, to_dev(Qb, dtype), to_dev(Kb, dtype), to_dev(Vb, dtype), dO, scale=scale)
+    torch.cuda.synchronize()
+    return dQ.cpu().numpy(), dK.cpu().numpy(), dV.cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("d,H", [(64, 1), (64, 3), (128, 2)])
+def test_backward_parity(f3s, oracle_mod, dtype, d, H):
+    csr = fi.random_csr(1000 + 7, 1000 + 7, 0, 40, keep_dups=True, unsorted=True, seed=d + H)
+    Qb, Kb, Vb = make_qkv(csr.n_rows, csr.n_cols, H, d, dtype, seed=21)
+    G = np.random.default_rng(d + H).standard_normal((csr.n_rows, H, d)).astype(np.float32)
+    scale = 1.0 / np.sqrt(d)
+    rp, ci = csr_to_dev(csr)
+    p = f3s.plan(rp, ci, csr.n_rows)
+    got = _bwd(f3s, p, Qb, Kb, Vb, G, dtype, scale)
+    ref = oracle_mod.attention_backward(csr.row_ptr, csr.col_idx, decode(Qb, dtype), decode(Kb, dtype),
+                                        decode(Vb, dtype), G.astype(np.float64), scale=scale)
+    for g, r in zip(got, ref):
+        _close(g, r)
+    empty = np.diff(csr.row_ptr) == 0
+    assert empty.any() and np.all(got[0][empty] == 0)
+    # deterministic: fixed visiting order in both passes, no atomics on the data
+    again = _bwd(f3s, p, Qb, Kb, Vb, G, dtype, scale)
+    assert all(np.array_equal(a, b) for a, b in zip(got, again))
+
+
+def test_backward_power_law(f3s, oracle_mod):
+    # hub rows and hub columns (windows of many chunks, columns with thousands of rows)
+    csr = fi.chung_lu(6000, 60000, gamma=2.1, max_deg=3000, seed=21)
+    Qb, Kb, Vb = make_qkv(6000, 6000, 2, 64, "fp16", seed=22)
+    G = np.random.default_rng(5).standard_normal((6000, 2, 64)).astype(np.float32)
+    rp, ci = csr_to_dev(csr)
+    p = f3s.plan(rp, ci, csr.n_rows)
+    got = _bwd(f3s, p, Qb, Kb, Vb, G, "fp16", 0.125)
+    ref = oracle_mod.attention_backward(csr.row_ptr, csr.col_idx, decode(Qb, "fp16"), decode(Kb, "fp16"),
+                                        decode(Vb, "fp16"), G.astype(np.float64), scale=0.125)
+    for g, r in zip(got, ref):
+        _close(g, r)
+
+
+def test_backward_row_shards_add_up(f3s):
+    # dK, dV of a row shard are that shard's partial sums: the shards' sum is the full result
+    import torch
+    n, H, d = 2000, 2, 64
+    csr = fi.random_csr(n, n, 1, 20, seed=9)
+    Qb, Kb, Vb = make_qkv(n, n, H, d, "bf16", seed=23)
+    G = np.random.default_rng(7).standard_normal((n, H, d)).astype(np.float32)
+    rp, ci = csr_to_dev(csr)
+    full = _bwd(f3s, f3s.plan(rp, ci, n), Qb, Kb, Vb, G, "bf16", 0.125)
+    bounds = [0, 992, n]
+    dQ_parts, dK_sum, dV_sum = [], 0.0, 0.0
+    for b, e in zip(bounds[:-1], bounds[1:]):
+        lrp = torch.from_numpy((csr.row_ptr[b:e + 1] - csr.row_ptr[b]).astype(np.int32)).cuda()
+        lci = torch.from_numpy(csr.col_idx[csr.row_ptr[b]:csr.row_ptr[e]].copy()).cuda()
+        ps = f3s.plan_rows(lrp, lci, e - b, n)
+        dO = torch.from_numpy(G[b:e]).cuda()
+        dQ, dK, dV = f3s.attention_backward(ps, to_dev(Qb[b:e].copy(), "bf16"), to_dev(Kb, "bf16"), to_dev(Vb, "bf16"),
+                                            dO, scale=0.125)
+        torch.cuda.synchronize()
+        dQ_parts.append(dQ.cpu().numpy())
+        dK_sum = dK_sum + dK.cpu().numpy().astype(np.float64)
+        dV_sum = dV_sum + dV.cpu().numpy().astype(np.float64)
+    assert np.array_equal(np.concatenate(dQ_parts), full[0])  # rows of a window live in one shard
+    assert np.max(np.abs(dK_sum - full[1])) <= 1e-5 and np.max(np.abs(dV_sum - full[2])) <= 1e-5
