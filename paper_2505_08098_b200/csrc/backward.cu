@@ -18,6 +18,8 @@
 
 #include <cub/cub.cuh>
 
+#include <vector>
+
 #include "internal.h"
 
 namespace f3s {
@@ -52,11 +54,23 @@ __global__ void __launch_bounds__(512) k_bwd_rows(const int32_t* __restrict__ rw
 #pragma unroll
     for (int e = 0; e < E; ++e) { q[e] = to_f(Q[base + e]); g[e] = dO[base + e]; acc[e] = 0.f; }
     const int32_t b = rw_ptr[k], en = rw_ptr[k + 1];
+    // the row's entries among the window's compacted columns, 32 at a time: lane t tests entry
+    // p0 + t, a ballot lists the hits, the warp walks the set bits
+#define F3S_FOR_ROW_ENTRIES(...)                                                               \
+    for (int32_t p0 = b; p0 < en; p0 += 32) {                                                  \
+        const int32_t pl = p0 + lane;                                                          \
+        uint32_t hits = __ballot_sync(0xffffffffu, pl < en && ((masks[pl] >> i) & 1));         \
+        const int32_t cl = pl < en ? cols[pl] : 0;                                             \
+        while (hits) {                                                                         \
+            const int t = __ffs(hits) - 1;                                                     \
+            hits &= hits - 1;                                                                  \
+            const int64_t jb = (int64_t)__shfl_sync(0xffffffffu, cl, t) * ld + h * D + lane * E; \
+            __VA_ARGS__                                                                        \
+        }                                                                                      \
+    }
     // pass 1: running max m (log2 units), l = sum 2^(x - m), u = sum 2^(x - m) dp  -> D = u / l
     float m = -INFINITY, l = 0.f, u = 0.f;
-    for (int32_t p = b; p < en; ++p) {
-        if (!((masks[p] >> i) & 1)) continue;  // warp-uniform
-        const int64_t jb = (int64_t)cols[p] * ld + h * D + lane * E;
+    F3S_FOR_ROW_ENTRIES({
         float s = 0.f, dp = 0.f;
 #pragma unroll
         for (int e = 0; e < E; ++e) { s += q[e] * to_f(K[jb + e]); dp += g[e] * to_f(V[jb + e]); }
@@ -68,13 +82,11 @@ __global__ void __launch_bounds__(512) k_bwd_rows(const int32_t* __restrict__ rw
         l = l * a + w;
         u = u * a + w * dp;
         m = mn;
-    }
+    })
     const float L = m + log2f(l);  // row log-sum-exp in log2 units (-inf for an empty row)
     const float Di = l > 0.f ? u / l : 0.f;
     // pass 2: p = 2^(x - L), ds = p (dp - D), dQ += scale ds k
-    for (int32_t p = b; p < en; ++p) {
-        if (!((masks[p] >> i) & 1)) continue;
-        const int64_t jb = (int64_t)cols[p] * ld + h * D + lane * E;
+    F3S_FOR_ROW_ENTRIES({
         float kv[E], s = 0.f, dp = 0.f;
 #pragma unroll
         for (int e = 0; e < E; ++e) { kv[e] = to_f(K[jb + e]); s += q[e] * kv[e]; dp += g[e] * to_f(V[jb + e]); }
@@ -83,7 +95,8 @@ __global__ void __launch_bounds__(512) k_bwd_rows(const int32_t* __restrict__ rw
         const float ds = exp2f(s * scale_log2 - L) * (dp - Di);
 #pragma unroll
         for (int e = 0; e < E; ++e) acc[e] = fmaf(scale * ds, kv[e], acc[e]);
-    }
+    })
+#undef F3S_FOR_ROW_ENTRIES
 #pragma unroll
     for (int e = 0; e < E; ++e) dQ[base + e] = acc[e];  // empty row: 0
     if (lane == 0) {
@@ -94,8 +107,9 @@ __global__ void __launch_bounds__(512) k_bwd_rows(const int32_t* __restrict__ rw
 
 // ---- column pass: dK, dV -------------------------------------------------------------------
 template <int D, typename T>
-__global__ void __launch_bounds__(256) k_bwd_cols(const int32_t* __restrict__ col_ptr, const int32_t* __restrict__ col_rows,
-                                                  int32_t n_cols, int H, const T* __restrict__ Q,
+__global__ void __launch_bounds__(256) k_bwd_cols(const int32_t* __restrict__ light, const int32_t* __restrict__ col_ptr,
+                                                  const int32_t* __restrict__ col_rows, int32_t n_cols, int H,
+                                                  const T* __restrict__ Q,
                                                   const T* __restrict__ K, const T* __restrict__ V,
                                                   const float* __restrict__ dO, const float* __restrict__ lse,
                                                   const float* __restrict__ Drow, float* __restrict__ dK,
@@ -104,9 +118,9 @@ __global__ void __launch_bounds__(256) k_bwd_cols(const int32_t* __restrict__ co
     const float scale_log2 = scale * 1.4426950408889634f;
     const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (wid >= (int64_t)n_cols * H) return;
-    const int64_t j = wid / H;
-    const int h = (int)(wid - j * H);
+    if (wid >= (int64_t)n_cols * H) return;  // n_cols: number of light columns
+    const int64_t j = light[wid / H];
+    const int h = (int)(wid - (wid / H) * H);
     const int64_t ld = (int64_t)H * D, jb = j * ld + h * D + lane * E;
     float kv[E], vv[E], gk[E], gv[E];
 #pragma unroll
@@ -134,6 +148,60 @@ __global__ void __launch_bounds__(256) k_bwd_cols(const int32_t* __restrict__ co
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) { dK[jb + e] = gk[e]; dV[jb + e] = gv[e]; }
+}
+
+// heavy columns (more than kHeavyCol rows: power-law in-degree hubs): one block of 8 warps per
+// (column, head); warp w takes rows w, w+8, ... and the 8 partial sums are added in warp order
+// (deterministic).  A hub of 13,000 rows on one warp alone set the whole pass's time.
+constexpr int kHeavyCol = 64;
+template <int D, typename T>
+__global__ void __launch_bounds__(256) k_bwd_cols_heavy(const int32_t* __restrict__ heavy, const int32_t* __restrict__ col_ptr,
+                                                        const int32_t* __restrict__ col_rows, int H,
+                                                        const T* __restrict__ Q, const T* __restrict__ K,
+                                                        const T* __restrict__ V, const float* __restrict__ dO,
+                                                        const float* __restrict__ lse, const float* __restrict__ Drow,
+                                                        float* __restrict__ dK, float* __restrict__ dV, float scale) {
+    constexpr int E = D / 32;
+    __shared__ float part[8][2][D];
+    const float scale_log2 = scale * 1.4426950408889634f;
+    const int64_t j = heavy[blockIdx.x / H];
+    const int h = blockIdx.x - (blockIdx.x / H) * H;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ld = (int64_t)H * D, jb = j * ld + h * D + lane * E;
+    float kv[E], vv[E], gk[E], gv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { kv[e] = to_f(K[jb + e]); vv[e] = to_f(V[jb + e]); gk[e] = 0.f; gv[e] = 0.f; }
+    for (int32_t t = col_ptr[j] + w; t < col_ptr[j + 1]; t += 8) {
+        const int64_t i = col_rows[t];
+        const int64_t ib = i * ld + h * D + lane * E;
+        float qv[E], gi[E], s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            qv[e] = to_f(Q[ib + e]);
+            gi[e] = dO[ib + e];
+            s += qv[e] * kv[e];
+            dp += gi[e] * vv[e];
+        }
+        s = warp_sum(s);
+        dp = warp_sum(dp);
+        const float pij = exp2f(s * scale_log2 - lse[i * H + h]);
+        const float ds = pij * (dp - Drow[i * H + h]);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            gk[e] = fmaf(scale * ds, qv[e], gk[e]);
+            gv[e] = fmaf(pij, gi[e], gv[e]);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) { part[w][0][lane * E + e] = gk[e]; part[w][1][lane * E + e] = gv[e]; }
+    __syncthreads();
+    for (int f = threadIdx.x; f < 2 * D; f += blockDim.x) {
+        const int which = f / D, x = f - which * D;
+        float acc = 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += part[u][which][x];  // fixed order
+        (which ? dV : dK)[j * ld + h * D + x] = acc;
+    }
 }
 
 // ---- transposed index of A (built once per plan) ----------------------------------------------
@@ -221,8 +289,28 @@ f3s_status build_transpose(Plan& p, cudaStream_t stream) {
         count_launch();
     }
     F3S_CUDA_TRY(cudaGetLastError());
+    // light / heavy column lists (one-time host pass over the column counts)
+    std::vector<int32_t> h_cp((size_t)p.n_cols + 1);
+    F3S_CUDA_TRY(cudaMemcpyAsync(h_cp.data(), col_ptr, sizeof(int32_t) * h_cp.size(), cudaMemcpyDeviceToHost, stream));
+    F3S_CUDA_TRY(cudaStreamSynchronize(stream));
+    std::vector<int32_t> light, heavy;
+    for (int32_t j = 0; j < p.n_cols; ++j) {
+        const int32_t c = h_cp[j + 1] - h_cp[j];
+        if (c > kHeavyCol) heavy.push_back(j);
+        else if (c > 0) light.push_back(j);
+    }
+    // (columns without rows get dK = dV = 0 from a memset in launch_bwd)
+    int32_t* lists = nullptr;
+    F3S_CUDA_TRY(cudaMalloc(&lists, sizeof(int32_t) * (light.size() + heavy.size() + 1)));
+    if (!light.empty())
+        F3S_CUDA_TRY(cudaMemcpy(lists, light.data(), sizeof(int32_t) * light.size(), cudaMemcpyHostToDevice));
+    if (!heavy.empty())
+        F3S_CUDA_TRY(cudaMemcpy(lists + light.size(), heavy.data(), sizeof(int32_t) * heavy.size(), cudaMemcpyHostToDevice));
     p.col_ptr = col_ptr;
     p.col_rows = col_rows;
+    p.col_lists = lists;
+    p.n_light = (int32_t)light.size();
+    p.n_heavy = (int32_t)heavy.size();
     return F3S_OK;
 }
 
@@ -251,12 +339,27 @@ f3s_status launch_bwd(Plan& p, const void* Q, const void* K, const void* V, cons
                                                            static_cast<const T*>(V), dO, dQ, lse, drow, scale);
     count_launch();
     F3S_CUDA_TRY(cudaGetLastError());
-    const int64_t warps = (int64_t)p.n_cols * H, cblocks = (warps + 7) / 8;
-    if (cblocks > 0x7FFFFFFF) { set_error("too many column blocks"); return F3S_ERR_UNSUPPORTED; }
-    k_bwd_cols<D, T><<<(unsigned)cblocks, 256, 0, stream>>>(p.col_ptr, p.col_rows, p.n_cols, H,
-                                                            static_cast<const T*>(Q), static_cast<const T*>(K),
-                                                            static_cast<const T*>(V), dO, lse, drow, dK, dV, scale);
-    count_launch();
+    if (p.n_light + p.n_heavy < p.n_cols) {  // columns without rows: zero gradients
+        F3S_CUDA_TRY(cudaMemsetAsync(dK, 0, sizeof(float) * (size_t)p.n_cols * H * D, stream));
+        F3S_CUDA_TRY(cudaMemsetAsync(dV, 0, sizeof(float) * (size_t)p.n_cols * H * D, stream));
+    }
+    const int64_t warps = (int64_t)p.n_light * H, cblocks = (warps + 7) / 8;
+    if (cblocks > 0x7FFFFFFF || (int64_t)p.n_heavy * H > 0x7FFFFFFF) {
+        set_error("too many column blocks");
+        return F3S_ERR_UNSUPPORTED;
+    }
+    if (cblocks > 0) {
+        k_bwd_cols<D, T><<<(unsigned)cblocks, 256, 0, stream>>>(p.col_lists, p.col_ptr, p.col_rows, p.n_light, H,
+                                                                static_cast<const T*>(Q), static_cast<const T*>(K),
+                                                                static_cast<const T*>(V), dO, lse, drow, dK, dV, scale);
+        count_launch();
+    }
+    if (p.n_heavy > 0) {
+        k_bwd_cols_heavy<D, T><<<(unsigned)((int64_t)p.n_heavy * H), 256, 0, stream>>>(
+            p.col_lists + p.n_light, p.col_ptr, p.col_rows, H, static_cast<const T*>(Q), static_cast<const T*>(K),
+            static_cast<const T*>(V), dO, lse, drow, dK, dV, scale);
+        count_launch();
+    }
     F3S_CUDA_TRY(cudaGetLastError());
     return F3S_OK;
 }

@@ -121,6 +121,7 @@ f3s_status f3s_plan_destroy(f3s_plan_t plan) {
     cudaFree(p->ginfo);
     cudaFree(p->col_ptr);
     cudaFree(p->col_rows);
+    cudaFree(p->col_lists);
     cudaFree(p->staging);
     delete p;
     return F3S_OK;

@@ -46,6 +46,8 @@ struct Plan {
     // col_rows[col_ptr[j] .. col_ptr[j+1]) = rows i with (i, j) in A, ascending
     int32_t* col_ptr = nullptr;   // [n_cols + 1]
     int32_t* col_rows = nullptr;  // [nnz]
+    int32_t* col_lists = nullptr; // [n_light + n_heavy]: columns with 1..64 rows, then with more
+    int32_t n_light = 0, n_heavy = 0;
     // e2e staging buffers for f3s_attention_host
     std::mutex staging_mu;
     void* staging = nullptr;
