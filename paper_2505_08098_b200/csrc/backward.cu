@@ -5,10 +5,11 @@
 //   dp_ij = dO_i . v_j,  D_i = sum_j p_ij dp_ij,  ds_ij = p_ij (dp_ij - D_i)
 //   dQ_i = scale sum_j ds_ij k_j,  dK_j = scale sum_i ds_ij q_i,  dV_j = sum_i p_ij dO_i.
 // Two deterministic passes, no atomics on the data:
-//   row pass    one warp per (query row, head), walking its row window's compacted columns
+//   row pass    one warp per (query row, head) (8 warps for rows of > 256 entries), walking its
+//               row window's compacted columns
 //               with the row's mask bit (the forward's plan): online max / sum / D (the same
 //               rescaling as Alg.1 l.16-18), then p, ds and dQ; it leaves LSE_i and D_i.
-//   column pass one warp per (key column, head), walking the column's rows of A^T in ascending
+//   column pass one warp per (key column, head) (8 for > 64 rows), walking the column's rows of A^T in ascending
 //               order (a transposed index built once per plan from the plan's masks): it
 //               recomputes p_ij = 2^(s_ij - LSE_i) and ds_ij and accumulates dK_j, dV_j.
 // CUDA-core kernels (first version of the NEXT row f3): the tensor-core form would reuse the
@@ -42,13 +43,14 @@ __global__ void __launch_bounds__(512) k_bwd_rows(const int32_t* __restrict__ rw
                                                   const T* __restrict__ Q, const T* __restrict__ K,
                                                   const T* __restrict__ V, const float* __restrict__ dO,
                                                   float* __restrict__ dQ, float* __restrict__ lse,
-                                                  float* __restrict__ Drow, float scale) {
+                                                  float* __restrict__ Drow, float scale,
+                                                  const uint8_t* __restrict__ heavy_row) {
     constexpr int E = D / 32;  // features per lane
     const float scale_log2 = scale * 1.4426950408889634f;
     const int k = blockIdx.x / H, h = blockIdx.x - (blockIdx.x / H) * H;
     const int i = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row = 16 * (int64_t)k + i;
-    if (row >= n_rows) return;
+    if (row >= n_rows || heavy_row[row]) return;  // heavy rows: k_bwd_rows_heavy
     const int64_t ld = (int64_t)H * D, base = row * ld + h * D + lane * E;
     float q[E], g[E], acc[E];
 #pragma unroll
@@ -102,6 +104,109 @@ __global__ void __launch_bounds__(512) k_bwd_rows(const int32_t* __restrict__ rw
     if (lane == 0) {
         lse[row * H + h] = L;
         Drow[row * H + h] = Di;
+    }
+}
+
+// heavy rows (more than kHeavyRow entries): one block of 8 warps per (row, head); warp w walks
+// the window entry blocks w, w+8, ... ; the per-warp (max, sum, D-sum) and dQ partials are
+// combined in warp order (deterministic)
+constexpr int kHeavyRow = 256;
+template <int D, typename T>
+__global__ void __launch_bounds__(256) k_bwd_rows_heavy(const int32_t* __restrict__ heavy, const int32_t* __restrict__ rw_ptr,
+                                                        const int32_t* __restrict__ cols, const uint16_t* __restrict__ masks,
+                                                        int H, const T* __restrict__ Q, const T* __restrict__ K,
+                                                        const T* __restrict__ V, const float* __restrict__ dO,
+                                                        float* __restrict__ dQ, float* __restrict__ lse,
+                                                        float* __restrict__ Drow, float scale) {
+    constexpr int E = D / 32;
+    __shared__ float st[8][3];
+    __shared__ float part[8][D];
+    const float scale_log2 = scale * 1.4426950408889634f;
+    const int64_t row = heavy[blockIdx.x / H];
+    const int h = blockIdx.x - (blockIdx.x / H) * H;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = (int)(row & 15);
+    const int64_t k = row >> 4;
+    const int64_t ld = (int64_t)H * D, base = row * ld + h * D + lane * E;
+    float q[E], g[E], acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { q[e] = to_f(Q[base + e]); g[e] = dO[base + e]; acc[e] = 0.f; }
+    const int32_t b = rw_ptr[k], en = rw_ptr[k + 1];
+#define F3S_FOR_MY_ENTRIES(...)                                                                \
+    for (int32_t p0 = b + 32 * w; p0 < en; p0 += 256) {                                        \
+        const int32_t pl = p0 + lane;                                                          \
+        uint32_t hits = __ballot_sync(0xffffffffu, pl < en && ((masks[pl] >> i) & 1));         \
+        const int32_t cl = pl < en ? cols[pl] : 0;                                             \
+        while (hits) {                                                                         \
+            const int t = __ffs(hits) - 1;                                                     \
+            hits &= hits - 1;                                                                  \
+            const int64_t jb = (int64_t)__shfl_sync(0xffffffffu, cl, t) * ld + h * D + lane * E; \
+            __VA_ARGS__                                                                        \
+        }                                                                                      \
+    }
+    float m = -INFINITY, l = 0.f, u = 0.f;
+    F3S_FOR_MY_ENTRIES({
+        float s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) { s += q[e] * to_f(K[jb + e]); dp += g[e] * to_f(V[jb + e]); }
+        s = warp_sum(s);
+        dp = warp_sum(dp);
+        const float x = s * scale_log2;
+        const float mn = fmaxf(m, x);
+        const float a = exp2f(m - mn), wt = exp2f(x - mn);
+        l = l * a + wt;
+        u = u * a + wt * dp;
+        m = mn;
+    })
+    if (lane == 0) { st[w][0] = m; st[w][1] = l; st[w][2] = u; }
+    __syncthreads();
+    float M = -INFINITY;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) M = fmaxf(M, st[v][0]);
+    float lt = 0.f, ut = 0.f;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {  // warps without entries have l = u = 0 (m = -inf -> weight 0)
+        const float sc = st[v][1] > 0.f ? exp2f(st[v][0] - M) : 0.f;
+        lt = fmaf(st[v][1], sc, lt);
+        ut = fmaf(st[v][2], sc, ut);
+    }
+    const float L = M + log2f(lt), Di = lt > 0.f ? ut / lt : 0.f;
+    F3S_FOR_MY_ENTRIES({
+        float kv[E], s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) { kv[e] = to_f(K[jb + e]); s += q[e] * kv[e]; dp += g[e] * to_f(V[jb + e]); }
+        s = warp_sum(s);
+        dp = warp_sum(dp);
+        const float ds = exp2f(s * scale_log2 - L) * (dp - Di);
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = fmaf(scale * ds, kv[e], acc[e]);
+    })
+#undef F3S_FOR_MY_ENTRIES
+#pragma unroll
+    for (int e = 0; e < E; ++e) part[w][lane * E + e] = acc[e];
+    __syncthreads();
+    for (int f = threadIdx.x; f < D; f += blockDim.x) {
+        float a2 = 0.f;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) a2 += part[v][f];  // fixed order
+        dQ[row * ld + h * D + f] = a2;
+    }
+    if (threadIdx.x == 0) {
+        lse[row * H + h] = L;
+        Drow[row * H + h] = Di;
+    }
+}
+
+// per-row entry counts from the plan's masks (row degrees of the deduplicated A)
+__global__ void k_row_deg(const int32_t* __restrict__ rw_ptr, int32_t R, const uint16_t* __restrict__ masks,
+                          int32_t* __restrict__ deg) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)R * 16;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = t >> 4;
+        const int i = (int)(t & 15);
+        int32_t c = 0;
+        for (int32_t p = rw_ptr[k]; p < rw_ptr[k + 1]; ++p) c += (masks[p] >> i) & 1;
+        deg[t] = c;
     }
 }
 
@@ -306,6 +411,32 @@ f3s_status build_transpose(Plan& p, cudaStream_t stream) {
         F3S_CUDA_TRY(cudaMemcpy(lists, light.data(), sizeof(int32_t) * light.size(), cudaMemcpyHostToDevice));
     if (!heavy.empty())
         F3S_CUDA_TRY(cudaMemcpy(lists + light.size(), heavy.data(), sizeof(int32_t) * heavy.size(), cudaMemcpyHostToDevice));
+    // heavy rows: degree from the plan's masks
+    std::vector<int32_t> h_deg((size_t)p.num_rw * 16);
+    {
+        Scratch degs;
+        degs.s = stream;
+        F3S_CUDA_TRY(cudaMallocAsync(&degs.p, sizeof(int32_t) * h_deg.size() + 16, stream));
+        k_row_deg<<<grid_for((int64_t)p.num_rw * 16, 256), 256, 0, stream>>>(p.rw_ptr, p.num_rw, p.masks,
+                                                                             (int32_t*)degs.p);
+        count_launch();
+        F3S_CUDA_TRY(cudaMemcpyAsync(h_deg.data(), degs.p, sizeof(int32_t) * h_deg.size(), cudaMemcpyDeviceToHost,
+                                     stream));
+        F3S_CUDA_TRY(cudaStreamSynchronize(stream));
+    }
+    std::vector<int32_t> hrows;
+    std::vector<uint8_t> flag((size_t)std::max(p.n_rows, 1), 0);
+    for (int32_t r = 0; r < p.n_rows; ++r)
+        if (h_deg[r] > kHeavyRow) { hrows.push_back(r); flag[r] = 1; }
+    int32_t* hr = nullptr;
+    uint8_t* hf = nullptr;
+    F3S_CUDA_TRY(cudaMalloc(&hr, sizeof(int32_t) * (hrows.size() + 1)));
+    F3S_CUDA_TRY(cudaMalloc(&hf, flag.size()));
+    if (!hrows.empty()) F3S_CUDA_TRY(cudaMemcpy(hr, hrows.data(), sizeof(int32_t) * hrows.size(), cudaMemcpyHostToDevice));
+    F3S_CUDA_TRY(cudaMemcpy(hf, flag.data(), flag.size(), cudaMemcpyHostToDevice));
+    p.heavy_rows = hr;
+    p.heavy_row_flag = hf;
+    p.n_heavy_rows = (int32_t)hrows.size();
     p.col_ptr = col_ptr;
     p.col_rows = col_rows;
     p.col_lists = lists;
@@ -336,8 +467,16 @@ f3s_status launch_bwd(Plan& p, const void* Q, const void* K, const void* V, cons
     if (blocks > 0x7FFFFFFF) { set_error("too many row blocks"); return F3S_ERR_UNSUPPORTED; }
     k_bwd_rows<D, T><<<(unsigned)blocks, 512, 0, stream>>>(p.rw_ptr, p.cols, p.masks, p.n_rows, H,
                                                            static_cast<const T*>(Q), static_cast<const T*>(K),
-                                                           static_cast<const T*>(V), dO, dQ, lse, drow, scale);
+                                                           static_cast<const T*>(V), dO, dQ, lse, drow, scale,
+                                                           p.heavy_row_flag);
     count_launch();
+    if (p.n_heavy_rows > 0) {
+        if ((int64_t)p.n_heavy_rows * H > 0x7FFFFFFF) { set_error("too many heavy rows"); return F3S_ERR_UNSUPPORTED; }
+        k_bwd_rows_heavy<D, T><<<(unsigned)((int64_t)p.n_heavy_rows * H), 256, 0, stream>>>(
+            p.heavy_rows, p.rw_ptr, p.cols, p.masks, H, static_cast<const T*>(Q), static_cast<const T*>(K),
+            static_cast<const T*>(V), dO, dQ, lse, drow, scale);
+        count_launch();
+    }
     F3S_CUDA_TRY(cudaGetLastError());
     if (p.n_light + p.n_heavy < p.n_cols) {  // columns without rows: zero gradients
         F3S_CUDA_TRY(cudaMemsetAsync(dK, 0, sizeof(float) * (size_t)p.n_cols * H * D, stream));

@@ -122,6 +122,8 @@ f3s_status f3s_plan_destroy(f3s_plan_t plan) {
     cudaFree(p->col_ptr);
     cudaFree(p->col_rows);
     cudaFree(p->col_lists);
+    cudaFree(p->heavy_rows);
+    cudaFree(p->heavy_row_flag);
     cudaFree(p->staging);
     delete p;
     return F3S_OK;

@@ -138,7 +138,7 @@ f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_
     struct Guard { Plan*& p; bool ok = false; ~Guard() { if (!ok && p) {
         cudaFree(p->rw_ptr); cudaFree(p->cols); cudaFree(p->masks); cudaFree(p->rw_order);
         cudaFree(p->rw_natural); cudaFree(p->counters); cudaFree(p->kcols); cudaFree(p->kmasks);
-        cudaFree(p->meta_lpt); cudaFree(p->meta_nat); cudaFree(p->meta_sub); cudaFree(p->ginfo); cudaFree(p->col_ptr); cudaFree(p->col_rows); cudaFree(p->col_lists); delete p; p = nullptr; } } } guard{plan};
+        cudaFree(p->meta_lpt); cudaFree(p->meta_nat); cudaFree(p->meta_sub); cudaFree(p->ginfo); cudaFree(p->col_ptr); cudaFree(p->col_rows); cudaFree(p->col_lists); cudaFree(p->heavy_rows); cudaFree(p->heavy_row_flag); delete p; p = nullptr; } } } guard{plan};
     F3S_CUDA_TRY(cudaGetDevice(&plan->device));
     const int32_t R = (n_rows + kRowsPerWindow - 1) / kRowsPerWindow;
     plan->n_rows = n_rows;
