@@ -1,29 +1,29 @@
 // attention_sm100.cu — the fused 3S kernel for B200 (sm_100a).
 //
 // Computes, per row window k (16 query rows) and head h, Alg.1 of the paper
-// (PAPER.md:287-322) re-designed for Blackwell (DESIGN.md §Kernel):
+// (PAPER.md:287-322) re-designed for Blackwell (DESIGN.md §7):
 //
-//   * work items (k, h) in LPT order from a persistent queue: one atomic per item;
-//   * warp 0 (producer): TMA-loads Q_w (16 x d, Alg.1 l.5) and, per chunk of up to 128
-//     compacted columns (sptd, l.7), gathers the K and V rows with cp.async.bulk.tensor
-//     tile::gather4 (l.8) into a variable-size shared-memory ring (128B-swizzled tiles);
-//   * warp 1 (MMA issuer, one thread): swap-AB contractions on tcgen05 with TMEM accumulators
+//   * work items (window or piece of a split window, head group) in LPT order from a
+//     persistent queue; one CTA per SM, 20 warps with fixed roles;
+//   * warp 2 (index): pops items and bulk-copies each chunk's column ids and 16-bit row masks
+//     (the BSB bitmap) into a chunk slot;
+//   * warp 0 (producer): TMA-loads Q_w (16 x d per head, Alg.1 l.5) and allocates each chunk's
+//     K and V tiles in two shared-memory byte rings;
+//   * warps 3-6 (loaders): gather the chunk's K and V rows (sptd, l.7-8) with 16-byte cp.async
+//     into 128B-swizzled UMMA tiles;
+//   * warp 1 (MMA1) and warp 7 (MMA2): swap-AB contractions on tcgen05 with TMEM accumulators,
 //       MMA1  S^T[C x 16]  = K_c[C x d] . Q_w^T        (SDDMM, l.13; M = 128, N = 16)
 //       MMA2  O^T[d x 16]  = V_c^T[d x C] . P^T[C x 16] (SpMM,  l.22; M = d,   N = 16)
-//     S^T lane p is compacted column p, so the 16-bit plan mask of that column is the
-//     bitmap row (l.14) of exactly one thread;
-//   * warp 2 (index): pops items from the queue in batches and bulk-copies each chunk's
-//     column ids and 16-bit row masks (the BSB bitmap) into a chunk slot;
-//   * softmax warpgroup (warps 3-6): tcgen05.ld S^T, mask to -inf, chunk row max by warp
-//     shuffles + a 4-warp combine, online softmax in fp32 with exp2 (l.16-18), P cast to the
-//     input dtype into shared memory (l.19), per-row rescale factors to the correction group;
-//   * correction warpgroup (warps 7-10): folds each chunk's O^T from TMEM into fp32 registers
-//     with the running rescale (l.21-22) and at the item's last chunk writes O = O / l (l.24;
-//     rows with l = 0 -> 0, reading c4).  Keeping the O stores out of the softmax group keeps
-//     its proxy fence (MEMBAR) cheap.
+//     each sleeping in mbarrier try_wait on the barriers of its next instruction;
+//   * two softmax warpgroups (alternate items): tcgen05.ld S^T (lane = compacted column, whose
+//     mask is the bitmap row of l.14), chunk row max by warp shuffles (+ a 4-warp combine), online
+//     softmax in fp32 with exp2 (l.16-18), P cast to the input dtype into shared memory (l.19);
+//   * correction warpgroup: folds each chunk's O^T into fp32 registers with the running rescale
+//     (l.21-22) and at the item's last chunk writes O = O / l (l.24; rows with l = 0 -> 0, reading
+//     c4) through a shared-memory tile and one TMA store — or a split piece's (m, l, O) partial.
 //
-// Everything between the gathers and the O store stays on chip.  No atomics on
-// the data path: results are bitwise deterministic.
+// Everything between the gathers and the O store stays on chip.  No atomics on the
+// data path: results are bitwise deterministic.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -202,7 +202,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
             int32_t* __restrict__ counter, int32_t n_items, int32_t H, int32_t n_rows, int32_t chunk_rows,
             const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float* __restrict__ O, float scale_log2,
-            uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt, uint32_t mma_sleep_ns,
+            uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt,
             float* __restrict__ scratch) {
     using C = Cfg<D, HG>;
     using B = Bars<D, HG>;
@@ -335,6 +335,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         } else {
                             mbar_arrive(fb);
                         }
+// F3S_TRACE_EV0 (diagnostic builds only; tools/variants.sh): 0 = the default stamps; 3 = per
+// softmax warp the time just before its pfull arrive (in events 0/2/3/7); 4 = when the MMA2 warp
+// saw P (event 0) and V (event 7) complete
 #ifndef F3S_TRACE_EV0
 #define F3S_TRACE_EV0 0
 #endif
@@ -600,17 +603,10 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             tc_fence_after();
             uint64_t t_s = 0;
             if (kDiag && p == 0) { t_s = globaltimer_ns(); lap(1); }
-            // MMA2 reads P^T columns [0, ralloc): a warp whose 32 columns all lie beyond has no
-            // score to load, no P to write and contributes -inf to the row max and 0 to l
-            // (warp-uniform; most chunks of small row windows use one or two of the four warps)
-#ifndef F3S_ACT
-#define F3S_ACT 0
-#endif
-            const bool act = !F3S_ACT || 32 * q < sl.ralloc;
             float x[16];
-            if ((expt & 32) || !act) {
+            if (expt & 32) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) x[i] = (expt & 32) ? 0.f : -INFINITY;
+                for (int i = 0; i < 16; ++i) x[i] = 0.f;
             } else {
                 tmem_ld_32x32b_x16(tmem + tl + (b * HG + (HG > 1 ? q : 0)) * 16, x);
 #pragma unroll
@@ -618,7 +614,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             // chunk row max (Alg.1 l.16): warp butterfly (+ 4-warp combine when the chunk's columns
             // span the four warps, HG = 1)
-            const float rm = ((expt & 32) || !act) ? ((expt & 32) ? 0.f : -INFINITY) : rowreduce16(x, lane, OpMax());
+            const float rm = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
             if (HG == 1) {
                 if (!(lane & 1)) red[(b * 4 + q) * 16 + ((lane >> 1) & 15)] = rm;
                 if (p == 0) lap(2);
@@ -656,7 +652,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     m[i] = fmaxf(kMFloor, cm[i]);
-                    pv[i] = ((expt & 1) || !act) ? 0.f : ex2(x[i] - m[i]);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
+                    pv[i] = (expt & 1) ? x[i] : ex2(x[i] - m[i]);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
                     l[i] = pv[i];
                     av[i] = 0.f;
                 }
@@ -666,12 +662,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     const float mn = fmaxf(m[i], cm[i]);
                     av[i] = (expt & 1) ? 1.f : ex2(m[i] - mn);  // e^{m_o - m_i} (l.18, l.21)
                     m[i] = mn;
-                    pv[i] = ((expt & 1) || !act) ? 0.f : ex2(x[i] - mn);
+                    pv[i] = (expt & 1) ? x[i] : ex2(x[i] - mn);
                     l[i] = fmaf(l[i], av[i], pv[i]);  // l_o (l.18)
                 }
             }
             if (p == 0) lap(6);
-            if (act) {  // E cast to the input dtype into SMEM (l.19): two 16-byte stores
+            {  // E cast to the input dtype into SMEM (l.19): two 16-byte stores
                 const uint4 lo = make_uint4(pack2<T>(pv[0], pv[1]), pack2<T>(pv[2], pv[3]), pack2<T>(pv[4], pv[5]),
                                             pack2<T>(pv[6], pv[7]));
                 const uint4 hi = make_uint4(pack2<T>(pv[8], pv[9]), pack2<T>(pv[10], pv[11]), pack2<T>(pv[12], pv[13]),
@@ -692,10 +688,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
             }
             if (p == 0) lap(7);
-#ifndef F3S_NOFENCE
-#define F3S_NOFENCE 0
-#endif
-            if (!F3S_NOFENCE) fence_proxy_async_smem();
+            fence_proxy_async_smem();
             tc_fence_before();
             if (F3S_TRACE_EV0 == 3 && kDiag && lane == 0) corr[b].tq[q] = globaltimer_ns();
             mbar_arrive(bar(B::pfull(b)));
@@ -855,10 +848,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const bool has = D == 128 || lane < 16;
                 const int f = D == 128 ? 32 * q + lane : 16 * q + lane;  // O^T lane -> feature (M = 64 layout)
                 bool do_store = true;
-#ifndef F3S_SPLIT_CODE
-#define F3S_SPLIT_CODE 1
-#endif
-                if (F3S_SPLIT_CODE && split) {
+                if (split) {
                     // piece of a split row window: leave (m, l, unnormalised O) in the scratch
                     // record of its global piece; k_split_merge combines the pieces after the
                     // kernel, in piece order (deterministic)
@@ -885,20 +875,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 // past n_rows of a ragged last window are clipped by the tensor map, reading c14)
                 const int ob = item % C::kNO;
                 float* ost = reinterpret_cast<float*>(smem + C::oOst + ob * C::kOBytes);
-#ifndef F3S_OSTG
-#define F3S_OSTG 0
-#endif
-                if (!do_store) {
-                } else if (F3S_OSTG) {  // direct coalesced stores: lane = feature, one row per instruction
-                    const int nvalid = min(16, n_rows - 16 * rw);  // ragged last window (reading c14)
-                    if (has && !(expt & 64)) {
-                        const int64_t ld = (int64_t)H * D;
-                        float* out = O + (int64_t)16 * rw * ld + (int64_t)hd * D + f;
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            if (i < nvalid) out[(int64_t)i * ld] = oacc[i] * inv[i];
-                    }
-                } else {
+                if (do_store) {
                     if (threadIdx.x == 32 * C::kCorr0) bulk_wait_group_read<C::kNO - 1>();  // staging tile ob free
                     named_bar_sync(3, 128);
                     if (has) {
@@ -1047,7 +1024,6 @@ f3s_status launch(const AttnArgs& a) {
     int chunk_rows = 128;
     if (const char* env = getenv("F3S_CHUNK_ROWS"))
         if (HG == 1) chunk_rows = std::max(16, std::min(128, atoi(env) / 16 * 16));  // (HG > 1: one chunk per item)
-    static uint32_t mma_sleep_ns = getenv("F3S_MMA_SLEEP") ? (uint32_t)atoi(getenv("F3S_MMA_SLEEP")) : 0u;
     int32_t* counter = p.counters + (g_call.fetch_add(1) % kNumCounterSlots);
     F3S_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int32_t), a.stream));
     auto kern = a.trace ? k_f3s_sm100<D, T, true, HG> : k_f3s_sm100<D, T, false, HG>;
@@ -1060,7 +1036,7 @@ f3s_status launch(const AttnArgs& a) {
     kern<<<grid, C::kThreads, C::kSmemBytes, a.stream>>>(
         mq, mk, mv, mo, a.lpt ? p.meta_sub : p.meta_nat, p.kcols, p.kmasks, counter,
         n_items, a.heads, p.n_rows, chunk_rows, static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.O,
-        a.scale * 1.4426950408889634f, a.trace, a.trace_chunks, a.expt, mma_sleep_ns, scratch);
+        a.scale * 1.4426950408889634f, a.trace, a.trace_chunks, a.expt, scratch);
     count_launch();
     F3S_CUDA_TRY(cudaGetLastError());
     if (split) {

@@ -62,15 +62,13 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     return t;
 }
 // Blocking wait with a watchdog: a pipeline bug traps (launch failure) instead of hanging the GPU.
-// The global-timer read between retries doubles as a back-off: measured, both a tighter spin and
-// a long suspend hint in try_wait were slower (issue-slot pressure / wake-up latency).
-#ifndef F3S_WAIT_HINT_NS
-#define F3S_WAIT_HINT_NS 0
-#endif
+// try_wait suspends the thread in hardware for a short system time limit; the global-timer read
+// between retries doubles as a back-off.  (Measured: both a tighter spin and a long suspend hint
+// were slower — issue-slot pressure / wake-up latency on the pipeline's critical path.)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = globaltimer_ns();
-    while (!(F3S_WAIT_HINT_NS > 0 ? mbar_try_wait_hint(bar, parity, F3S_WAIT_HINT_NS) : mbar_try_wait(bar, parity))) {
+    while (!mbar_try_wait(bar, parity)) {
         if (globaltimer_ns() - t0 > 20000000000ull) __trap();
     }
 }
