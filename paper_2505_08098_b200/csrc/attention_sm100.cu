@@ -103,7 +103,10 @@ struct Cfg {
     // two softmax warpgroups take alternate work items: one warpgroup's chunk is a long chain of
     // dependent short-latency steps (measured: issue-active ~17% of its cycles), so a second
     // independent chain doubles the softmax throughput
-    static constexpr int kSoftmaxWGs = 2;
+#ifndef F3S_SMWG
+#define F3S_SMWG 2
+#endif
+    static constexpr int kSoftmaxWGs = F3S_SMWG;
     static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps + 1,
                          kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
     static constexpr int kThreads = 32 * (kCorr0 + 4);  // control, MMA, index, loaders, softmax, correction
@@ -133,8 +136,8 @@ template <int D, int HG> struct Bars {
     __host__ __device__ static constexpr int lempty(int b) { return kB0 + 4 * C::kSB + C::kLB + b; }
     __host__ __device__ static constexpr int rfull(int s) { return kB0 + 4 * C::kSB + 2 * C::kLB + s; }
     __host__ __device__ static constexpr int kempty(int s) { return kB0 + 4 * C::kSB + 2 * C::kLB + C::kNS + s; }
-    // S^T buffer b may be overwritten by MMA1: both softmax warpgroups passed its previous chunk
-    // (the owner after the P-tile wait, the other in its skip path): 8 warp arrivals
+    // S^T buffer b may be overwritten by MMA1: every softmax warpgroup passed its previous chunk
+    // (the owner after the P-tile wait, the others in their skip path): 4 warp arrivals each
     __host__ __device__ static constexpr int sfree(int b) { return kB0 + 4 * C::kSB + 2 * C::kLB + 2 * C::kNS + b; }
 };
 
@@ -263,7 +266,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             mbar_init(bar(B::pfull(b)), 128);
             mbar_init(bar(B::ofull(b)), 1);
             mbar_init(bar(B::pempty(b)), 128);
-            mbar_init(bar(B::sfree(b)), 8);
+            mbar_init(bar(B::sfree(b)), 4 * C::kSoftmaxWGs);
         }
         for (int b = 0; b < C::kLB; ++b) {
             mbar_init(bar(B::lfull(b)), 128);
@@ -585,7 +588,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             const int flags = sl.flags;
             if (flags & 1) ++item;
-            if ((item & 1) != wg) {  // the other warpgroup's item
+            if (item % C::kSoftmaxWGs != wg) {  // another warpgroup's item
                 // Observe the phase of the shared S^T buffer b, then release it: MMA1 may refill
                 // buffer b only when both warpgroups passed this chunk, so neither can take phase
                 // k+1 of sfull(b) for phase k.  Free of cost: MMA1 completes in chunk order, so
@@ -755,7 +758,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 mbar_wait(bar(B::lfull(ib)), (item / C::kLB) & 1);
                 float* ost = reinterpret_cast<float*>(smem + C::oOst);
                 if (lead) bulk_wait_group_read<0>();  // the previous item's store has read the tile
-                named_bar_sync(3, 128);
+                named_bar_sync(1 + C::kSoftmaxWGs, 128);
                 const bool has = lane < 16;           // O^T lane -> feature 16q + lane (M = 64 layout)
                 const int f = 16 * q + lane;
 #pragma unroll 1
@@ -780,7 +783,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 mbar_arrive(bar(B::pempty(b)));
                 mbar_arrive(bar(B::lempty(ib)));
                 fence_proxy_async_smem();
-                named_bar_sync(3, 128);
+                named_bar_sync(1 + C::kSoftmaxWGs, 128);
                 if (lead) {
                     if (!(expt & 64)) tma_store_2d(&tmO, sb + C::oOst, hd * D, 16 * rw);
                     bulk_commit_group();
@@ -877,13 +880,13 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 float* ost = reinterpret_cast<float*>(smem + C::oOst + ob * C::kOBytes);
                 if (do_store) {
                     if (threadIdx.x == 32 * C::kCorr0) bulk_wait_group_read<C::kNO - 1>();  // staging tile ob free
-                    named_bar_sync(3, 128);
+                    named_bar_sync(1 + C::kSoftmaxWGs, 128);
                     if (has) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) ost[i * D + f] = oacc[i] * inv[i];
                     }
                     fence_proxy_async_smem();
-                    named_bar_sync(3, 128);
+                    named_bar_sync(1 + C::kSoftmaxWGs, 128);
                     if (threadIdx.x == 32 * C::kCorr0) {
                         if (!(expt & 64)) tma_store_2d(&tmO, sb + C::oOst + ob * C::kOBytes, hd * D, 16 * rw);
                         bulk_commit_group();

@@ -17,3 +17,4 @@ timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -c
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_f3s_sm100 -s 3 -c 1 -o gpurun_out/${T}_prof_arxiv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_f3s_sm100 -s 3 -c 1 -o gpurun_out/${T}_prof_batched python bench.py --config batched --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 ls gpurun_out | grep "^${T}_" | head -50
+for c in arxiv batched reddit cora; do timeout -s KILL 300 python tools/bench_backward.py --config $c 2>/dev/null | tail -1; done > gpurun_out/${T}_bench_backward.jsonl
