@@ -255,19 +255,20 @@ __global__ void __launch_bounds__(256) k_bwd_cols(const int32_t* __restrict__ li
     for (int e = 0; e < E; ++e) { dK[jb + e] = gk[e]; dV[jb + e] = gv[e]; }
 }
 
-// heavy columns (more than kHeavyCol rows: power-law in-degree hubs): one block of 8 warps per
-// (column, head); warp w takes rows w, w+8, ... and the 8 partial sums are added in warp order
+// heavy columns (more than kHeavyCol rows: power-law in-degree hubs): one block of NW = 8 (32 above
+// kHugeCol rows) warps per (column, head); warp w takes rows w, w+NW, ... and the NW partial sums
+// are added in warp order
 // (deterministic).  A hub of 13,000 rows on one warp alone set the whole pass's time.
-constexpr int kHeavyCol = 64;
-template <int D, typename T>
-__global__ void __launch_bounds__(256) k_bwd_cols_heavy(const int32_t* __restrict__ heavy, const int32_t* __restrict__ col_ptr,
+constexpr int kHeavyCol = 64, kHugeCol = 1024;  // > kHugeCol rows: 32 warps
+template <int D, typename T, int NW>
+__global__ void __launch_bounds__(32 * NW) k_bwd_cols_heavy(const int32_t* __restrict__ heavy, const int32_t* __restrict__ col_ptr,
                                                         const int32_t* __restrict__ col_rows, int H,
                                                         const T* __restrict__ Q, const T* __restrict__ K,
                                                         const T* __restrict__ V, const float* __restrict__ dO,
                                                         const float* __restrict__ lse, const float* __restrict__ Drow,
                                                         float* __restrict__ dK, float* __restrict__ dV, float scale) {
     constexpr int E = D / 32;
-    __shared__ float part[8][2][D];
+    __shared__ float part[NW][2][D];
     const float scale_log2 = scale * 1.4426950408889634f;
     const int64_t j = heavy[blockIdx.x / H];
     const int h = blockIdx.x - (blockIdx.x / H) * H;
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(256) k_bwd_cols_heavy(const int32_t* __restric
     float kv[E], vv[E], gk[E], gv[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) { kv[e] = to_f(K[jb + e]); vv[e] = to_f(V[jb + e]); gk[e] = 0.f; gv[e] = 0.f; }
-    for (int32_t t = col_ptr[j] + w; t < col_ptr[j + 1]; t += 8) {
+    for (int32_t t = col_ptr[j] + w; t < col_ptr[j + 1]; t += NW) {
         const int64_t i = col_rows[t];
         const int64_t ib = i * ld + h * D + lane * E;
         float qv[E], gi[E], s = 0.f, dp = 0.f;
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(256) k_bwd_cols_heavy(const int32_t* __restric
         const int which = f / D, x = f - which * D;
         float acc = 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc += part[u][which][x];  // fixed order
+        for (int u = 0; u < NW; ++u) acc += part[u][which][x];  // fixed order
         (which ? dV : dK)[j * ld + h * D + x] = acc;
     }
 }
@@ -398,12 +399,15 @@ f3s_status build_transpose(Plan& p, cudaStream_t stream) {
     std::vector<int32_t> h_cp((size_t)p.n_cols + 1);
     F3S_CUDA_TRY(cudaMemcpyAsync(h_cp.data(), col_ptr, sizeof(int32_t) * h_cp.size(), cudaMemcpyDeviceToHost, stream));
     F3S_CUDA_TRY(cudaStreamSynchronize(stream));
-    std::vector<int32_t> light, heavy;
+    std::vector<int32_t> light, heavy, huge;
     for (int32_t j = 0; j < p.n_cols; ++j) {
         const int32_t c = h_cp[j + 1] - h_cp[j];
-        if (c > kHeavyCol) heavy.push_back(j);
+        if (c > kHugeCol) huge.push_back(j);
+        else if (c > kHeavyCol) heavy.push_back(j);
         else if (c > 0) light.push_back(j);
     }
+    const int32_t n_heavy8 = (int32_t)heavy.size();
+    heavy.insert(heavy.end(), huge.begin(), huge.end());  // heavy list: 8-warp columns, then 32-warp ones
     // (columns without rows get dK = dV = 0 from a memset in launch_bwd)
     int32_t* lists = nullptr;
     F3S_CUDA_TRY(cudaMalloc(&lists, sizeof(int32_t) * (light.size() + heavy.size() + 1)));
@@ -442,6 +446,7 @@ f3s_status build_transpose(Plan& p, cudaStream_t stream) {
     p.col_lists = lists;
     p.n_light = (int32_t)light.size();
     p.n_heavy = (int32_t)heavy.size();
+    p.n_heavy8 = n_heavy8;
     return F3S_OK;
 }
 
@@ -493,10 +498,16 @@ f3s_status launch_bwd(Plan& p, const void* Q, const void* K, const void* V, cons
                                                                 static_cast<const T*>(V), dO, lse, drow, dK, dV, scale);
         count_launch();
     }
-    if (p.n_heavy > 0) {
-        k_bwd_cols_heavy<D, T><<<(unsigned)((int64_t)p.n_heavy * H), 256, 0, stream>>>(
+    if (p.n_heavy8 > 0) {
+        k_bwd_cols_heavy<D, T, 8><<<(unsigned)((int64_t)p.n_heavy8 * H), 256, 0, stream>>>(
             p.col_lists + p.n_light, p.col_ptr, p.col_rows, H, static_cast<const T*>(Q), static_cast<const T*>(K),
             static_cast<const T*>(V), dO, lse, drow, dK, dV, scale);
+        count_launch();
+    }
+    if (p.n_heavy > p.n_heavy8) {
+        k_bwd_cols_heavy<D, T, 32><<<(unsigned)((int64_t)(p.n_heavy - p.n_heavy8) * H), 1024, 0, stream>>>(
+            p.col_lists + p.n_light + p.n_heavy8, p.col_ptr, p.col_rows, H, static_cast<const T*>(Q),
+            static_cast<const T*>(K), static_cast<const T*>(V), dO, lse, drow, dK, dV, scale);
         count_launch();
     }
     F3S_CUDA_TRY(cudaGetLastError());

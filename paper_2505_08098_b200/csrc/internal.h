@@ -47,7 +47,7 @@ struct Plan {
     int32_t* col_ptr = nullptr;   // [n_cols + 1]
     int32_t* col_rows = nullptr;  // [nnz]
     int32_t* col_lists = nullptr; // [n_light + n_heavy]: columns with 1..64 rows, then with more
-    int32_t n_light = 0, n_heavy = 0;
+    int32_t n_light = 0, n_heavy = 0, n_heavy8 = 0;  // heavy list = n_heavy8 8-warp columns, then 32-warp ones
     int32_t* heavy_rows = nullptr;    // rows with more than 256 entries (backward row pass)
     uint8_t* heavy_row_flag = nullptr;  // [n_rows]
     int32_t n_heavy_rows = 0;
