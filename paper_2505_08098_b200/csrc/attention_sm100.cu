@@ -625,10 +625,6 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             // P_b / corr_b are free once the correction group consumed chunk seq - kSB
             mbar_wait(bar(B::pempty(b)), bph ^ 1);
-            // S^T_b was loaded above; releasing it only now (after the P-tile wait) also keeps the
-            // pempty phases exact: MMA1(seq + kSB) then implies the correction consumed seq - kSB
-            tc_fence_before();
-            if (lane == 0) mbar_arrive(bar(B::sfree(b)));
             if (p == 0) lap(3);
             const float4* r4 = reinterpret_cast<const float4*>(red + b * 64);
             // P^T is the MN-major B operand of MMA2 with a 32-byte swizzle: compacted column p
@@ -651,6 +647,13 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                 for (int i = 0; i < 16; ++i) cm[i] = __shfl_sync(0xffffffffu, rm, 2 * i);
             }
+            // Release S^T_b (loaded above) and the row-max partials red[b] (read just above: the
+            // owner of chunk seq + kSB rewrites them once MMA1 refilled S^T_b).  Releasing after the
+            // P-tile wait also keeps the pempty phases exact: MMA1(seq + kSB) then implies the
+            // correction consumed chunk seq - kSB.
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(B::sfree(b)));
             if (flags & 1) {  // item's first chunk: m_o = floor, l_o = 0, nothing to rescale (alpha = 0)
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
