@@ -254,7 +254,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             mbar_init(bar(B::kfull(s)), 32 * C::kLoaderWarps);  // one cp.async completion per loader lane
             mbar_init(bar(B::vfull(s)), 32 * C::kLoaderWarps);
             mbar_init(bar(B::rfull(s)), 1);
-            mbar_init(bar(B::empty(s)), 1);   // V tile (and the slot) retired: MMA2 done
+            // V tile and slot retired: MMA2 done and every softmax warp has read the slot (a warp
+            // that lags behind must not find the slot already refilled with chunk seq + kNS)
+            mbar_init(bar(B::empty(s)), 1 + 4 * C::kSoftmaxWGs);
             mbar_init(bar(B::kempty(s)), 1);  // K tile retired: MMA1 done
         }
         for (int q = 0; q < C::kNQ; ++q) {
@@ -589,6 +591,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int flags = sl.flags;
             if (flags & 1) ++item;
             if (item % C::kSoftmaxWGs != wg) {  // another warpgroup's item
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar(B::empty(s)));  // done with the slot
                 // Observe the phase of the shared S^T buffer b, then release it: MMA1 may refill
                 // buffer b only when both warpgroups passed this chunk, so neither can take phase
                 // k+1 of sfull(b) for phase k.  Free of cost: MMA1 completes in chunk order, so
@@ -602,6 +606,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int col = HG == 1 ? p : lane;
             const uint32_t mask = col < rows ? (uint32_t)sl.masks[col] : 0u;
             const int rw = sl.rw, hd = sl.head, sp = flags >> 8;  // split piece (0: none)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(B::empty(s)));  // done with the slot
             mbar_wait(bar(B::sfull(b)), bph);
             tc_fence_after();
             uint64_t t_s = 0;
