@@ -254,9 +254,10 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             mbar_init(bar(B::kfull(s)), 32 * C::kLoaderWarps);  // one cp.async completion per loader lane
             mbar_init(bar(B::vfull(s)), 32 * C::kLoaderWarps);
             mbar_init(bar(B::rfull(s)), 1);
-            // V tile and slot retired: MMA2 done and every softmax warp has read the slot (a warp
-            // that lags behind must not find the slot already refilled with chunk seq + kNS)
-            mbar_init(bar(B::empty(s)), 1 + 4 * C::kSoftmaxWGs);
+            // V tile and slot retired: MMA2 done and the warps of the other softmax warpgroup(s)
+            // have read the slot header (a warpgroup lagging in its skip path must not find the
+            // slot refilled with chunk seq + kNS; the owner read it before its P, hence before MMA2)
+            mbar_init(bar(B::empty(s)), 1 + 4 * (C::kSoftmaxWGs - 1));
             mbar_init(bar(B::kempty(s)), 1);  // K tile retired: MMA1 done
         }
         for (int q = 0; q < C::kNQ; ++q) {
@@ -606,8 +607,6 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int col = HG == 1 ? p : lane;
             const uint32_t mask = col < rows ? (uint32_t)sl.masks[col] : 0u;
             const int rw = sl.rw, hd = sl.head, sp = flags >> 8;  // split piece (0: none)
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar(B::empty(s)));  // done with the slot
             mbar_wait(bar(B::sfull(b)), bph);
             tc_fence_after();
             uint64_t t_s = 0;

@@ -160,3 +160,26 @@ def test_config_full_parity(f3s, oracle_mod, cfg):
     O = run(f3s, csr, Qb, Kb, Vb, w.dtype, w.scale)
     ref = oracle_mod.attention(csr.row_ptr, csr.col_idx, Qb, Kb, Vb, scale=w.scale, dtype=w.dtype)
     assert_close(O, ref)
+
+
+@pytest.mark.parametrize("heads", [1, 2])
+def test_long_items_under_perturbed_timing(f3s, oracle_mod, heads):
+    """Long work items (dense communities: row windows of ~20 chunks) run through the profile-mode
+    build of the kernel, whose extra clock reads slow some warps down: the barrier protocol must
+    not depend on timing (this configuration exposed a slot-recycling race)."""
+    import torch
+    csr = fi.dcsbm(24000, 3000000, comm_size=3000, mu=0.9, gamma=2.1, max_deg=2000, seed=31)
+    Qb, Kb, Vb = make_qkv(csr.n_rows, csr.n_cols, heads, 64, "fp16", seed=33)
+    rp, ci = csr_to_dev(csr)
+    p = f3s.plan(rp, ci, csr.n_rows)
+    Q, K, V = to_dev(Qb, "fp16"), to_dev(Kb, "fp16"), to_dev(Vb, "fp16")
+    O = torch.empty(Q.shape, dtype=torch.float32, device="cuda")
+    f3s.attention_trace(p, Q, K, V, O, scale=0.125, trace_chunks=0)  # profile mode
+    torch.cuda.synchronize()
+    rows = np.arange(0, csr.n_rows, 7, dtype=np.int32)
+    ref = oracle_mod.attention(csr.row_ptr, csr.col_idx, Qb, Kb, Vb, scale=0.125, rows=rows)
+    assert_close(O.cpu().numpy()[rows], ref)
+    # and the product kernel on the same plan
+    O2 = f3s.attention(p, Q, K, V, scale=0.125)
+    torch.cuda.synchronize()
+    assert_close(O2.cpu().numpy()[rows], ref)
