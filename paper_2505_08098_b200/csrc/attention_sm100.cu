@@ -964,8 +964,41 @@ EncodeTiledFn get_encode() {
 
 // 2-D tensor map over a row-major [rows, inner] matrix; 16-bit elements use 64-element (128-byte)
 // boxes with the 128-byte swizzle of the UMMA tiles, fp32 (O) a dense unswizzled box_inner-wide box
+// Encoding a tensor map costs a few microseconds of host time per call, which dominates small
+// launches (cora); the last few encodings are reused (per host thread) for identical arguments.
+struct MapKey {
+    const void* base;
+    int64_t inner, rows;
+    uint32_t type, box_inner, box_rows, swz;
+    bool operator==(const MapKey& o) const {
+        return base == o.base && inner == o.inner && rows == o.rows && type == o.type && box_inner == o.box_inner &&
+               box_rows == o.box_rows && swz == o.swz;
+    }
+};
+f3s_status make_map_uncached(CUtensorMap* map, const void* base, CUtensorMapDataType type, int64_t inner,
+                             int64_t rows, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz);
 f3s_status make_map(CUtensorMap* map, const void* base, CUtensorMapDataType type, int64_t inner, int64_t rows,
                     uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz) {
+    constexpr int kCache = 8;
+    thread_local MapKey keys[kCache];
+    thread_local CUtensorMap maps[kCache];
+    thread_local int used = 0, next = 0;
+    const MapKey k{base, inner, rows, (uint32_t)type, box_inner, box_rows, (uint32_t)swz};
+    for (int i = 0; i < used; ++i)
+        if (keys[i] == k) {
+            *map = maps[i];
+            return F3S_OK;
+        }
+    f3s_status st = make_map_uncached(map, base, type, inner, rows, box_inner, box_rows, swz);
+    if (st != F3S_OK) return st;
+    keys[next] = k;
+    maps[next] = *map;
+    next = (next + 1) % kCache;
+    if (used < kCache) ++used;
+    return F3S_OK;
+}
+f3s_status make_map_uncached(CUtensorMap* map, const void* base, CUtensorMapDataType type, int64_t inner,
+                             int64_t rows, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz) {
     EncodeTiledFn enc = get_encode();
     if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return F3S_ERR_CUDA; }
     const int esz = type == CU_TENSOR_MAP_DATA_TYPE_FLOAT32 ? 4 : 2;
