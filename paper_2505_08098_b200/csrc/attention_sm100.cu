@@ -87,8 +87,15 @@ struct Cfg {
     static constexpr int oCorr = oLm + kLB * 16 * 4;        // CorrSlot [kSB]
     static constexpr int kCorrBytes = 128;                  // sizeof(CorrSlot)
     static constexpr int oReg = oCorr + kSB * kCorrBytes;   // int2 [2][kNS] ring regions (K, V)
+    // per-chunk flags for the softmax warpgroups, in a ring longer than the slot ring: a warpgroup
+    // that skips another's chunk reads them here, never the slot (which MMA2 may already have
+    // retired and the index warp refilled); chunk c's entry is rewritten only after MMA1 of
+    // chunk c + kNI - kNS, i.e. after every warpgroup passed chunk c
+    static constexpr int kNI = 64;
+    static_assert(kNI >= kNS + 2 * kSB + 8, "info ring");
+    static constexpr int oInfo = oReg + 2 * kNS * 8;        // int [kNI]
     static constexpr int kNumBars = 6 * kNS + 2 * kNQ + 5 * kSB + 2 * kLB;
-    static constexpr int oBar = oReg + 2 * kNS * 8;
+    static constexpr int oBar = oInfo + kNI * 4;
     static constexpr int oTmem = oBar + kNumBars * 8;
     static constexpr int kSmemBytes = oTmem + 16;
     static constexpr int kCtasPerSm = 1;
@@ -254,10 +261,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             mbar_init(bar(B::kfull(s)), 32 * C::kLoaderWarps);  // one cp.async completion per loader lane
             mbar_init(bar(B::vfull(s)), 32 * C::kLoaderWarps);
             mbar_init(bar(B::rfull(s)), 1);
-            // V tile and slot retired: MMA2 done and the warps of the other softmax warpgroup(s)
-            // have read the slot header (a warpgroup lagging in its skip path must not find the
-            // slot refilled with chunk seq + kNS; the owner read it before its P, hence before MMA2)
-            mbar_init(bar(B::empty(s)), 1 + 4 * (C::kSoftmaxWGs - 1));
+            mbar_init(bar(B::empty(s)), 1);   // V tile (and the slot) retired: MMA2 done
             mbar_init(bar(B::kempty(s)), 1);  // K tile retired: MMA1 done
         }
         for (int q = 0; q < C::kNQ; ++q) {
@@ -331,6 +335,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         sl.rows = rows;
                         sl.qslot = qs;
                         sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2) | (sp << 8);
+                        reinterpret_cast<volatile int32_t*>(smem + C::oInfo)[seq % C::kNI] = sl.flags;
                         sl.ralloc = rows > 0 ? (HG == 1 ? ((rows + 15) & ~15) : C::kMaxRows) : 0;
                         const uint32_t fb = bar(B::idxfull(s));
                         if (rows > 0) {
@@ -359,6 +364,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int s = seq % C::kNS;
             mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
             slots[s].rows = -1;
+            reinterpret_cast<volatile int32_t*>(smem + C::oInfo)[seq % C::kNI] = -1;
             mbar_arrive(bar(B::idxfull(s)));
             prof_flush(0);
         }
@@ -579,8 +585,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             mbar_wait(bar(B::kfull(s)), (seq / C::kNS) & 1);
             if (p == 0) lap(0);
             const Slot& sl = slots[s];
-            const int rows = sl.rows;
-            if (rows < 0) {  // warpgroup 0 forwards the stop to the correction group
+            const int info = reinterpret_cast<const volatile int32_t*>(smem + C::oInfo)[seq % C::kNI];
+            if (info < 0) {  // warpgroup 0 forwards the stop to the correction group
                 if (wg == 0) {
                     mbar_wait(bar(B::pempty(b)), bph ^ 1);
                     if (p == 0) corr[b].rows = -1;
@@ -589,11 +595,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
                 break;
             }
-            const int flags = sl.flags;
+            const int flags = info;
             if (flags & 1) ++item;
             if (item % C::kSoftmaxWGs != wg) {  // another warpgroup's item
-                __syncwarp();
-                if (lane == 0) mbar_arrive(bar(B::empty(s)));  // done with the slot
                 // Observe the phase of the shared S^T buffer b, then release it: MMA1 may refill
                 // buffer b only when both warpgroups passed this chunk, so neither can take phase
                 // k+1 of sfull(b) for phase k.  Free of cost: MMA1 completes in chunk order, so
@@ -603,6 +607,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 ++seq;
                 continue;
             }
+            // the owner reads the slot: it cannot be retired before this chunk's P (MMA2 needs it)
+            const int rows = sl.rows;
             // S^T lane p <-> compacted column p (HG = 1), or column `lane` of head q (HG = 4)
             const int col = HG == 1 ? p : lane;
             const uint32_t mask = col < rows ? (uint32_t)sl.masks[col] : 0u;
