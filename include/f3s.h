@@ -192,6 +192,13 @@ f3s_status f3s_attention_trace(f3s_plan_t plan, const void* Q, const void* K, co
  */
 f3s_status f3s_attention_host(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O,
                               float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
+/* The same, stream-ordered: returns once the copies, the fused call and the read-back are
+ * enqueued; O is valid after `stream` completes.  The device staging buffer belongs to the
+ * stream (one per stream and plan), so calls on two streams overlap one call's host-to-device
+ * copies with the other's device-to-host copy (full-duplex PCIe/NVLink-C2C).  With pageable host
+ * memory the copies are synchronous (CUDA semantics); use pinned buffers to overlap. */
+f3s_status f3s_attention_host_async(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O,
+                                    float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
 
 /*
  * Host partitioner for multi-GPU runs: split rows [0, n) into `parts` contiguous ranges whose

@@ -124,7 +124,7 @@ f3s_status f3s_plan_destroy(f3s_plan_t plan) {
     cudaFree(p->col_lists);
     cudaFree(p->heavy_rows);
     cudaFree(p->heavy_row_flag);
-    cudaFree(p->staging);
+    for (auto& st : p->staging) cudaFree(st.ptr);
     delete p;
     return F3S_OK;
 }
@@ -215,23 +215,36 @@ f3s_status f3s_attention_trace(f3s_plan_t plan, const void* Q, const void* K, co
     }
 }
 
-f3s_status f3s_attention_host(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
-                              int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
+f3s_status f3s_attention_host_async(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O,
+                                    float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
     f3s_status st = check_attention_args(plan, Q, K, V, O, scale, heads, d, dtype, false);
     if (st != F3S_OK) return st;
     Plan& p = *reinterpret_cast<Plan*>(plan);
     const size_t qn = (size_t)p.n_rows * heads * d, kn = (size_t)p.n_cols * heads * d;
     auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t need = up(qn * 2) + 2 * up(kn * 2) + up(qn * 4);
-    std::lock_guard<std::mutex> lock(p.staging_mu);
-    if (p.staging_bytes < need) {
-        cudaFree(p.staging);
-        p.staging = nullptr;
-        p.staging_bytes = 0;
-        F3S_CUDA_TRY(cudaMalloc(&p.staging, need));
-        p.staging_bytes = need;
+    char* base = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(p.staging_mu);
+        Plan::Staging* sg = nullptr;
+        for (auto& x : p.staging)
+            if (x.stream == stream) sg = &x;
+        if (!sg) {
+            p.staging.push_back({stream, nullptr, 0});
+            sg = &p.staging.back();
+        }
+        if (sg->bytes < need) {
+            if (sg->ptr) {  // the stream's earlier calls may still use the old buffer
+                F3S_CUDA_TRY(cudaStreamSynchronize(stream));
+                cudaFree(sg->ptr);
+            }
+            sg->ptr = nullptr;
+            sg->bytes = 0;
+            F3S_CUDA_TRY(cudaMalloc(&sg->ptr, need));
+            sg->bytes = need;
+        }
+        base = static_cast<char*>(sg->ptr);
     }
-    char* base = static_cast<char*>(p.staging);
     void* dQ = base;
     void* dK = base + up(qn * 2);
     void* dV = base + up(qn * 2) + up(kn * 2);
@@ -244,6 +257,13 @@ f3s_status f3s_attention_host(f3s_plan_t plan, const void* Q, const void* K, con
     st = run_attention(plan, dQ, dK, dV, dO, scale, heads, d, dtype, F3S_VARIANT_DEFAULT, stream);
     if (st != F3S_OK) return st;
     if (qn) F3S_CUDA_TRY(cudaMemcpyAsync(O, dO, qn * 4, cudaMemcpyDeviceToHost, stream));
+    return F3S_OK;
+}
+
+f3s_status f3s_attention_host(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
+                              int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
+    f3s_status st = f3s_attention_host_async(plan, Q, K, V, O, scale, heads, d, dtype, stream);
+    if (st != F3S_OK) return st;
     F3S_CUDA_TRY(cudaStreamSynchronize(stream));
     return F3S_OK;
 }

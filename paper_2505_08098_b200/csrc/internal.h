@@ -51,10 +51,15 @@ struct Plan {
     int32_t* heavy_rows = nullptr;    // rows with more than 256 entries (backward row pass)
     uint8_t* heavy_row_flag = nullptr;  // [n_rows]
     int32_t n_heavy_rows = 0;
-    // e2e staging buffers for f3s_attention_host
+    // e2e staging buffers for f3s_attention_host(_async): one device buffer per stream (reused by
+    // later calls on the same stream, which the stream order makes safe)
+    struct Staging {
+        cudaStream_t stream;
+        void* ptr;
+        size_t bytes;
+    };
     std::mutex staging_mu;
-    void* staging = nullptr;
-    size_t staging_bytes = 0;
+    std::vector<Staging> staging;
 };
 
 constexpr int kNumCounterSlots = 64;

@@ -50,6 +50,7 @@ _lib.f3s_attention_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i3
 _lib.f3s_attention_trace.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]
 _lib.f3s_attention_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_host_async.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_partition_rows.argtypes = [_vp, _i32, _i32, _vp]
 _lib.f3s_partition_at.argtypes = [_vp, _i32, _vp, _i32, _i32, _vp]
 _lib.f3s_status_string.argtypes = [_i32]
@@ -58,12 +59,12 @@ _lib.f3s_last_error.restype = ctypes.c_char_p
 _lib.f3s_launch_count.restype = _i64
 for _name in ("f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
               "f3s_attention", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows",
-              "f3s_partition_at", "f3s_attention_backward"):
+              "f3s_partition_at", "f3s_attention_backward", "f3s_attention_host_async"):
     getattr(_lib, _name).restype = _i32
 
 EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
             "f3s_attention", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows", "f3s_partition_at",
-            "f3s_attention_backward",
+            "f3s_attention_backward", "f3s_attention_host_async",
             "f3s_status_string", "f3s_last_error", "f3s_launch_count"]
 
 
@@ -210,6 +211,12 @@ def attention_host(p: Plan, Q, K, V, O, *, scale: float, heads: int, d: int, dty
         return x.ctypes.data if isinstance(x, np.ndarray) else x.data_ptr()
     _check(_lib.f3s_attention_host(p.handle, ptr(Q), ptr(K), ptr(V), ptr(O), float(scale), heads, d, dtype,
                                    _stream(stream)), "f3s_attention_host")
+
+
+def attention_host_async(p: Plan, Q, K, V, O, *, scale: float, heads: int, d: int, dtype: int, stream=None) -> None:
+    """f3s_attention_host_async: enqueue on `stream`; O (pinned host) is valid once the stream completes."""
+    _check(_lib.f3s_attention_host_async(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), O.data_ptr(), float(scale),
+                                         heads, d, dtype, _stream(stream)), "f3s_attention_host_async")
 
 
 def partition_rows(row_ptr: np.ndarray, parts: int) -> np.ndarray:

@@ -183,3 +183,23 @@ def test_long_items_under_perturbed_timing(f3s, oracle_mod, heads):
     O2 = f3s.attention(p, Q, K, V, scale=0.125)
     torch.cuda.synchronize()
     assert_close(O2.cpu().numpy()[rows], ref)
+
+
+def test_host_async_two_streams(f3s):
+    """f3s_attention_host_async: stream-ordered, one staging buffer per stream; two streams in flight
+    give the device path's result bit for bit."""
+    import torch
+    csr = fi.chung_lu(4000, 30000, gamma=2.4, max_deg=400, seed=17)
+    Qb, Kb, Vb = make_qkv(4000, 4000, 2, 64, "bf16", seed=17)
+    rp, ci = csr_to_dev(csr)
+    p = f3s.plan(rp, ci, 4000)
+    Od = f3s.attention(p, to_dev(Qb, "bf16"), to_dev(Kb, "bf16"), to_dev(Vb, "bf16"), scale=0.2).cpu().numpy()
+    pin = lambda b: torch.from_numpy(b.view(np.int16)).pin_memory()
+    Qh, Kh, Vh = pin(Qb), pin(Kb), pin(Vb)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.empty((4000, 2, 64), dtype=torch.float32).pin_memory() for _ in range(4)]
+    for t in range(4):
+        f3s.attention_host_async(p, Qh, Kh, Vh, outs[t], scale=0.2, heads=2, d=64, dtype=f3s.BF16, stream=streams[t % 2])
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.numpy(), Od)
