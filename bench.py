@@ -39,7 +39,8 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="arxiv")
     ap.add_argument("--variant", default="default", choices=["default", "no_reorder", "simt", "one_head"])
-    ap.add_argument("--dtype", default=None, choices=[None, "fp16", "bf16"])
+    ap.add_argument("--dtype", default=None, choices=[None, "fp16", "bf16", "e4m3"],
+                    help="e4m3: the workload's values rounded to FP8 E4M3 (SURVEY 8(f) f4; N = 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle work for cpu_baseline")
@@ -116,11 +117,33 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def algorithmic_bytes(info: dict, H: int, d: int, n_rows: int) -> int:
-    """K+V rows gathered once per row window (W*H*d*2 each), Q read once,
-    O written once in fp32, plus the plan (rw_ptr, rw_order int32; cols int32 + masks uint16)."""
+def algorithmic_bytes(info: dict, H: int, d: int, n_rows: int, eb: int = 2) -> int:
+    """K+V rows gathered once per row window (W*H*d*eb each), Q read once,
+    O written once in fp32, plus the plan (rw_ptr, rw_order int32; cols int32 + masks uint16);
+    eb = bytes per input element (2; 1 for e4m3)."""
     W, R = info["total_cols"], info["num_rw"]
-    return int(W * H * d * 2 * 2 + n_rows * H * d * 2 + n_rows * H * d * 4 + 4 * (R + 1) + 4 * R + 6 * W)
+    return int(W * H * d * eb * 2 + n_rows * H * d * eb + n_rows * H * d * 4 + 4 * (R + 1) + 4 * R + 6 * W)
+
+
+def e4m3_inputs(Qb, Kb, Vb):
+    """The workload's fp16 values rounded (RNE) to FP8 E4M3: (uint8 arrays, float64 decoded arrays)."""
+    import torch
+    out = []
+    for b in (Qb, Kb, Vb):  # fp16 bits -> float32 (exact) -> e4m3 (torch's RNE cast)
+        t = torch.from_numpy(np.ascontiguousarray(b).view(np.float16).astype(np.float32)).to(torch.float8_e4m3fn)
+        out.append((t.view(torch.uint8).numpy(), t.to(torch.float64).numpy()))
+    return [o[0] for o in out], [o[1] for o in out]
+
+
+def oracle_rows_f64(csr, rows, Qd, Kd, Vd, scale):
+    """fp64 oracle (attention_f64 on decoded values) for a subset of rows, via the sub-CSR of those rows."""
+    import oracle
+    rp = csr.row_ptr.astype(np.int64)
+    deg = rp[rows + 1] - rp[rows]
+    sub_rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    sub_ci = np.concatenate([csr.col_idx[rp[r]:rp[r + 1]] for r in rows]).astype(np.int32) if len(rows) else \
+        np.zeros(0, np.int32)
+    return oracle.attention_f64(sub_rp, sub_ci, np.ascontiguousarray(Qd[rows]), Kd, Vd, scale=scale)
 
 
 def padded_flops(rw_ptr: np.ndarray, H: int, d: int, chunk: int = 128) -> int:
@@ -130,7 +153,7 @@ def padded_flops(rw_ptr: np.ndarray, H: int, d: int, chunk: int = 128) -> int:
 
 
 # ---------------------------------------------------------------------------------------------
-def cpu_oracle_sample(w, csr, Qb, Kb, Vb, target_s: float, seed: int = 7):
+def cpu_oracle_sample(w, csr, Qb, Kb, Vb, target_s: float, seed: int = 7, f64: bool = False):
     """Time the fp64 oracle (as it stands) on a seeded random sample of rows; returns
     (edge-GFLOP/s, seconds, rows sampled, nnz sampled, threads, rows, O_ref)."""
     import oracle
@@ -140,8 +163,14 @@ def cpu_oracle_sample(w, csr, Qb, Kb, Vb, target_s: float, seed: int = 7):
     # calibrate on a small sample
     m = min(n, 2000)
     rows = np.sort(rng.choice(n, size=m, replace=False)).astype(np.int32)
+    # f64: Qb, Kb, Vb are decoded float64 arrays (e4m3 inputs)
+
+    def run(rows):
+        if f64:
+            return oracle_rows_f64(csr, rows, Qb, Kb, Vb, w.scale)
+        return oracle.attention(csr.row_ptr, csr.col_idx, Qb, Kb, Vb, scale=w.scale, dtype=w.dtype, rows=rows)
     t0 = time.perf_counter()
-    oracle.attention(csr.row_ptr, csr.col_idx, Qb, Kb, Vb, scale=w.scale, dtype=w.dtype, rows=rows)
+    run(rows)
     dt = max(time.perf_counter() - t0, 1e-4)
     per_row = dt / m
     m = int(min(n, max(m, target_s / per_row)))
@@ -150,7 +179,7 @@ def cpu_oracle_sample(w, csr, Qb, Kb, Vb, target_s: float, seed: int = 7):
     reps = max(1, int(round(target_s / max(per_row * m, 1e-3)))) if m == n else 1
     t0 = time.perf_counter()
     for _ in range(reps):
-        ref = oracle.attention(csr.row_ptr, csr.col_idx, Qb, Kb, Vb, scale=w.scale, dtype=w.dtype, rows=rows)
+        ref = run(rows)
     dt = time.perf_counter() - t0
     # useful flops counted on the deduplicated support (4 * nnz * d * H)
     nnz_s = int(deg[rows].sum())
@@ -166,7 +195,7 @@ def reference_arm(args, rank: int):
     import oracle
     from f3s_inputs import configs
     w = configs.get(args.config)
-    if args.dtype:
+    if args.dtype and args.dtype != "e4m3":  # (the oracle's speed does not depend on the input type)
         w.dtype = args.dtype
     csr = w.graph()
     Qb, Kb, Vb = w.qkv(csr)
@@ -231,17 +260,24 @@ def main():
     sp = stream.cuda_stream
 
     w = configs.get(args.config)
-    if args.dtype:
+    if args.dtype and args.dtype != "e4m3":
         w.dtype = args.dtype
+    dtype = args.dtype or w.dtype  # e4m3: the config's fp16 values rounded to e4m3
     csr = w.graph()
     H, d = w.H, w.d
-    dt_code = f3s.FP16 if w.dtype == "fp16" else f3s.BF16
-    tdt = torch.float16 if w.dtype == "fp16" else torch.bfloat16
+    dt_code = {"fp16": f3s.FP16, "bf16": f3s.BF16, "e4m3": f3s.E4M3}[dtype]
+    tdt = {"fp16": torch.float16, "bf16": torch.bfloat16, "e4m3": torch.float8_e4m3fn}[dtype]
+    eb = 1 if dtype == "e4m3" else 2
+    ht = torch.uint8 if eb == 1 else torch.int16  # host view of the input bits
     batched = w.name == "batched"
     Qb, Kb, Vb = w.qkv(csr)
+    Qo, Ko, Vo = Qb, Kb, Vb  # what the oracle gets
+    if dtype == "e4m3":
+        assert world == 1, "e4m3 bench: N = 1"
+        (Qb, Kb, Vb), (Qo, Ko, Vo) = e4m3_inputs(Qb, Kb, Vb)
 
     def dev_tensor(bits):
-        return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).to(dev).view(tdt)
+        return torch.from_numpy(np.ascontiguousarray(bits)).view(ht).to(dev).view(tdt)
 
     # ---- plan (one-time preprocessing; timed separately) ----
     if world == 1:
@@ -330,7 +366,7 @@ def main():
 
     # roofline of the dominant kernel (k_f3s_sm100), per launch on this rank
     rw_ptr = plan.export()[0]
-    b_alg = algorithmic_bytes(info, H, d, n_loc)
+    b_alg = algorithmic_bytes(info, H, d, n_loc, eb)
     f_pad = padded_flops(rw_ptr, H, d)
     hbm_gbs, bf16_tf, peak_src = load_peaks()
     achieved = b_alg / (kern_ms * 1e-3) / 1e9
@@ -344,9 +380,9 @@ def main():
     e2e = None
     if not args.no_e2e:
         if world == 1:
-            Qh = torch.from_numpy(Qb.view(np.int16)).pin_memory()
-            Kh = torch.from_numpy(Kb.view(np.int16)).pin_memory()
-            Vh = torch.from_numpy(Vb.view(np.int16)).pin_memory()
+            Qh = torch.from_numpy(Qb).view(ht).pin_memory()
+            Kh = torch.from_numpy(Kb).view(ht).pin_memory()
+            Vh = torch.from_numpy(Vb).view(ht).pin_memory()
             # consecutive steps alternate between two streams (each with its own device staging and
             # pinned output), so one step's host-to-device copies overlap the previous step's
             # device-to-host read-back; every step still copies its inputs in and its O out
@@ -419,7 +455,7 @@ def main():
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        gf, secs, rows, nnz_s, cores, ref, reps = cpu_oracle_sample(w, csr, Qb, Kb, Vb, args.cpu_seconds)
+        gf, secs, rows, nnz_s, cores, ref, reps = cpu_oracle_sample(w, csr, Qo, Ko, Vo, args.cpu_seconds, f64=eb == 1)
         cpu = {"value": round(gf, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{len(rows)} seeded random rows of {csr.n_rows} ({nnz_s} of {nnz_total} nnz) x {reps} "
                          f"pass(es), {secs:.1f} s fp64 on {cores} threads"}
@@ -428,13 +464,14 @@ def main():
         nr = np.linalg.norm(ref)
         parity = {"rows_checked": int(len(rows)), "max_abs": float(np.abs(diff).max()),
                   "rel_fro": float(np.linalg.norm(diff) / nr) if nr > 0 else float(np.linalg.norm(diff)),
-                  "tol": {"max_abs": 1e-2, "rel_fro": 5e-3}}
+                  "tol": {"max_abs": 1e-2, "rel_fro": 5e-3} if eb == 2 else
+                  "per row (2^-4 + deg * 2^-18) * max|V_j| (DESIGN.md c24)"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
-            "scaling": "weak" if batched else "strong", "vs_baseline": None, "dtype": "f16" if w.dtype == "fp16" else "bf16",
+            "scaling": "weak" if batched else "strong", "vs_baseline": None, "dtype": {"fp16": "f16", "bf16": "bf16", "e4m3": "e4m3"}[dtype],
             "data": "synthetic",
             "config": {"workload": w.description, "n": csr.n_rows, "nnz": nnz_total, "heads": H, "d": d,
                        "row_windows": info["num_rw"], "compacted_cols": info["total_cols"], "tcb16x8": info["total_tcb8"],

@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -47,10 +48,16 @@ using namespace sm100;
 // holds the window's columns for 4 heads, head g in tile rows / S^T lanes 32g .. 32g+31, so
 // softmax warp q works on head q alone (row max within the warp) and the per-chunk pipeline
 // cost is paid once per 4 heads.
-template <int D, int HG = 1>
+// EB = bytes per input element: 2 (fp16/bf16) or 1 (fp8 e4m3: d = 128, one 128-byte panel per row).
+template <int D, int HG = 1, int EB = 2>
 struct Cfg {
-    static_assert(HG == 1 || (HG == 4 && D == 64), "head groups: d = 64 only");
-    static constexpr int P = D / 64;                 // 128-byte panels per gathered row of one head
+    static_assert(HG == 1 || (HG == 4 && D == 64 && EB == 2), "head groups: d = 64 only");
+    static_assert(EB == 2 || (EB == 1 && D == 128 && HG == 1), "fp8: d = 128 only");
+    static constexpr int RB = D * EB;                // bytes of one gathered row of one head
+    static constexpr int P = RB / 128;               // 128-byte panels per gathered row of one head
+    // MMA2 K-step (chunk rows per instruction): 16 for kind::f16, 32 for kind::f8f6f4; ring tiles
+    // are allocated in whole K-steps
+    static constexpr int kRowAlign = 32 / EB;
     static constexpr int kGroupBytes = 1024 * P;     // 8 gathered rows (one swizzle atom per panel)
     static constexpr int kMaxRows = 128;             // compacted columns per chunk at most (MMA1 M = 128)
     // K tiles live until MMA1 completes, V tiles until MMA2 completes: two FIFO rings
@@ -66,7 +73,7 @@ struct Cfg {
     static constexpr int kRingBytes = kRingK + kRingV;
     static constexpr int kNS = D == 128 ? 20 : 22;   // chunk slots (ids, masks, descriptor, barriers)
     static constexpr int kNQ = HG == 4 ? 6 : D == 128 ? F3S_KNQ128 : 12;  // Q tile slots (items in flight per CTA)
-    static constexpr int kQBytes = 16 * D * 2 * HG;  // HG head tiles of 16 x D
+    static constexpr int kQBytes = 16 * RB * HG;     // HG head tiles of 16 x D
     static constexpr int kPBytes = 16 * kMaxRows * 2;
     static constexpr int kSB = 4;                    // S/P/O buffers in flight (TMEM and SMEM)
     static constexpr int kNO = HG == 4 ? 1 : 2;      // O staging tiles (16 x HG*D fp32) for the TMA store
@@ -126,8 +133,8 @@ struct Cfg {
     static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 };
 
-template <int D, int HG> struct Bars {
-    using C = Cfg<D, HG>;
+template <int D, int HG, int EB = 2> struct Bars {
+    using C = Cfg<D, HG, EB>;
     __host__ __device__ static constexpr int idxfull(int s) { return s; }
     __host__ __device__ static constexpr int kfull(int s) { return C::kNS + s; }
     __host__ __device__ static constexpr int vfull(int s) { return 2 * C::kNS + s; }
@@ -206,7 +213,7 @@ template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi
 template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) { return pack_bf16x2(lo, hi); }
 
 template <int D, typename T, bool kDiag, int HG>
-__global__ void __launch_bounds__(Cfg<D, HG>::kThreads, Cfg<D, HG>::kCtasPerSm)
+__global__ void __launch_bounds__(Cfg<D, HG, (int)sizeof(T)>::kThreads, Cfg<D, HG, (int)sizeof(T)>::kCtasPerSm)
 k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const int4* __restrict__ meta,
             const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
@@ -214,8 +221,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float* __restrict__ O, float scale_log2,
             uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt,
             float* __restrict__ scratch) {
-    using C = Cfg<D, HG>;
-    using B = Bars<D, HG>;
+    constexpr int EB = (int)sizeof(T);
+    using C = Cfg<D, HG, EB>;
+    using B = Bars<D, HG, EB>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sb = smem_u32(smem);
     if (sb & 1023) __trap();  // swizzled tiles need 1024-byte alignment
@@ -336,7 +344,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         sl.qslot = qs;
                         sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2) | (sp << 8);
                         reinterpret_cast<volatile int32_t*>(smem + C::oInfo)[seq % C::kNI] = sl.flags;
-                        sl.ralloc = rows > 0 ? (HG == 1 ? ((rows + 15) & ~15) : C::kMaxRows) : 0;
+                        sl.ralloc = rows > 0 ? (HG == 1 ? ((rows + C::kRowAlign - 1) & ~(C::kRowAlign - 1)) : C::kMaxRows) : 0;
                         const uint32_t fb = bar(B::idxfull(s));
                         if (rows > 0) {
                             const uint32_t r8 = (uint32_t)((rows + 7) & ~7);
@@ -398,8 +406,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     for (int g = 0; g < HG; ++g)
 #pragma unroll
                         for (int pp = 0; pp < C::P; ++pp)
-                            tma_load_2d(sb + C::oQ + qs * C::kQBytes + g * 16 * D * 2 + pp * 2048, &tmQ,
-                                        bar(B::qfull(qs)), (h + g) * D + 64 * pp, 16 * k);
+                            tma_load_2d(sb + C::oQ + qs * C::kQBytes + g * 16 * C::RB + pp * 2048, &tmQ,
+                                        bar(B::qfull(qs)), (h + g) * D + (128 / EB) * pp, 16 * k);
                 }
             }
             const uint32_t tile = (uint32_t)(sl.ralloc / 8) * C::kGroupBytes;
@@ -448,12 +456,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         // Lane l of a warp copies 16-byte piece (l % pieces) of one gathered row straight into the
         // 128B-swizzled UMMA layout; the rows of a chunk are dealt round-robin to the warps.
         // Each lane arrives on the chunk's K/V barriers when its own copies have landed.
-        constexpr int kPieces = D * 2 / 16;
+        constexpr int kPieces = C::RB / 16;
         constexpr int kRowsPerOp = 32 / kPieces;
         const int lw = warp - C::kLoader0;
         const int piece = lane % kPieces, rsub = lane / kPieces;
         const int pnl = piece >> 3, cc = piece & 7;
-        const int64_t ldb = (int64_t)H * D * 2;
+        const int64_t ldb = (int64_t)H * C::RB;
         int32_t seq = 0;
         for (;;) {
             const int s = seq % C::kNS;
@@ -469,8 +477,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const int h = sl.head;
             const uint32_t kt = sb + C::oRing + sl.ring_off + pnl * 1024;
             const uint32_t vt = sb + C::oRingV + sl.pad + pnl * 1024;
-            const uint8_t* kbase = Kg + (int64_t)h * D * 2 + piece * 16;
-            const uint8_t* vbase = Vg + (int64_t)h * D * 2 + piece * 16;
+            const uint8_t* kbase = Kg + (int64_t)h * C::RB + piece * 16;
+            const uint8_t* vbase = Vg + (int64_t)h * C::RB + piece * 16;
             // HG = 1: tile row r = compacted column r.  HG = 4: tile row 32g + r = column r of head h + g.
             const int ops = (expt & 8) ? 0 : (HG == 1 ? (rows + kRowsPerOp - 1) / kRowsPerOp : C::kMaxRows / kRowsPerOp);
 #pragma unroll 2
@@ -479,7 +487,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const int r = HG == 1 ? tr : (tr & 31);
                 if (r < rows) {
                     const int64_t j = sl.cols[r];
-                    const int64_t src = j * ldb + (HG == 1 ? 0 : (int64_t)(tr >> 5) * D * 2);
+                    const int64_t src = j * ldb + (HG == 1 ? 0 : (int64_t)(tr >> 5) * C::RB);
                     const uint32_t o = (uint32_t)(tr >> 3) * C::kGroupBytes + (uint32_t)(tr & 7) * 128 +
                                        (uint32_t)((cc ^ (tr & 7)) << 4);
                     cp_async_16(kt + o, kbase + src);
@@ -520,10 +528,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                     for (int g = 0; g < HG; ++g)
 #pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk)
-                            mma_f16_ss_warp(tmem + (b * HG + g) * 16, a0 + (((kk >> 2) * 1024 + (kk & 3) * 32) >> 4),
-                                            b0 + ((g * 16 * D * 2 + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4), idesc1,
-                                            kk > 0 ? 1u : 0u);
+                        for (int kk = 0; kk < C::RB / 32; ++kk) {  // K-steps of 32 bytes
+                            const uint64_t ad = a0 + (((kk >> 2) * 1024 + (kk & 3) * 32) >> 4);
+                            const uint64_t bd = b0 + ((g * 16 * C::RB + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4);
+                            if (EB == 1) mma_f8_ss_warp(tmem + (b * HG + g) * 16, ad, bd, idesc1, kk > 0 ? 1u : 0u);
+                            else mma_f16_ss_warp(tmem + (b * HG + g) * 16, ad, bd, idesc1, kk > 0 ? 1u : 0u);
+                        }
                 }
                 mma_commit_warp(bar(B::sfull(b)));
                 mma_commit_warp(bar(B::kempty(s)));
@@ -531,9 +541,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 if (lane == 0 && F3S_TRACE_EV0 != 3) stamp(n1, 2);
             }
         } else {
-            constexpr uint32_t idesc2 = idesc_f16(fmt, 1, 1, D, 16);    // O^T = V_c^T . P^T (A, B MN-major)
+            // O^T = V_c^T . P^T: A (V_c) MN-major; B (P^T) MN-major with a 32-byte swizzle for
+            // 16-bit P, K-major [16 x 128 bytes] with the 128-byte swizzle for fp8 P (8-bit
+            // MN-major B would need 16-byte rows)
+            constexpr uint32_t idesc2 = idesc_f16(fmt, 1, EB == 2 ? 1 : 0, D, 16);
             const uint64_t dV = smem_desc_sw128(0, 1024, C::kGroupBytes);
-            const uint64_t dP = smem_desc_sw32(0, 4096, 256);
+            const uint64_t dP = EB == 2 ? smem_desc_sw32(0, 4096, 256) : smem_desc_sw128(0, 16, 1024);
             for (int32_t n2 = 0;; ++n2) {
                 const int s = n2 % C::kNS, b = n2 % C::kSB;
                 mbar_wait(bar(B::kfull(s)), (n2 / C::kNS) & 1);  // slot of chunk n2 filled
@@ -547,13 +560,19 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 if (rows > 0 && !(expt & 2)) {
                     const uint64_t a0 = dV + ((sb + C::oRingV + slots[s].pad) >> 4);
                     const uint64_t b0 = dP + ((sb + C::oP + b * C::kPBytes) >> 4);
-                    const int nsteps = (rows + 15) >> 4;
+                    const int nsteps = (rows + C::kRowAlign - 1) / C::kRowAlign;
+                    if (EB == 1) {
+                        for (int st = 0; st < nsteps; ++st)  // 32 chunk rows = 4 row groups, 32 bytes of a P row
+                            mma_f8_ss_warp(tmem + 16 * C::kSB + b * 16, a0 + ((st * 4 * C::kGroupBytes) >> 4),
+                                           b0 + ((st * 32) >> 4), idesc2, st > 0 ? 1u : 0u);
+                    } else {
 #pragma unroll
-                    for (int g = 0; g < HG; ++g)  // head g: tile rows / P^T columns 32g .. (HG > 1)
-                        for (int st = 0; st < nsteps; ++st)
-                            mma_f16_ss_warp(tmem + 16 * C::kSB * HG + (b * HG + g) * 16,
-                                            a0 + ((g * 4 * C::kGroupBytes + st * 2 * C::kGroupBytes) >> 4),
-                                            b0 + ((g * 1024 + st * 512) >> 4), idesc2, st > 0 ? 1u : 0u);
+                        for (int g = 0; g < HG; ++g)  // head g: tile rows / P^T columns 32g .. (HG > 1)
+                            for (int st = 0; st < nsteps; ++st)
+                                mma_f16_ss_warp(tmem + 16 * C::kSB * HG + (b * HG + g) * 16,
+                                                a0 + ((g * 4 * C::kGroupBytes + st * 2 * C::kGroupBytes) >> 4),
+                                                b0 + ((g * 1024 + st * 512) >> 4), idesc2, st > 0 ? 1u : 0u);
+                    }
                 }
                 mma_commit_warp(bar(B::ofull(b)));
                 mma_commit_warp(bar(B::empty(s)));
@@ -642,6 +661,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             // owns one 32-byte row (its 16 query rows), 8 rows per 256-byte atom, the two 16-byte
             // halves swapped when bit 2 of p is set.
             uint4* prow = reinterpret_cast<uint4*>(smem + C::oP + b * C::kPBytes + (p >> 3) * 256 + (p & 7) * 32);
+            // fp8 P: E scaled by 2^8 (exponent offset) so that [0, 1] lands in e4m3's normal range
+            // [2^-6, 448] down to 2^-14; l_o sums the same scaled values, so O / l is unchanged
+            auto pexp = [](float v) { return EB == 1 ? ex2(v + 8.f) : ex2(v); };
             const int sw = (p >> 2) & 1;
             float av[16], pv[16];
             float cm[16];  // chunk row max
@@ -669,7 +691,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     m[i] = fmaxf(kMFloor, cm[i]);
-                    pv[i] = (expt & 1) ? x[i] : ex2(x[i] - m[i]);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
+                    pv[i] = (expt & 1) ? x[i] : pexp(x[i] - m[i]);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
                     l[i] = pv[i];
                     av[i] = 0.f;
                 }
@@ -679,12 +701,20 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     const float mn = fmaxf(m[i], cm[i]);
                     av[i] = (expt & 1) ? 1.f : ex2(m[i] - mn);  // e^{m_o - m_i} (l.18, l.21)
                     m[i] = mn;
-                    pv[i] = (expt & 1) ? x[i] : ex2(x[i] - mn);
+                    pv[i] = (expt & 1) ? x[i] : pexp(x[i] - mn);
                     l[i] = fmaf(l[i], av[i], pv[i]);  // l_o (l.18)
                 }
             }
             if (p == 0) lap(6);
-            {  // E cast to the input dtype into SMEM (l.19): two 16-byte stores
+            if constexpr (EB == 1) {
+                // E cast to e4m3 (satfinite, round to nearest even) into the K-major 128B-swizzled
+                // [16 x 128] B tile: byte p of row i, 16-byte chunk (p >> 4) ^ (i & 7)
+                uint8_t* pt = smem + C::oP + b * C::kPBytes + (p & 15);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    pt[(i >> 3) * 1024 + (i & 7) * 128 + ((((p >> 4) ^ (i & 7)) & 7) << 4)] =
+                        (uint8_t)__nv_cvt_float_to_fp8(pv[i], __NV_SATFINITE, __NV_E4M3);
+            } else {  // E cast to the input dtype into SMEM (l.19): two 16-byte stores
                 const uint4 lo = make_uint4(pack2<T>(pv[0], pv[1]), pack2<T>(pv[2], pv[3]), pack2<T>(pv[4], pv[5]),
                                             pack2<T>(pv[6], pv[7]));
                 const uint4 hi = make_uint4(pack2<T>(pv[8], pv[9]), pack2<T>(pv[10], pv[11]), pack2<T>(pv[12], pv[13]),
@@ -1007,7 +1037,7 @@ f3s_status make_map_uncached(CUtensorMap* map, const void* base, CUtensorMapData
                              int64_t rows, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz) {
     EncodeTiledFn enc = get_encode();
     if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return F3S_ERR_CUDA; }
-    const int esz = type == CU_TENSOR_MAP_DATA_TYPE_FLOAT32 ? 4 : 2;
+    const int esz = type == CU_TENSOR_MAP_DATA_TYPE_FLOAT32 ? 4 : type == CU_TENSOR_MAP_DATA_TYPE_UINT8 ? 1 : 2;
     cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)inner * esz};
     cuuint32_t box[2] = {box_inner, box_rows};
@@ -1021,6 +1051,8 @@ f3s_status make_map_uncached(CUtensorMap* map, const void* base, CUtensorMapData
     return F3S_OK;
 }
 f3s_status make_map(CUtensorMap* map, const void* base, f3s_dtype dtype, int64_t inner, int64_t rows, uint32_t box_rows) {
+    if (dtype == F3S_E4M3)  // 8-bit elements: 128-element (128-byte) boxes
+        return make_map(map, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, inner, rows, 128, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
     return make_map(map, base, dtype == F3S_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                     inner, rows, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
@@ -1029,7 +1061,7 @@ std::atomic<uint32_t> g_call{0};
 
 template <int D, typename T, int HG>
 f3s_status launch(const AttnArgs& a) {
-    using C = Cfg<D, HG>;
+    using C = Cfg<D, HG, (int)sizeof(T)>;
     const Plan& p = *a.plan;
     const int64_t out_bytes = (int64_t)p.n_rows * a.heads * D * 4;
     if (p.nnz == 0 || p.n_cols == 0) {  // every row is empty: O = 0 (reading c4)
@@ -1106,6 +1138,10 @@ f3s_status launch_attention_sm100(const AttnArgs& a) {
     // pipeline cost is shared by 4 heads (batched small graphs).  F3S_HG1=1 forces HG = 1.
     static const bool hg1 = getenv("F3S_HG1") != nullptr;
     const Plan& p = *a.plan;
+    if (a.dtype == F3S_E4M3) {  // d = 128 (checked by the API)
+        if (a.d != 128) { set_error("e4m3 needs d = 128"); return F3S_ERR_UNSUPPORTED; }
+        return launch<128, __nv_fp8_e4m3, 1>(a);
+    }
     const bool hg4 = !hg1 && !a.one_head && a.d == 64 && a.heads % 4 == 0 && p.max_width <= 32 && p.n_groups == 0;
     if (a.dtype == F3S_FP16) {
         if (hg4) return launch<64, __half, 4>(a);

@@ -28,7 +28,11 @@ static f3s_status check_attention_args(f3s_plan_t plan, const void* Q, const voi
     if (!plan) { set_error("plan is NULL"); return F3S_ERR_INVALID_VALUE; }
     if (heads < 1) { set_error("heads must be >= 1"); return F3S_ERR_INVALID_VALUE; }
     if (!std::isfinite(scale)) { set_error("scale must be finite"); return F3S_ERR_INVALID_VALUE; }
-    if (dtype != F3S_FP16 && dtype != F3S_BF16) { set_error("dtype must be F3S_FP16 or F3S_BF16"); return F3S_ERR_INVALID_VALUE; }
+    if (dtype != F3S_FP16 && dtype != F3S_BF16 && dtype != F3S_E4M3) {
+        set_error("dtype must be F3S_FP16, F3S_BF16 or F3S_E4M3");
+        return F3S_ERR_INVALID_VALUE;
+    }
+    if (dtype == F3S_E4M3 && d != 128) { set_error("F3S_E4M3 needs d = 128"); return F3S_ERR_UNSUPPORTED; }
     const Plan& p = *reinterpret_cast<const Plan*>(plan);
     if (p.n_rows > 0 && (!Q || !O)) { set_error("Q/O is NULL"); return F3S_ERR_INVALID_VALUE; }
     if (p.n_cols > 0 && (!K || !V)) { set_error("K/V is NULL"); return F3S_ERR_INVALID_VALUE; }
@@ -56,6 +60,10 @@ static f3s_status run_attention(f3s_plan_t plan, const void* Q, const void* K, c
     a.grid_override = grid;
     a.one_head = variant == F3S_VARIANT_ONE_HEAD;
     if (a.plan->n_rows == 0) return F3S_OK;
+    if (dtype == F3S_E4M3 && (variant == F3S_VARIANT_SIMT || variant == F3S_VARIANT_ONE_HEAD)) {
+        set_error("F3S_E4M3: DEFAULT and NO_REORDER variants only");
+        return F3S_ERR_UNSUPPORTED;
+    }
     switch (variant) {
         case F3S_VARIANT_DEFAULT:
         case F3S_VARIANT_NO_REORDER:
@@ -180,6 +188,7 @@ f3s_status f3s_attention_backward(f3s_plan_t plan, const void* Q, const void* K,
     try {
         f3s_status st = check_attention_args(plan, Q, K, V, dQ, scale, heads, d, dtype, true);
         if (st != F3S_OK) return st;
+        if (dtype == F3S_E4M3) { set_error("backward: F3S_FP16 or F3S_BF16 only"); return F3S_ERR_UNSUPPORTED; }
         Plan& p = *reinterpret_cast<Plan*>(plan);
         if (p.n_rows > 0 && !dO) { set_error("dO is NULL"); return F3S_ERR_INVALID_VALUE; }
         if (p.n_cols > 0 && (!dK || !dV)) { set_error("dK/dV is NULL"); return F3S_ERR_INVALID_VALUE; }
@@ -220,9 +229,12 @@ f3s_status f3s_attention_host_async(f3s_plan_t plan, const void* Q, const void* 
     f3s_status st = check_attention_args(plan, Q, K, V, O, scale, heads, d, dtype, false);
     if (st != F3S_OK) return st;
     Plan& p = *reinterpret_cast<Plan*>(plan);
-    const size_t qn = (size_t)p.n_rows * heads * d, kn = (size_t)p.n_cols * heads * d;
+    size_t qn = (size_t)p.n_rows * heads * d, kn = (size_t)p.n_cols * heads * d;
     auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
-    const size_t need = up(qn * 2) + 2 * up(kn * 2) + up(qn * 4);
+    const size_t es = dtype == F3S_E4M3 ? 1 : 2;  // bytes per input element
+    qn *= es;  // input sizes in bytes from here on; the output is fp32
+    kn *= es;
+    const size_t need = up(qn) + 2 * up(kn) + up(qn / es * 4);
     char* base = nullptr;
     {
         std::lock_guard<std::mutex> lock(p.staging_mu);
@@ -246,17 +258,17 @@ f3s_status f3s_attention_host_async(f3s_plan_t plan, const void* Q, const void* 
         base = static_cast<char*>(sg->ptr);
     }
     void* dQ = base;
-    void* dK = base + up(qn * 2);
-    void* dV = base + up(qn * 2) + up(kn * 2);
-    float* dO = reinterpret_cast<float*>(base + up(qn * 2) + 2 * up(kn * 2));
-    if (qn) F3S_CUDA_TRY(cudaMemcpyAsync(dQ, Q, qn * 2, cudaMemcpyHostToDevice, stream));
+    void* dK = base + up(qn);
+    void* dV = base + up(qn) + up(kn);
+    float* dO = reinterpret_cast<float*>(base + up(qn) + 2 * up(kn));
+    if (qn) F3S_CUDA_TRY(cudaMemcpyAsync(dQ, Q, qn, cudaMemcpyHostToDevice, stream));
     if (kn) {
-        F3S_CUDA_TRY(cudaMemcpyAsync(dK, K, kn * 2, cudaMemcpyHostToDevice, stream));
-        F3S_CUDA_TRY(cudaMemcpyAsync(dV, V, kn * 2, cudaMemcpyHostToDevice, stream));
+        F3S_CUDA_TRY(cudaMemcpyAsync(dK, K, kn, cudaMemcpyHostToDevice, stream));
+        F3S_CUDA_TRY(cudaMemcpyAsync(dV, V, kn, cudaMemcpyHostToDevice, stream));
     }
     st = run_attention(plan, dQ, dK, dV, dO, scale, heads, d, dtype, F3S_VARIANT_DEFAULT, stream);
     if (st != F3S_OK) return st;
-    if (qn) F3S_CUDA_TRY(cudaMemcpyAsync(O, dO, qn * 4, cudaMemcpyDeviceToHost, stream));
+    if (qn) F3S_CUDA_TRY(cudaMemcpyAsync(O, dO, qn / es * 4, cudaMemcpyDeviceToHost, stream));
     return F3S_OK;
 }
 

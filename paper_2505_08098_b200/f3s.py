@@ -22,7 +22,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 OK, INVALID_VALUE, INVALID_CSR, UNSUPPORTED, OUT_OF_MEMORY, CUDA, INTERNAL = range(7)
-FP16, BF16 = 0, 1
+FP16, BF16, E4M3 = 0, 1, 2  # f3s_dtype
 VARIANT_DEFAULT, VARIANT_NO_REORDER, VARIANT_SIMT, VARIANT_ONE_HEAD = 0, 1, 2, 3
 VARIANTS = {"default": VARIANT_DEFAULT, "no_reorder": VARIANT_NO_REORDER, "simt": VARIANT_SIMT,
             "one_head": VARIANT_ONE_HEAD}
@@ -93,7 +93,9 @@ def _dtype_code(t) -> int:
         return FP16
     if t.dtype == torch.bfloat16:
         return BF16
-    raise TypeError(f"Q/K/V must be float16 or bfloat16, got {t.dtype}")
+    if t.dtype == torch.float8_e4m3fn:
+        return E4M3
+    raise TypeError(f"Q/K/V must be float16, bfloat16 or float8_e4m3fn, got {t.dtype}")
 
 
 class Plan:
