@@ -374,7 +374,7 @@ def main():
         ta = torch.tensor([achieved], device=dev, dtype=torch.float64)
         dist.all_reduce(ta, op=dist.ReduceOp.MIN)
         achieved = ta.item()
-    traffic = load_traffic(args.config) if world == 1 else None
+    traffic = load_traffic(args.config + ("_e4m3" if eb == 1 else "")) if world == 1 else None
 
     # ---- end to end through the C ABI with host buffers (pinned), N = 1 ----
     e2e = None

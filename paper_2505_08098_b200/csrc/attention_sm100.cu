@@ -69,16 +69,30 @@ struct Cfg {
 #define F3S_KNQ128 4
 #endif
     static constexpr int kRingK = HG == 4 ? 48 * 1024 : 64 * 1024;
-    static constexpr int kRingV = HG == 4 ? 64 * 1024 : D == 128 ? F3S_RINGV128_KB * 1024 : 88 * 1024;
+#ifndef F3S_RINGV8_KB
+#define F3S_RINGV8_KB 88
+#endif
+    static constexpr int kRingV = HG == 4 ? 64 * 1024 : EB == 1 ? F3S_RINGV8_KB * 1024 : D == 128 ? F3S_RINGV128_KB * 1024 : 88 * 1024;
     static constexpr int kRingBytes = kRingK + kRingV;
     static constexpr int kNS = D == 128 ? 20 : 22;   // chunk slots (ids, masks, descriptor, barriers)
-    static constexpr int kNQ = HG == 4 ? 6 : D == 128 ? F3S_KNQ128 : 12;  // Q tile slots (items in flight per CTA)
+#ifndef F3S_KNQ8
+#define F3S_KNQ8 8
+#endif
+    // Q tile slots (items in flight per CTA); fp8 tiles are half as large and carry half the bytes
+    // per chunk, so more items are kept in flight
+    static constexpr int kNQ = HG == 4 ? 6 : EB == 1 ? F3S_KNQ8 : D == 128 ? F3S_KNQ128 : 12;
     static constexpr int kQBytes = 16 * RB * HG;     // HG head tiles of 16 x D
-    static constexpr int kPBytes = 16 * kMaxRows * 2;
-    static constexpr int kSB = 4;                    // S/P/O buffers in flight (TMEM and SMEM)
-    static constexpr int kNO = HG == 4 ? 1 : 2;      // O staging tiles (16 x HG*D fp32) for the TMA store
+    static constexpr int kPBytes = 16 * kMaxRows * EB;
+#ifndef F3S_KSB8
+#define F3S_KSB8 4
+#endif
+    static constexpr int kSB = EB == 1 ? F3S_KSB8 : 4;  // S/P/O buffers in flight (TMEM and SMEM)
+#ifndef F3S_KNO8
+#define F3S_KNO8 2
+#endif
+    static constexpr int kNO = HG == 4 ? 1 : EB == 1 ? F3S_KNO8 : 2;  // O staging tiles (16 x HG*D fp32) for the TMA store
     static constexpr int kOBytes = 16 * D * 4 * HG;
-    static constexpr int kTmemCols = HG == 4 ? 512 : 128;  // S^T and O^T: kSB x HG buffers of 16 columns each
+    static constexpr int kTmemCols = HG == 4 ? 512 : kSB <= 4 ? 128 : 256;  // S^T and O^T: kSB x HG buffers of 16 columns each
     static_assert(2 * 16 * kSB * HG <= kTmemCols, "TMEM columns");
     static constexpr int kSlotBytes = 32 + 128 * 4 + 128 * 2;  // sizeof(Slot)
     static constexpr int oRing = 0;                  // K ring, then V ring

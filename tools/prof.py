@@ -14,6 +14,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="arxiv")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--dtype", default="fp16", choices=["fp16", "e4m3"])
     a = ap.parse_args()
     import torch
     from f3s_inputs import configs
@@ -22,6 +23,8 @@ def main():
     csr = w.graph()
     Qb, Kb, Vb = w.qkv(csr)
     dev = lambda b: torch.from_numpy(b.view(np.int16)).cuda().view(torch.float16)
+    if a.dtype == "e4m3":
+        dev = lambda b: torch.from_numpy(b.view(np.float16).astype(np.float32)).to(torch.float8_e4m3fn).cuda()
     p = f3s.plan(torch.from_numpy(csr.row_ptr).cuda(), torch.from_numpy(csr.col_idx).cuda(), csr.n_rows)
     Q, K, V = dev(Qb), dev(Kb), dev(Vb)
     O = torch.empty(Q.shape, dtype=torch.float32, device="cuda")

@@ -1,10 +1,11 @@
 #!/bin/bash
 # bench several experiment builds (libf3s_<v>.so) back to back: VARIANTS="a b" CONFIGS="arxiv batched"
+# [BENCH_ARGS="--dtype e4m3"]
 mkdir -p gpurun_out
 for v in ${VARIANTS}; do
   for c in ${CONFIGS:-arxiv batched}; do
     if [ "$v" = base ]; then unset F3S_LIB_VARIANT; else export F3S_LIB_VARIANT=$v; fi
-    timeout -s KILL 300 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/var_${v}_$c.json 2> gpurun_out/var_${v}_$c.err
+    timeout -s KILL 300 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline --no-e2e ${BENCH_ARGS} > gpurun_out/var_${v}_$c.json 2> gpurun_out/var_${v}_$c.err
     python -c "
 import json
 try:
