@@ -38,7 +38,19 @@ def test_sass_is_blackwell_native(f3s):
     assert "UBLKCP" in out           # cp.async.bulk (column ids / masks into chunk slots)
     assert "LDGSTS" in out           # cp.async gathers of K/V rows
     assert "LDTM" in out             # tcgen05.ld (S^T and O^T out of TMEM)
+    assert "UTCQMMA" in out          # tcgen05.mma kind::f8f6f4 (E4M3 inputs, f4)
     assert re.search(r"\s HMMA", out) is None  # no legacy mma.sync path (UTCHMMA is tcgen05)
+
+
+def test_dtype_codes_match_the_header(f3s):
+    import torch
+    header = open(os.path.join(ROOT, "include", "f3s.h")).read()
+    enum = dict((k, int(v)) for k, v in re.findall(r"(F3S_(?:FP16|BF16|E4M3)) = (\d+)", header))
+    assert enum == {"F3S_FP16": f3s.FP16, "F3S_BF16": f3s.BF16, "F3S_E4M3": f3s.E4M3}
+    for dt, code in ((torch.float16, f3s.FP16), (torch.bfloat16, f3s.BF16), (torch.float8_e4m3fn, f3s.E4M3)):
+        assert f3s._dtype_code(torch.zeros(1, dtype=dt)) == code
+    with pytest.raises(TypeError):
+        f3s._dtype_code(torch.zeros(1, dtype=torch.float32))
 
 
 def test_status_strings(f3s):
