@@ -114,3 +114,17 @@ def test_fp8_rejected_where_unsupported(f3s):
         f3s.attention(p, x, x, x, scale=1.0, variant="simt")
     with pytest.raises(f3s.F3SError):
         f3s.attention_backward(p, x, x, x, torch.zeros((64, 1, 128), device="cuda"), scale=1.0)
+
+
+@pytest.mark.parametrize("variant", ["default", "no_reorder"])
+def test_fp8_eight_heads_variants(f3s, oracle_mod, variant):
+    # the bench's head count (8 x 128) on an arxiv-like degree mix, both work orders
+    import torch
+    csr = fi.chung_lu(3000, 20000, directed=True, gamma=2.3, max_deg=400, seed=85)
+    (Q, Qd), (K, Kd), (V, Vd) = (_e4m3((3000, 8, 128), (9 << 8) | t) for t in (1, 2, 3))
+    rp, ci = csr_to_dev(csr)
+    p = f3s.plan(rp, ci, 3000)
+    O = f3s.attention(p, Q, K, V, scale=1.0 / np.sqrt(128), variant=variant)
+    torch.cuda.synchronize()
+    ref = oracle_mod.attention_f64(csr.row_ptr, csr.col_idx, Qd, Kd, Vd, scale=1.0 / np.sqrt(128))
+    _check_bound(csr, O.cpu().numpy(), Vd, ref)

@@ -12,6 +12,7 @@ for c in cora batched products reddit; do
 done
 timeout -s KILL 600 python bench.py --variant simt --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${T}_bench_arxiv_simt.json 2>&1
 timeout -s KILL 600 python bench.py --variant no_reorder --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${T}_bench_arxiv_noreorder.json 2>&1
+timeout -s KILL 600 python bench.py --dtype e4m3 > gpurun_out/${T}_bench_arxiv_e4m3.json 2>&1
 timeout -s KILL 600 python bench.py --config batched --variant one_head --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${T}_bench_batched_onehead.json 2>&1
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${T}_launches_arxiv.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_f3s_sm100 -s 3 -c 1 -o gpurun_out/${T}_prof_arxiv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
