@@ -49,7 +49,7 @@ typedef enum {
 } f3s_status;
 
 /* Element type of Q, K, V.  F3S_E4M3 (OCP FP8 E4M3, torch.float8_e4m3fn; SURVEY 8(f) f4 "FP8 K/V
- * gathers", FP8 being the paper's future work): d = 128 only, f3s_attention /
+ * gathers", FP8 being the paper's future work): d in {64, 128}, f3s_attention /
  * f3s_attention_host(_async) / the DEFAULT and NO_REORDER variants only.  S is exact on the
  * given fp8 values (fp32 accumulate); P is rounded to e4m3 for the SpMM (l.19), so |O - O_exact|
  * <= 2^-4 * max |V_j| over the row's neighbours (plus fp32 rounding), reading c24. */
@@ -141,7 +141,7 @@ f3s_status f3s_plan_export(f3s_plan_t plan, int32_t* rw_ptr, int32_t* cols, uint
  *  K, V   device [n_cols, heads, d] dtype, contiguous, 16-byte aligned
  *  O      device [n_rows, heads, d] float32, contiguous; must not alias Q/K/V
  *  scale  multiplies Q K^T before the softmax (scale = 1 reproduces Eq.1; 1/sqrt(d) for GT)
- *  heads  >= 1;  d in {64, 128};  dtype F3S_FP16 or F3S_BF16, or F3S_E4M3 with d = 128
+ *  heads  >= 1;  d in {64, 128};  dtype F3S_FP16, F3S_BF16 or F3S_E4M3
  * Asynchronous on `stream`; only launch-time errors are reported (device faults surface at
  * the caller's next synchronisation, CUDA convention).  Bitwise deterministic.
  */

@@ -52,9 +52,12 @@ using namespace sm100;
 template <int D, int HG = 1, int EB = 2>
 struct Cfg {
     static_assert(HG == 1 || (HG == 4 && D == 64 && EB == 2), "head groups: d = 64 only");
-    static_assert(EB == 2 || (EB == 1 && D == 128 && HG == 1), "fp8: d = 128 only");
+    static_assert(EB == 2 || (EB == 1 && HG == 1), "fp8: one head per chunk");
     static constexpr int RB = D * EB;                // bytes of one gathered row of one head
-    static constexpr int P = RB / 128;               // 128-byte panels per gathered row of one head
+    // 128-byte panels per gathered row of one head (fp8, d = 64: a 64-byte row in the first half of
+    // one panel; the MMAs read only its K-steps)
+    static constexpr int P = RB >= 128 ? RB / 128 : 1;
+    static constexpr int kRowPitch = 128 * P;        // bytes between tile rows of one 8-row group panel set
     // MMA2 K-step (chunk rows per instruction): 16 for kind::f16, 32 for kind::f8f6f4; ring tiles
     // are allocated in whole K-steps
     static constexpr int kRowAlign = 32 / EB;
@@ -81,7 +84,7 @@ struct Cfg {
     // Q tile slots (items in flight per CTA); fp8 tiles are half as large and carry half the bytes
     // per chunk, so more items are kept in flight
     static constexpr int kNQ = HG == 4 ? 6 : EB == 1 ? F3S_KNQ8 : D == 128 ? F3S_KNQ128 : 12;
-    static constexpr int kQBytes = 16 * RB * HG;     // HG head tiles of 16 x D
+    static constexpr int kQBytes = 16 * kRowPitch * HG;  // HG head tiles of 16 x D
     static constexpr int kPBytes = 16 * kMaxRows * EB;
 #ifndef F3S_KSB8
 #define F3S_KSB8 4
@@ -420,7 +423,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     for (int g = 0; g < HG; ++g)
 #pragma unroll
                         for (int pp = 0; pp < C::P; ++pp)
-                            tma_load_2d(sb + C::oQ + qs * C::kQBytes + g * 16 * C::RB + pp * 2048, &tmQ,
+                            tma_load_2d(sb + C::oQ + qs * C::kQBytes + g * 16 * C::kRowPitch + pp * 2048, &tmQ,
                                         bar(B::qfull(qs)), (h + g) * D + (128 / EB) * pp, 16 * k);
                 }
             }
@@ -544,7 +547,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                         for (int kk = 0; kk < C::RB / 32; ++kk) {  // K-steps of 32 bytes
                             const uint64_t ad = a0 + (((kk >> 2) * 1024 + (kk & 3) * 32) >> 4);
-                            const uint64_t bd = b0 + ((g * 16 * C::RB + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4);
+                            const uint64_t bd = b0 + ((g * 16 * C::kRowPitch + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4);
                             if (EB == 1) mma_f8_ss_warp(tmem + (b * HG + g) * 16, ad, bd, idesc1, kk > 0 ? 1u : 0u);
                             else mma_f16_ss_warp(tmem + (b * HG + g) * 16, ad, bd, idesc1, kk > 0 ? 1u : 0u);
                         }
@@ -1152,9 +1155,10 @@ f3s_status launch_attention_sm100(const AttnArgs& a) {
     // pipeline cost is shared by 4 heads (batched small graphs).  F3S_HG1=1 forces HG = 1.
     static const bool hg1 = getenv("F3S_HG1") != nullptr;
     const Plan& p = *a.plan;
-    if (a.dtype == F3S_E4M3) {  // d = 128 (checked by the API)
-        if (a.d != 128) { set_error("e4m3 needs d = 128"); return F3S_ERR_UNSUPPORTED; }
-        return launch<128, __nv_fp8_e4m3, 1>(a);
+    if (a.dtype == F3S_E4M3) {
+        // d = 64: the Q box (128 elements) also covers the next head's 64 (zero-filled past the
+        // last head by the tensor map); MMA1 reads only the first 64 bytes of each row
+        return a.d == 128 ? launch<128, __nv_fp8_e4m3, 1>(a) : launch<64, __nv_fp8_e4m3, 1>(a);
     }
     const bool hg4 = !hg1 && !a.one_head && a.d == 64 && a.heads % 4 == 0 && p.max_width <= 32 && p.n_groups == 0;
     if (a.dtype == F3S_FP16) {

@@ -32,7 +32,6 @@ static f3s_status check_attention_args(f3s_plan_t plan, const void* Q, const voi
         set_error("dtype must be F3S_FP16, F3S_BF16 or F3S_E4M3");
         return F3S_ERR_INVALID_VALUE;
     }
-    if (dtype == F3S_E4M3 && d != 128) { set_error("F3S_E4M3 needs d = 128"); return F3S_ERR_UNSUPPORTED; }
     const Plan& p = *reinterpret_cast<const Plan*>(plan);
     if (p.n_rows > 0 && (!Q || !O)) { set_error("Q/O is NULL"); return F3S_ERR_INVALID_VALUE; }
     if (p.n_cols > 0 && (!K || !V)) { set_error("K/V is NULL"); return F3S_ERR_INVALID_VALUE; }
