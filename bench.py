@@ -5,8 +5,14 @@ A step is one fused 3S call (f3s_attention: the whole hot path of SURVEY §8(a) 
 workload's graph) with inputs resident in HBM; at N>1 it is the K/V all-gather plus the local
 fused call on every rank (rows sharded by nnz).  Prints ONE JSON line on rank 0.
 
-  python bench.py [--gpus N --steps K --warmup W] [--config arxiv|cora|products|reddit|batched]
+  python bench.py [--gpus N --steps K --warmup W] [--config products|arxiv|cora|reddit|batched]
   python bench.py --impl reference ...   # the fp64 CPU oracle as the reference arm
+  python bench.py --gpus 2 --dry-run     # multi-rank orchestration on CPU (gloo), no kernel
+
+With --gpus N > 1 and no torchrun environment, bench.py launches its own N ranks through
+torch.distributed.run (127.0.0.1) and relays rank 0's line.  Every timed step is preceded by an
+untimed L2 flush (a 256 MB write > 126 MB L2) unless --warm-l2; the warm back-to-back kernel time
+is reported beside it.
 
 metric: useful edge-GFLOP/s = 4 * nnz * d * heads / time (north_star), whole job.
 """
@@ -37,13 +43,22 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="arxiv")
+    ap.add_argument("--config", default="products",
+                    help="BASELINE.json workload; products (the largest) is the headline")
     ap.add_argument("--variant", default="default", choices=["default", "no_reorder", "simt", "one_head"])
     ap.add_argument("--dtype", default=None, choices=[None, "fp16", "bf16", "e4m3"],
                     help="e4m3: the workload's values rounded to FP8 E4M3 (SURVEY 8(f) f4; N = 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle work for cpu_baseline")
+    ap.add_argument("--warm-l2", action="store_true", help="no L2 flush between timed steps")
+    ap.add_argument("--graph-batch", type=int, default=None,
+                    help="also time N calls captured in one CUDA graph (default 100 for cora, else 0)")
+    ap.add_argument("--kv-interleaved", action="store_true",
+                    help="N = 1: K and V in one [n, 2, H, d] buffer (the layout of the multi-GPU all-gather)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU/gloo run of the multi-rank orchestration (partition, [K||V] all-gather, timing "
+                         "reduction, JSON line) without the CUDA kernel; value is null")
     return ap.parse_args()
 
 
@@ -235,13 +250,86 @@ def reference_arm(args, rank: int):
 
 
 # ---------------------------------------------------------------------------------------------
+def respawn(args) -> int:
+    """--gpus N > 1 outside torchrun: launch N ranks of this script (127.0.0.1) and relay rank 0."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def percentiles(ms: list) -> dict:
+    a = np.asarray(ms, np.float64)
+    return {"p10": round(float(np.percentile(a, 10)), 4), "p50": round(float(np.percentile(a, 50)), 4),
+            "p90": round(float(np.percentile(a, 90)), 4)}
+
+
+def dry_run(args, rank: int, world: int):
+    """Multi-rank orchestration on CPU with gloo: the nnz partition, the [K||V] shard layout and its
+    all-gather (checked bitwise against the global K/V), the max-over-ranks timing reduction and
+    the JSON line.  No attention is computed (there is no CPU path): value is null."""
+    import torch
+    import torch.distributed as dist
+
+    from f3s_inputs import configs
+    from paper_2505_08098_b200 import dist as f3sdist
+    dist.init_process_group("gloo")
+    w = configs.get(args.config)
+    csr = w.graph()
+    Qb, Kb, Vb = w.qkv(csr)
+    spec = f3sdist.shard_spec(csr.row_ptr, csr.col_idx, rank, world,
+                              graph_ptr=csr.graph_ptr if w.name == "batched" else None)
+    checks = {"rows_cover": None, "kv_allgather_bitwise": None}
+    b = torch.tensor([spec.row_begin, spec.row_end], dtype=torch.int64)
+    allb = [torch.zeros_like(b) for _ in range(world)]
+    dist.all_gather(allb, b)
+    bounds = [tuple(x.tolist()) for x in allb]
+    checks["rows_cover"] = bool(bounds[0][0] == 0 and bounds[-1][1] == csr.n_rows and
+                                all(bounds[i][1] == bounds[i + 1][0] for i in range(world - 1)))
+    if not spec.batched:
+        KVs = f3sdist.kv_shard(spec, Kb, Vb, csr.n_cols)
+        KVs = torch.from_numpy(KVs.view(np.float16))  # gloo moves fp16 (bit patterns are copied as is)
+        KVf = torch.empty((world * spec.kv_rows,) + tuple(KVs.shape[1:]), dtype=KVs.dtype)
+        ms = []
+        for _ in range(args.warmup + args.steps):
+            dist.barrier()
+            t0 = time.perf_counter()
+            f3sdist.allgather_kv_into(KVf, KVs)
+            ms.append((time.perf_counter() - t0) * 1e3)
+        ms = ms[args.warmup:]
+        got = KVf.numpy().view(np.uint16)[:csr.n_cols]
+        checks["kv_allgather_bitwise"] = bool(np.array_equal(got[:, 0], Kb) and np.array_equal(got[:, 1], Vb))
+    else:
+        ms = [0.0]
+        checks["kv_allgather_bitwise"] = "batched: no collective"
+    t = torch.tensor([float(np.mean(ms))], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ok = torch.tensor([1 if all(v is True or isinstance(v, str) for v in checks.values()) else 0])
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "dry_run": True, "backend": "gloo (CPU)",
+                          "allgather_ms_max_over_ranks": round(t.item(), 3), "checks": checks,
+                          "all_ranks_ok": bool(ok.item()), "bounds": bounds,
+                          "config": {"workload": w.description, "n": csr.n_rows, "nnz": int(csr.nnz)}}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        sys.exit(respawn(args))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         reference_arm(args, rank)
+        return
+    if args.dry_run:
+        dry_run(args, rank, world)
         return
 
     import torch
@@ -275,20 +363,26 @@ def main():
     if dtype == "e4m3":
         assert world == 1, "e4m3 bench: N = 1"
         (Qb, Kb, Vb), (Qo, Ko, Vo) = e4m3_inputs(Qb, Kb, Vb)
+    es = eb
 
     def dev_tensor(bits):
         return torch.from_numpy(np.ascontiguousarray(bits)).view(ht).to(dev).view(tdt)
 
     # ---- plan (one-time preprocessing; timed separately) ----
+    KV_sh = KV = None
+    kv_ld = 0
     if world == 1:
         rp = torch.from_numpy(csr.row_ptr).to(dev)
         ci = torch.from_numpy(csr.col_idx).to(dev)
         plan = f3s.plan(rp, ci, csr.n_rows)
-        row_b, row_e, n_cols_loc = 0, csr.n_rows, csr.n_cols
+        row_b, row_e = 0, csr.n_rows
         Q = dev_tensor(Qb)
-        K = dev_tensor(Kb)
-        V = dev_tensor(Vb)
-        K_sh = V_sh = None
+        if args.kv_interleaved:
+            KV = dev_tensor(np.stack([Kb, Vb], axis=1))
+            kv_ld = 2 * H * d
+        else:
+            K = dev_tensor(Kb)
+            V = dev_tensor(Vb)
     else:
         shard = f3sdist.make_shard(csr.row_ptr, csr.col_idx, rank, world, device=dev,
                                    graph_ptr=csr.graph_ptr if batched else None)
@@ -299,41 +393,43 @@ def main():
         if batched:  # whole graphs per rank: own K/V rows, no collective
             K = dev_tensor(Kb[row_b:row_e])
             V = dev_tensor(Vb[row_b:row_e])
-            K_sh = V_sh = None
-        else:  # equal padded K/V shards, replicated by one all-gather each (NCCL over NVLink)
-            S = spec.kv_rows
-            lo, hi = f3sdist.kv_slice(spec, csr.n_cols)
-            K_sh = torch.zeros((S, H, d), dtype=tdt, device=dev)
-            V_sh = torch.zeros((S, H, d), dtype=tdt, device=dev)
-            K_sh[:hi - lo] = dev_tensor(Kb[lo:hi])
-            V_sh[:hi - lo] = dev_tensor(Vb[lo:hi])
-            K = torch.empty((world * S, H, d), dtype=tdt, device=dev)
-            V = torch.empty((world * S, H, d), dtype=tdt, device=dev)
+        else:  # equal padded [K||V] shards, replicated by ONE all-gather (NCCL over NVLink)
+            KV_sh = dev_tensor(f3sdist.kv_shard(spec, Kb, Vb, csr.n_cols))
+            KV = torch.empty((world * spec.kv_rows, 2, H, d), dtype=tdt, device=dev)
+            kv_ld = 2 * H * d
     info = plan.info()
     n_loc = row_e - row_b
     O = torch.empty((max(n_loc, 1), H, d), dtype=torch.float32, device=dev)
     variant = f3s.VARIANTS[args.variant]
+    if kv_ld and args.variant != "default":
+        raise SystemExit("--variant needs separate K/V (N = 1 without --kv-interleaved)")
 
-    def attn():
-        if n_loc > 0:
+    def attn(s=sp):
+        if n_loc == 0:
+            return
+        if kv_ld:
+            f3s.attention_kv_raw(plan, Q.data_ptr(), KV.data_ptr(), KV.data_ptr() + H * d * es, kv_ld, O.data_ptr(),
+                                 w.scale, H, d, dt_code, s)
+        else:
             f3s.attention_raw(plan, Q.data_ptr(), K.data_ptr(), V.data_ptr(), O.data_ptr(), w.scale, H, d, dt_code,
-                              sp, variant)
+                              s, variant)
 
-    def step():
-        if K_sh is not None:
-            dist.all_gather_into_tensor(K, K_sh)
-            dist.all_gather_into_tensor(V, V_sh)
-        attn()
+    def exchange():
+        if KV_sh is not None:
+            f3sdist.allgather_kv_into(KV, KV_sh)
 
     for _ in range(args.warmup):
-        step()
+        exchange()
+        attn()
     torch.cuda.synchronize()
 
     # ---- timed region: exactly K steps, barrier + sync on both sides ----
+    cold = not args.warm_l2
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if cold else None
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.4)
-    ev_k = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = f3s.launch_count()
     if world > 1:
@@ -341,24 +437,64 @@ def main():
     torch.cuda.synchronize()
     t_start.record(stream)
     for i in range(args.steps):
-        if K_sh is not None:
-            dist.all_gather_into_tensor(K, K_sh)
-            dist.all_gather_into_tensor(V, V_sh)
-        ev_k[i][0].record(stream)
+        if cold:
+            flush.fill_(i & 0xFF)  # untimed: evicts the previous step's K/V/plan lines from L2
+        ev[i][0].record(stream)
+        exchange()
+        ev[i][1].record(stream)
         attn()
-        ev_k[i][1].record(stream)
+        ev[i][2].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = f3s.launch_count() - launches0
     clk = clocks.stop()
-    step_ms = t_start.elapsed_time(t_end) / args.steps
-    kern_ms = sum(a.elapsed_time(b) for a, b in ev_k) / args.steps
+    step_list = [a.elapsed_time(c) for a, _, c in ev]
+    kern_list = [b.elapsed_time(c) for _, b, c in ev]
+    region_ms = t_start.elapsed_time(t_end)
+    step_ms, kern_ms = float(np.mean(step_list)), float(np.mean(kern_list))
     if world > 1:
         tt = torch.tensor([step_ms, kern_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         step_ms, kern_ms = tt.tolist()
+
+    # warm-L2 back-to-back kernel time (secondary)
+    warm_ms = None
+    if cold:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nw = max(3, min(args.steps, 20))
+        e0.record(stream)
+        for _ in range(nw):
+            attn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        warm_ms = e0.elapsed_time(e1) / nw
+
+    # CUDA-graph batch (launch-bound small graphs, e.g. cora): N calls captured once, replayed
+    gbatch = args.graph_batch if args.graph_batch is not None else (100 if w.name == "cora" else 0)
+    graph = None
+    if gbatch > 0 and world == 1:
+        gs = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            attn(gs.cuda_stream)  # warm the tensor-map cache on this stream
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=gs):
+                for _ in range(gbatch):
+                    attn(gs.cuda_stream)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        gms = e0.elapsed_time(e1) / (reps * gbatch)
+        graph = {"calls_per_graph": gbatch, "ms_per_call": round(gms, 5),
+                 "value": round(4.0 * csr.nnz * d * H / (gms * 1e-3) / 1e9, 3)}
 
     nnz_total = int(csr.nnz)
     useful_flops = 4.0 * nnz_total * d * H
@@ -411,45 +547,43 @@ def main():
                    "api": "f3s_attention_host_async on two alternating streams (pinned host Q/K/V -> device -> fused "
                           "call -> host O; one step's uploads overlap the previous step's read-back)"}
         else:
-            Qh = torch.from_numpy(np.ascontiguousarray(Qb[row_b:row_e]).view(np.int16)).pin_memory()
-            S = K.shape[0] // world if K_sh is not None else 0
-            if K_sh is not None:
-                lo, hi = f3sdist.kv_slice(spec, csr.n_cols)
-                Kh = torch.zeros((S, H, d), dtype=torch.int16).pin_memory()
-                Vh = torch.zeros((S, H, d), dtype=torch.int16).pin_memory()
-                Kh[:hi - lo] = torch.from_numpy(Kb[lo:hi].view(np.int16))
-                Vh[:hi - lo] = torch.from_numpy(Vb[lo:hi].view(np.int16))
+            Qh = torch.from_numpy(np.ascontiguousarray(Qb[row_b:row_e])).view(ht).pin_memory()
+            if KV_sh is not None:
+                KVh = torch.from_numpy(f3sdist.kv_shard(spec, Kb, Vb, csr.n_cols)).view(ht).pin_memory()
+                h2d = [(Q, Qh), (KV_sh, KVh)]
             else:
-                Kh = torch.from_numpy(np.ascontiguousarray(Kb[row_b:row_e]).view(np.int16)).pin_memory()
-                Vh = torch.from_numpy(np.ascontiguousarray(Vb[row_b:row_e]).view(np.int16)).pin_memory()
+                Kh = torch.from_numpy(np.ascontiguousarray(Kb[row_b:row_e])).view(ht).pin_memory()
+                Vh = torch.from_numpy(np.ascontiguousarray(Vb[row_b:row_e])).view(ht).pin_memory()
+                h2d = [(Q, Qh), (K, Kh), (V, Vh)]
             Oh = torch.empty((max(n_loc, 1), H, d), dtype=torch.float32).pin_memory()
-            Kd = K_sh if K_sh is not None else K
-            Vd = V_sh if V_sh is not None else V
 
             def e2e_step():
-                Q.view(torch.int16).copy_(Qh, non_blocking=True)
-                Kd.view(torch.int16).copy_(Kh, non_blocking=True)
-                Vd.view(torch.int16).copy_(Vh, non_blocking=True)
-                step()
+                for dt_, ht_ in h2d:
+                    dt_.view(ht).copy_(ht_, non_blocking=True)
+                exchange()
+                attn()
                 Oh.copy_(O, non_blocking=True)
                 torch.cuda.synchronize()
 
             for _ in range(2):
                 e2e_step()
             dist.barrier()
-            t0 = time.perf_counter()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e_steps = max(3, min(args.steps, 10))
+            e0.record(stream)
             for _ in range(e_steps):
                 e2e_step()
-            dist.barrier()
-            e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
-            tt = torch.tensor([e_ms, Qh.numel() * 2 + Kh.numel() * 4, Oh.numel() * 4], device=dev, dtype=torch.float64)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e_ms = e0.elapsed_time(e1) / e_steps
+            tt = torch.tensor([e_ms, sum(h.numel() * h.element_size() for _, h in h2d), Oh.numel() * 4], device=dev,
+                              dtype=torch.float64)
             dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
             dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
             e_ms, hb, db = tt.tolist()
             e2e = {"value": round(useful_flops / (e_ms * 1e-3) / 1e9, 3), "unit": UNIT, "ms_per_step": round(e_ms, 3),
                    "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(db),
-                   "api": "torch pinned copies + dist all-gather + f3s_attention per rank"}
+                   "api": "per rank: pinned Q and [K||V] shard uploads, one all-gather, f3s_attention_kv, O read-back"}
 
     # ---- cpu baseline: the oracle on this host, bounded sample (rank 0, N = 1 only) ----
     cpu = None
@@ -468,18 +602,28 @@ def main():
                   "per row (2^-4 + deg * 2^-18) * max|V_j| (DESIGN.md c24)"}
 
     if rank == 0:
+        kv_bytes = (Kb.nbytes + Vb.nbytes)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
-            "scaling": "weak" if batched else "strong", "vs_baseline": None, "dtype": {"fp16": "f16", "bf16": "bf16", "e4m3": "e4m3"}[dtype],
-            "data": "synthetic",
+            "scaling": "weak" if batched else "strong", "vs_baseline": None,
+            "dtype": {"fp16": "f16", "bf16": "bf16", "e4m3": "e4m3"}[dtype], "data": "synthetic",
             "config": {"workload": w.description, "n": csr.n_rows, "nnz": nnz_total, "heads": H, "d": d,
                        "row_windows": info["num_rw"], "compacted_cols": info["total_cols"], "tcb16x8": info["total_tcb8"],
                        "accum": "f32", "variant": args.variant, "plan_build_ms": round(info["build_ms"], 3),
-                       "l2": "no flush: per-step inputs+outputs {:.2f} GB > 126 MB L2".format(
-                           (Qb.nbytes + Kb.nbytes + Vb.nbytes + Qb.size * 4) / 1e9),
+                       "split_chunks": info["split_chunks"], "split_windows": info["split_groups"],
+                       "kv_layout": "interleaved [n, 2, H, d]" if kv_ld else "separate K, V [n, H, d]",
+                       "l2": ("cold: a 256 MB write (> 126 MB L2) before every timed step, not timed; "
+                              f"K+V {kv_bytes / 1e6:.1f} MB") if cold else
+                             f"warm: back-to-back steps (K+V {kv_bytes / 1e6:.1f} MB "
+                             f"{'>' if kv_bytes > 126e6 else '<'} 126 MB L2)",
                        "parallelism": "single-gpu" if world == 1 else
-                       ("graphs sharded by nnz, no collective" if batched else f"rows sharded by nnz over {world} + NCCL K/V all-gather")},
+                       ("graphs sharded by nnz, no collective" if batched else
+                        f"rows sharded by nnz over {world} + one NCCL [K||V] all-gather")},
+            "timing": {"step_ms": percentiles(step_list), "kernel_ms": percentiles(kern_list),
+                       "region_ms_incl_flush": round(region_ms, 3),
+                       "warm_l2_kernel_ms": round(warm_ms, 4) if warm_ms is not None else None,
+                       "rank0_exchange_ms": round(float(np.mean(step_list) - np.mean(kern_list)), 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm_gbs, "unit": "GB/s",
                          "frac": round(achieved / hbm_gbs, 4), "traffic": traffic, "peak_source": peak_src,
                          "kernel": "k_f3s_sm100" if args.variant != "simt" else "k_attn_simt",
@@ -488,6 +632,7 @@ def main():
                          "tensor_time_frac": round((f_pad / (bf16_tf * 1e12)) / (kern_ms * 1e-3), 4)},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "cuda_graph_batch": graph,
             "gpu_launches": int(launches),
             "clocks": clk,
             "parity": parity,

@@ -68,6 +68,7 @@ typedef struct {
     float reserved;
     int32_t split_chunks; /* heavy-window split: pieces of at most this many 128-column chunks  */
     int32_t split_groups; /* row windows that are split      */
+    int64_t total_chunks; /* sum over windows of max(1, ceil(w / 128)): kernel chunks of one head  */
 } f3s_plan_info;
 
 /*
@@ -118,20 +119,29 @@ f3s_status f3s_plan_get_info(f3s_plan_t plan, f3s_plan_info* info);
  * thread blocks per row window").  f3s_attention (default variant) processes
  * a row window of more than max_chunks 128-column chunks as pieces of max_chunks chunks on
  * different CTAs; each piece leaves its partial (row max, row sum, unnormalised O) in a
- * per-call scratch buffer and the CTA that completes a window's last piece merges all pieces
- * in piece order (O = sum_p e^{m_p - M} O_p / sum_p e^{m_p - M} l_p), so results stay
- * bitwise deterministic.  f3s_plan picks max(16, ceil(total chunks / (2 * SMs))); this call
- * rebuilds the piece list with another bound (max_chunks <= 0: never split).  Host-synchronous;
- * not to be called while attention calls on the plan are in flight.
- * Errors: INVALID_VALUE (NULL plan), UNSUPPORTED (more than 65535 pieces per window), CUDA.
+ * per-call stream-ordered scratch buffer and a second launch merges the pieces of every split
+ * window in piece order (O = sum_p 2^{m_p - M} O_p / sum_p 2^{m_p - M} l_p), so results stay
+ * bitwise deterministic.  f3s_plan picks f3s_default_split_chunks(info.total_chunks, SMs); this
+ * call rebuilds the piece list with another bound (max_chunks <= 0: never split).  A row-shard
+ * plan (f3s_plan_rows) counts only its own chunks: to split exactly like the single-GPU plan
+ * (and so keep shard results bitwise equal to it) pass the bound of the GLOBAL chunk count,
+ * f3s_default_split_chunks(sum of every shard's total_chunks, SMs).  Host-synchronous; not to be
+ * called while attention calls on the plan are in flight.  On failure the plan keeps its
+ * previous piece list.
+ * Errors: INVALID_VALUE (NULL plan), UNSUPPORTED (more than 2^23 pieces in total), OUT_OF_MEMORY, CUDA.
  */
 f3s_status f3s_plan_set_split(f3s_plan_t plan, int32_t max_chunks);
+
+/* The default split bound: max(16, ceil(total_chunks / (2 * num_sms))) (a window is split when
+ * it alone exceeds half of an SM's even share of all chunks).  Pure host arithmetic. */
+int32_t f3s_default_split_chunks(int64_t total_chunks, int32_t num_sms);
 
 f3s_status f3s_plan_export(f3s_plan_t plan, int32_t* rw_ptr, int32_t* cols, uint16_t* masks, int32_t* rw_order);
 
 /*
  * The fused 3S pass (Alg.1) on sm_100a: per row window and head, gathers
- * of K and V rows by the compacted column list (Alg.1 l.7-8) into shared memory with TMA,
+ * of K and V rows by the compacted column list (Alg.1 l.7-8) into 128B-swizzled shared-memory
+ * tiles (16-byte cp.async; the Q tile and the O tile move by TMA),
  * S^T = K_c Q_w^T on tcgen05 tensor cores into TMEM (l.13), bitmap mask (l.14), online
  * softmax in fp32 (l.16-18), P cast to the input dtype (l.19), O^T += V_c^T P^T on tcgen05
  * (l.21-22), O = O / l written once (l.24).  Row windows are scheduled longest-first
@@ -142,11 +152,26 @@ f3s_status f3s_plan_export(f3s_plan_t plan, int32_t* rw_ptr, int32_t* cols, uint
  *  O      device [n_rows, heads, d] float32, contiguous; must not alias Q/K/V
  *  scale  multiplies Q K^T before the softmax (scale = 1 reproduces Eq.1; 1/sqrt(d) for GT)
  *  heads  >= 1;  d in {64, 128};  dtype F3S_FP16, F3S_BF16 or F3S_E4M3
+ * The library cannot see allocation sizes: Q/O must hold n_rows*heads*d elements and K/V
+ * n_cols*heads*d (the Python binding checks shapes and dtypes before calling).
+ * Runs on the plan's device (the calling thread's current device is restored on return).
  * Asynchronous on `stream`; only launch-time errors are reported (device faults surface at
- * the caller's next synchronisation, CUDA convention).  Bitwise deterministic.
+ * the caller's next synchronisation, CUDA convention).  Each call owns its work-queue counter
+ * (a stream-ordered allocation), so calls may be in flight on any number of streams and CUDA
+ * graphs.  Bitwise deterministic.
  */
 f3s_status f3s_attention(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
                          int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
+
+/*
+ * f3s_attention with K and V rows at an arbitrary row stride (the multi-GPU form: one all-gather
+ * of an interleaved [n_cols, 2, heads, d] buffer replicates K and V together, so K = buf,
+ * V = buf + heads*d, kv_row_stride = 2*heads*d).  Row j of K is K + j*kv_row_stride elements
+ * (likewise V); kv_row_stride >= heads*d and a multiple of 16 bytes.  Default variant; otherwise
+ * as f3s_attention.  Errors: as f3s_attention; INVALID_VALUE / UNSUPPORTED for a bad stride.
+ */
+f3s_status f3s_attention_kv(f3s_plan_t plan, const void* Q, const void* K, const void* V, int64_t kv_row_stride,
+                            float* O, float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
 
 /*
  * Backward of f3s_attention ("SpMM and SDDMM operations in reverse order",
@@ -170,7 +195,7 @@ f3s_status f3s_attention_backward(f3s_plan_t plan, const void* Q, const void* K,
 
 /* Kernel variants for ablations (bench.py --variant); f3s_attention uses F3S_VARIANT_DEFAULT. */
 typedef enum {
-    F3S_VARIANT_DEFAULT = 0, /* tcgen05 + TMA gather kernel, LPT-ordered persistent queue       */
+    F3S_VARIANT_DEFAULT = 0, /* tcgen05 kernel, LPT-ordered persistent queue, heavy-window split */
     F3S_VARIANT_NO_REORDER = 1, /* same kernel, row windows in natural order */
     F3S_VARIANT_SIMT = 2,    /* CUDA-core reference kernel of the same dataflow (no tensor core) */
     F3S_VARIANT_ONE_HEAD = 3 /* tcgen05 kernel with one head per chunk even where the default packs

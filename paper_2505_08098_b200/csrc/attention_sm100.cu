@@ -63,41 +63,45 @@ struct Cfg {
     static constexpr int kRowAlign = 32 / EB;
     static constexpr int kGroupBytes = 1024 * P;     // 8 gathered rows (one swizzle atom per panel)
     static constexpr int kMaxRows = 128;             // compacted columns per chunk at most (MMA1 M = 128)
-    // K tiles live until MMA1 completes, V tiles until MMA2 completes: two FIFO rings
-    // (the F3S_* macros are experiment knobs for tools/variants.sh; the defaults are the product)
-#ifndef F3S_RINGV128_KB
-#define F3S_RINGV128_KB 88
+    // two softmax warpgroups take alternate CHUNKS (chunk c -> warpgroup c % 2): every chunk's
+    // softmax is relative to its own row max, so chunks of one item are independent and both
+    // warpgroups stay busy on long items; the correction group merges the chunk partials
+    static constexpr int kSoftmaxWGs = 2;
+    // S/P/O buffers in flight (TMEM and SMEM); buffer b belongs to warpgroup b % kSoftmaxWGs
+#ifndef F3S_KSB
+#define F3S_KSB 4
 #endif
-#ifndef F3S_KNQ128
-#define F3S_KNQ128 4
-#endif
-    static constexpr int kRingK = HG == 4 ? 48 * 1024 : 64 * 1024;
-#ifndef F3S_RINGV8_KB
-#define F3S_RINGV8_KB 88
-#endif
-    static constexpr int kRingV = HG == 4 ? 64 * 1024 : EB == 1 ? F3S_RINGV8_KB * 1024 : D == 128 ? F3S_RINGV128_KB * 1024 : 88 * 1024;
-    static constexpr int kRingBytes = kRingK + kRingV;
+    static constexpr int kSB = HG == 4 ? 4 : F3S_KSB;
+    static_assert(kSB % kSoftmaxWGs == 0, "S/P/O buffers are owned by one warpgroup each");
     static constexpr int kNS = D == 128 ? 20 : 22;   // chunk slots (ids, masks, descriptor, barriers)
-#ifndef F3S_KNQ8
-#define F3S_KNQ8 8
-#endif
     // Q tile slots (items in flight per CTA); fp8 tiles are half as large and carry half the bytes
     // per chunk, so more items are kept in flight
-    static constexpr int kNQ = HG == 4 ? 6 : EB == 1 ? F3S_KNQ8 : D == 128 ? F3S_KNQ128 : 12;
+#ifndef F3S_NQ
+#define F3S_NQ 0
+#endif
+    static constexpr int kNQ = HG == 4 ? 6 : EB == 1 ? 8 : F3S_NQ > 0 ? F3S_NQ : 4;
     static constexpr int kQBytes = 16 * kRowPitch * HG;  // HG head tiles of 16 x D
     static constexpr int kPBytes = 16 * kMaxRows * EB;
-#ifndef F3S_KSB8
-#define F3S_KSB8 4
-#endif
-    static constexpr int kSB = EB == 1 ? F3S_KSB8 : 4;  // S/P/O buffers in flight (TMEM and SMEM)
-#ifndef F3S_KNO8
-#define F3S_KNO8 2
-#endif
-    static constexpr int kNO = HG == 4 ? 1 : EB == 1 ? F3S_KNO8 : 2;  // O staging tiles (16 x HG*D fp32) for the TMA store
+    static constexpr int kNO = HG == 4 ? 1 : 2;      // O staging tiles (16 x HG*D fp32) for the TMA store
     static constexpr int kOBytes = 16 * D * 4 * HG;
     static constexpr int kTmemCols = HG == 4 ? 512 : kSB <= 4 ? 128 : 256;  // S^T and O^T: kSB x HG buffers of 16 columns each
     static_assert(2 * 16 * kSB * HG <= kTmemCols, "TMEM columns");
     static constexpr int kSlotBytes = 32 + 128 * 4 + 128 * 2;  // sizeof(Slot)
+    static constexpr int kCorrBytes = 352;                  // sizeof(CorrSlot)
+    static constexpr int kNumBars = 6 * kNS + 2 * kNQ + 5 * kSB;
+    // everything but the two gather rings
+    static constexpr int kFixedBytes = kNQ * kQBytes + kSB * kPBytes + kNO * kOBytes + kNS * kSlotBytes +
+                                       kSB * 4 * 16 * 4 + kSB * kCorrBytes + 2 * kNS * 8 + kNumBars * 8 + 16;
+    // K tiles live until MMA1 completes, V tiles until MMA2 completes: two FIFO rings.  The V ring
+    // (tiles wait there for the softmax and MMA2) takes all the shared memory that is left, in
+    // whole allocation units (16 gathered rows)
+#ifndef F3S_RINGK_KB
+#define F3S_RINGK_KB 64
+#endif
+    static constexpr int kRingK = HG == 4 ? 48 * 1024 : F3S_RINGK_KB * 1024;
+    static constexpr int kRingV = HG == 4 ? 64 * 1024
+                                          : (227 * 1024 - kRingK - kFixedBytes) / (2 * kGroupBytes) * (2 * kGroupBytes);
+    static constexpr int kRingBytes = kRingK + kRingV;
     static constexpr int oRing = 0;                  // K ring, then V ring
     static constexpr int oRingV = kRingK;
     static constexpr int oQ = oRing + kRingBytes;
@@ -105,39 +109,17 @@ struct Cfg {
     static constexpr int oOst = oP + kSB * kPBytes;
     static constexpr int oSlot = oOst + kNO * kOBytes;
     static constexpr int oRed = oSlot + kNS * kSlotBytes;  // float [kSB][4][16] chunk row-max partials
-    static constexpr int kLB = 8;                    // row-sum hand-off buffers (items in flight, even)
-    static constexpr int oLred = oRed + kSB * 4 * 16 * 4;  // float [kLB][4][16] row-sum partials per item
-    static constexpr int oLm = oLred + kLB * 4 * 16 * 4;   // float [kLB][16] row max of a split piece
-    static constexpr int oCorr = oLm + kLB * 16 * 4;        // CorrSlot [kSB]
-    static constexpr int kCorrBytes = 128;                  // sizeof(CorrSlot)
+    static constexpr int oCorr = oRed + kSB * 4 * 16 * 4;  // CorrSlot [kSB]
     static constexpr int oReg = oCorr + kSB * kCorrBytes;   // int2 [2][kNS] ring regions (K, V)
-    // per-chunk flags for the softmax warpgroups, in a ring longer than the slot ring: a warpgroup
-    // that skips another's chunk reads them here, never the slot (which MMA2 may already have
-    // retired and the index warp refilled); chunk c's entry is rewritten only after MMA1 of
-    // chunk c + kNI - kNS, i.e. after every warpgroup passed chunk c
-    static constexpr int kNI = 64;
-    static_assert(kNI >= kNS + 2 * kSB + 8, "info ring");
-    static constexpr int oInfo = oReg + 2 * kNS * 8;        // int [kNI]
-    static constexpr int kNumBars = 6 * kNS + 2 * kNQ + 5 * kSB + 2 * kLB;
-    static constexpr int oBar = oInfo + kNI * 4;
+    static constexpr int oBar = oReg + 2 * kNS * 8;
     static constexpr int oTmem = oBar + kNumBars * 8;
     static constexpr int kSmemBytes = oTmem + 16;
     static constexpr int kCtasPerSm = 1;
     // MMA1 and MMA2 are issued by two warps that each sleep on their own barriers (mbarrier
     // try_wait wakes ~60 cycles after the arrive); one warp polling four barriers with test_wait
     // (~150 cycles each) reacted 0.9-2.8 us late (measured)
-#ifndef F3S_LOADERS
-#define F3S_LOADERS 4
-#endif
-    static constexpr int kLoaderWarps = F3S_LOADERS;  // cp.async gather warps (20 warps in all keeps 96 registers)
+    static constexpr int kLoaderWarps = 4;           // cp.async gather warps (20 warps in all keeps 96 registers)
     static constexpr int kMma2Warp = 3 + kLoaderWarps;
-    // two softmax warpgroups take alternate work items: one warpgroup's chunk is a long chain of
-    // dependent short-latency steps (measured: issue-active ~17% of its cycles), so a second
-    // independent chain doubles the softmax throughput
-#ifndef F3S_SMWG
-#define F3S_SMWG 2
-#endif
-    static constexpr int kSoftmaxWGs = F3S_SMWG;
     static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps + 1,
                          kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
     static constexpr int kThreads = 32 * (kCorr0 + 4);  // control, MMA, index, loaders, softmax, correction
@@ -163,13 +145,11 @@ template <int D, int HG, int EB = 2> struct Bars {
     __host__ __device__ static constexpr int pfull(int b) { return kB0 + C::kSB + b; }
     __host__ __device__ static constexpr int ofull(int b) { return kB0 + 2 * C::kSB + b; }
     __host__ __device__ static constexpr int pempty(int b) { return kB0 + 3 * C::kSB + b; }
-    __host__ __device__ static constexpr int lfull(int b) { return kB0 + 4 * C::kSB + b; }
-    __host__ __device__ static constexpr int lempty(int b) { return kB0 + 4 * C::kSB + C::kLB + b; }
-    __host__ __device__ static constexpr int rfull(int s) { return kB0 + 4 * C::kSB + 2 * C::kLB + s; }
-    __host__ __device__ static constexpr int kempty(int s) { return kB0 + 4 * C::kSB + 2 * C::kLB + C::kNS + s; }
-    // S^T buffer b may be overwritten by MMA1: every softmax warpgroup passed its previous chunk
-    // (the owner after the P-tile wait, the others in their skip path): 4 warp arrivals each
-    __host__ __device__ static constexpr int sfree(int b) { return kB0 + 4 * C::kSB + 2 * C::kLB + 2 * C::kNS + b; }
+    __host__ __device__ static constexpr int rfull(int s) { return kB0 + 4 * C::kSB + s; }
+    __host__ __device__ static constexpr int kempty(int s) { return kB0 + 4 * C::kSB + C::kNS + s; }
+    // S^T buffer b may be overwritten by MMA1: its owner warpgroup's 4 warps read it (and the
+    // row-max partials) for the buffer's previous chunk
+    __host__ __device__ static constexpr int sfree(int b) { return kB0 + 4 * C::kSB + 2 * C::kNS + b; }
 };
 
 // One chunk of one work item: written by the index warp (ids/masks by cp.async.bulk), the
@@ -177,7 +157,7 @@ template <int D, int HG, int EB = 2> struct Bars {
 struct __align__(16) Slot {
     int32_t rw;        // row window k
     int32_t head;      // head h
-    int32_t rows;      // valid compacted columns in this chunk (0 for an empty RW, -1 = stop)
+    int32_t rows;      // valid compacted columns in this chunk (0 for an empty RW; < 0: stop)
     int32_t ring_off;  // byte offset of the K tile in the ring (V tile follows)
     int32_t qslot;
     int32_t flags;     // bit0 first chunk of item, bit1 last chunk, bit2 Q-slot phase, bits 8..31 split:
@@ -187,12 +167,12 @@ struct __align__(16) Slot {
     int32_t cols[128];     // gathered row ids (tail repeats the last column)
     uint16_t masks[128];   // 16-bit row masks (bitmap)
 };
-// softmax -> correction hand-off for one chunk (double-buffered with P)
+// softmax -> correction hand-off for one chunk (one per S/P/O buffer)
 struct __align__(16) CorrSlot {
-    float alpha[16];   // e^{m_old - m_new} per query row (Alg.1 l.21)
+    float m[16];         // the chunk's row max m_c (log2 units, floored; Alg.1 l.16)
+    float lpart[4][16];  // per-warp partial row sums of the chunk's unrounded E = 2^(S - m_c) (l.17)
     int32_t rows, flags, rw, head;
-    uint64_t t_s, t_p; // F3S_TRACE stamps of the softmax group (written out by the correction group)
-    uint64_t tq[4];    // diagnostics (F3S_TRACE_EV0 == 3): per-warp time just before the pfull arrive
+    uint64_t t_s, t_p;   // F3S_TRACE stamps of the softmax group (written out by the correction group)
 };
 
 static_assert(sizeof(CorrSlot) == Cfg<64>::kCorrBytes && sizeof(Slot) == Cfg<64>::kSlotBytes, "layout");
@@ -229,18 +209,23 @@ template <typename T> __device__ __forceinline__ uint32_t pack2(float lo, float 
 template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) { return pack_f16x2(lo, hi); }
 template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) { return pack_bf16x2(lo, hi); }
 
+// Running row max starts at a finite floor instead of -inf so that every exponent is well
+// defined without branches: 2^(floor - m) = 0 for a real m, 2^(-inf - m) = 0 for masked scores,
+// and a row with no entry in a chunk keeps m_c = floor and an all-zero E (reading c5).
+constexpr float kMFloor = -8.5e37f;
+
 template <int D, typename T, bool kDiag, int HG>
 __global__ void __launch_bounds__(Cfg<D, HG, (int)sizeof(T)>::kThreads, Cfg<D, HG, (int)sizeof(T)>::kCtasPerSm)
-k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const int4* __restrict__ meta,
+k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, const int4* __restrict__ meta,
             const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
-            int32_t* __restrict__ counter, int32_t n_items, int32_t H, int32_t n_rows, int32_t chunk_rows,
-            const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float* __restrict__ O, float scale_log2,
-            uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt,
+            int32_t* __restrict__ counter, int32_t n_items, int32_t H, int64_t ldkv,
+            const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float scale_log2,
+            uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt_arg,
             float* __restrict__ scratch) {
     constexpr int EB = (int)sizeof(T);
     using C = Cfg<D, HG, EB>;
     using B = Bars<D, HG, EB>;
+    constexpr int chunk_rows = C::kMaxRows;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sb = smem_u32(smem);
     if (sb & 1023) __trap();  // swizzled tiles need 1024-byte alignment
@@ -248,21 +233,22 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     auto bar = [&](int i) -> uint32_t { return sb + C::oBar + 8u * i; };
     Slot* slots = reinterpret_cast<Slot*>(smem + C::oSlot);
     CorrSlot* corr = reinterpret_cast<CorrSlot*>(smem + C::oCorr);
+    // Sensitivity experiments exist only in the diagnostics instantiation (f3s_attention_trace
+    // with trace_chunks < 0; results are wrong): bit0 no exp work in the softmax, bit1 no MMA2,
+    // bit2 no MMA1, bit3 no K/V gathers, bit5 no S load / row max, bit6 no O stores, bit7 no
+    // correction work.  The product kernel (kDiag = false) compiles every test away.
+    const int32_t expt = kDiag ? expt_arg : 0;
     // F3S_TRACE: per CTA and chunk, globaltimer stamps of the pipeline events
     // [0 slot written, 1 gathers issued, 2 MMA1 issued, 3 S seen, 4 P written, 5 MMA2 issued, 6 O seen, 7 item stored]
     auto stamp = [&](int32_t c, int ev) {
         if (kDiag && trace != nullptr && c < trace_chunks)
             trace[((size_t)blockIdx.x * trace_chunks + c) * 8 + ev] = globaltimer_ns();
     };
-    // profile mode (trace_chunks == 0): each role accumulates ns spent per phase in registers
-    // (SM cycles) and writes trace[cta][64] once at the end (no stores on the hot path)
+    // profile mode (trace_chunks == 0): each role accumulates SM cycles spent per phase in
+    // registers and writes trace[cta][64] once at the end (no stores on the hot path)
     const bool prof = kDiag && trace != nullptr && trace_chunks == 0;
-    // expt (f3s_attention_trace only; results are wrong): bit0 no exp work in the softmax,
-    // bit1 no MMA2, bit2 no MMA1, bit3 no K/V gathers, bit4 consumer-side proxy fence before the
-    // MMAs, bit5 no S load / row max in the softmax, bit6 no O stores, bit7 no correction work.  0 in
-    // every real call.
     uint32_t pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t pt0 = prof ? (uint32_t)clock() : 0;  // SM cycles (cheap to read, unlike globaltimer)
+    uint32_t pt0 = prof ? (uint32_t)clock() : 0;
     auto lap = [&](int k) {  // charge the cycles since the previous lap to counter k
         if (prof) {
             const uint32_t t = (uint32_t)clock();
@@ -298,18 +284,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             mbar_init(bar(B::pfull(b)), 128);
             mbar_init(bar(B::ofull(b)), 1);
             mbar_init(bar(B::pempty(b)), 128);
-            mbar_init(bar(B::sfree(b)), 4 * C::kSoftmaxWGs);
-        }
-        for (int b = 0; b < C::kLB; ++b) {
-            mbar_init(bar(B::lfull(b)), 128);
-            mbar_init(bar(B::lempty(b)), 128);
+            mbar_init(bar(B::sfree(b)), 4);
         }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmQ);
-        tma_prefetch_desc(&tmK);
-        tma_prefetch_desc(&tmV);
         tma_prefetch_desc(&tmO);
     }
     if (warp == 1) {
@@ -360,7 +340,6 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         sl.rows = rows;
                         sl.qslot = qs;
                         sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2) | (sp << 8);
-                        reinterpret_cast<volatile int32_t*>(smem + C::oInfo)[seq % C::kNI] = sl.flags;
                         sl.ralloc = rows > 0 ? (HG == 1 ? ((rows + C::kRowAlign - 1) & ~(C::kRowAlign - 1)) : C::kMaxRows) : 0;
                         const uint32_t fb = bar(B::idxfull(s));
                         if (rows > 0) {
@@ -371,13 +350,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         } else {
                             mbar_arrive(fb);
                         }
-// F3S_TRACE_EV0 (diagnostic builds only; tools/variants.sh): 0 = the default stamps; 3 = per
-// softmax warp the time just before its pfull arrive (in events 0/2/3/7); 4 = when the MMA2 warp
-// saw P (event 0) and V (event 7) complete
-#ifndef F3S_TRACE_EV0
-#define F3S_TRACE_EV0 0
-#endif
-                        if (F3S_TRACE_EV0 == 0) stamp(seq, 0);
+                        stamp(seq, 0);
                         lap(2);
                     }
                     ++seq;
@@ -386,11 +359,14 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
         }
         if (lane == 0) {
-            const int s = seq % C::kNS;
-            mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
-            slots[s].rows = -1;
-            reinterpret_cast<volatile int32_t*>(smem + C::oInfo)[seq % C::kNI] = -1;
-            mbar_arrive(bar(B::idxfull(s)));
+            // one stop marker per softmax warpgroup (each walks only its own chunk parity); the
+            // producer, loaders and MMA warps stop at the first.  rows = -1 - w.
+            for (int w = 0; w < C::kSoftmaxWGs; ++w, ++seq) {
+                const int s = seq % C::kNS;
+                mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+                slots[s].rows = -1 - w;
+                mbar_arrive(bar(B::idxfull(s)));
+            }
             prof_flush(0);
         }
         __syncwarp();
@@ -478,7 +454,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         const int lw = warp - C::kLoader0;
         const int piece = lane % kPieces, rsub = lane / kPieces;
         const int pnl = piece >> 3, cc = piece & 7;
-        const int64_t ldb = (int64_t)H * C::RB;
+        const int64_t ldb = ldkv;  // bytes between consecutive K (and V) rows
         int32_t seq = 0;
         for (;;) {
             const int s = seq % C::kNS;
@@ -534,7 +510,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const Slot& sl = slots[s];
                 const int rows = sl.rows, flags = sl.flags, qslot = sl.qslot, roff = sl.ring_off;
                 if (rows < 0) break;
-                mbar_wait(bar(B::sfree(b)), ((n1 / C::kSB) & 1) ^ 1);  // both warpgroups passed chunk n1 - kSB
+                mbar_wait(bar(B::sfree(b)), ((n1 / C::kSB) & 1) ^ 1);  // owner read chunk n1 - kSB
                 if (flags & 1) mbar_wait(bar(B::qfull(qslot)), (flags >> 2) & 1);
                 tc_fence_after();
                 const uint64_t a0 = dK + ((sb + C::oRing + roff) >> 4);
@@ -555,7 +531,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 mma_commit_warp(bar(B::sfull(b)));
                 mma_commit_warp(bar(B::kempty(s)));
                 if (flags & 2) mma_commit_warp(bar(B::qempty(qslot)));
-                if (lane == 0 && F3S_TRACE_EV0 != 3) stamp(n1, 2);
+                if (lane == 0) stamp(n1, 2);
             }
         } else {
             // O^T = V_c^T . P^T: A (V_c) MN-major; B (P^T) MN-major with a 32-byte swizzle for
@@ -570,9 +546,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const int rows = slots[s].rows;
                 if (rows < 0) break;
                 mbar_wait(bar(B::pfull(b)), (n2 / C::kSB) & 1);  // P_c written
-                if (F3S_TRACE_EV0 == 4 && lane == 0) stamp(n2, 0);
                 mbar_wait(bar(B::vfull(s)), (n2 / C::kNS) & 1);  // V_c landed
-                if (F3S_TRACE_EV0 == 4 && lane == 0) stamp(n2, 7);
                 tc_fence_after();
                 if (rows > 0 && !(expt & 2)) {
                     const uint64_t a0 = dV + ((sb + C::oRingV + slots[s].pad) >> 4);
@@ -599,56 +573,42 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         }
         __syncwarp();
     } else if (warp < C::kCorr0) {
-        // ===== softmax warpgroup =====================================================
+        // ===== softmax warpgroups ====================================================
+        // Warpgroup wg takes chunks c = wg, wg + 2, ... (every chunk of every item).  Per chunk
+        // (Alg.1 l.14-19): masked scores, the chunk's row max m_c (l.16), E = 2^(S - m_c) (l.17),
+        // E cast to the input dtype for MMA2 (l.19), and the per-warp partial row sums of the
+        // unrounded E (l.18).  Relative to m_c rather than the running max, every chunk is
+        // independent of the item's earlier chunks; the correction group applies the rescaling
+        // of l.18/l.21 when it merges the chunk into the running (m, l, O).
         const int q = warp & 3;          // TMEM lane quadrant this warp may access
         const int p = 32 * q + lane;     // compacted column of the chunk (S^T lane)
-        const int wg = (warp - C::kSoftmax0) >> 2;  // this warpgroup owns the items with index % 2 == wg
+        const int wg = (warp - C::kSoftmax0) >> 2;
         const uint32_t tl = (uint32_t)(32 * q) << 16;
         float* red = reinterpret_cast<float*>(smem + C::oRed);
-        float* lred = reinterpret_cast<float*>(smem + C::oLred);
-        // Running row max starts at a finite floor instead of -inf so that every exponent below
-        // is well defined without branches: alpha = 2^(m_old - m_new) is 0 at a row's first
-        // entries and 1 while the row is still empty; masked scores are -inf and give p = 0.
-        constexpr float kMFloor = -8.5e37f;
-        float m[16], l[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) { m[i] = kMFloor; l[i] = 0.f; }
-        int32_t seq = 0, item = -1;  // item: index of the current chunk's work item in queue order
-        for (;;) {
+        for (int32_t seq = wg;; seq += C::kSoftmaxWGs) {
             const int s = seq % C::kNS;
             const int b = seq % C::kSB;
             const uint32_t bph = (seq / C::kSB) & 1;
-            mbar_wait(bar(B::kfull(s)), (seq / C::kNS) & 1);
+            // the slot header and masks (idxfull: the index warp's writes and bulk copies);
+            // the slot cannot be retired before MMA2 has this chunk's P
+            mbar_wait(bar(B::idxfull(s)), (seq / C::kNS) & 1);
             if (p == 0) lap(0);
             const Slot& sl = slots[s];
-            const int info = reinterpret_cast<const volatile int32_t*>(smem + C::oInfo)[seq % C::kNI];
-            if (info < 0) {  // warpgroup 0 forwards the stop to the correction group
-                if (wg == 0) {
+            const int rows = sl.rows;
+            if (rows < 0) {  // the warpgroup that meets the first stop marker forwards it
+                if (rows == -1) {
                     mbar_wait(bar(B::pempty(b)), bph ^ 1);
                     if (p == 0) corr[b].rows = -1;
                     mbar_arrive(bar(B::pfull(b)));
-                    if (p == 0) prof_flush(18);
                 }
+                if (p == 0) prof_flush(18);
                 break;
             }
-            const int flags = info;
-            if (flags & 1) ++item;
-            if (item % C::kSoftmaxWGs != wg) {  // another warpgroup's item
-                // Observe the phase of the shared S^T buffer b, then release it: MMA1 may refill
-                // buffer b only when both warpgroups passed this chunk, so neither can take phase
-                // k+1 of sfull(b) for phase k.  Free of cost: MMA1 completes in chunk order, so
-                // this warpgroup's next chunk waits longer anyway.
-                mbar_wait(bar(B::sfull(b)), bph);
-                if (lane == 0) mbar_arrive(bar(B::sfree(b)));
-                ++seq;
-                continue;
-            }
-            // the owner reads the slot: it cannot be retired before this chunk's P (MMA2 needs it)
-            const int rows = sl.rows;
+            const int flags = sl.flags;
             // S^T lane p <-> compacted column p (HG = 1), or column `lane` of head q (HG = 4)
             const int col = HG == 1 ? p : lane;
             const uint32_t mask = col < rows ? (uint32_t)sl.masks[col] : 0u;
-            const int rw = sl.rw, hd = sl.head, sp = flags >> 8;  // split piece (0: none)
+            const int rw = sl.rw, hd = sl.head;
             mbar_wait(bar(B::sfull(b)), bph);
             tc_fence_after();
             uint64_t t_s = 0;
@@ -662,29 +622,15 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                 for (int i = 0; i < 16; ++i) x[i] = ((mask >> i) & 1u) ? x[i] * scale_log2 : -INFINITY;  // Alg.1 l.14
             }
-            // chunk row max (Alg.1 l.16): warp butterfly (+ 4-warp combine when the chunk's columns
-            // span the four warps, HG = 1)
+            // chunk row max (Alg.1 l.16): warp butterfly (+ a 4-warp combine when the chunk's
+            // columns span the four warps, HG = 1)
             const float rm = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
+            float cm[16];
             if (HG == 1) {
                 if (!(lane & 1)) red[(b * 4 + q) * 16 + ((lane >> 1) & 15)] = rm;
                 if (p == 0) lap(2);
                 named_bar_sync(1 + wg, 128);
-            }
-            // P_b / corr_b are free once the correction group consumed chunk seq - kSB
-            mbar_wait(bar(B::pempty(b)), bph ^ 1);
-            if (p == 0) lap(3);
-            const float4* r4 = reinterpret_cast<const float4*>(red + b * 64);
-            // P^T is the MN-major B operand of MMA2 with a 32-byte swizzle: compacted column p
-            // owns one 32-byte row (its 16 query rows), 8 rows per 256-byte atom, the two 16-byte
-            // halves swapped when bit 2 of p is set.
-            uint4* prow = reinterpret_cast<uint4*>(smem + C::oP + b * C::kPBytes + (p >> 3) * 256 + (p & 7) * 32);
-            // fp8 P: E scaled by 2^8 (exponent offset) so that [0, 1] lands in e4m3's normal range
-            // [2^-6, 448] down to 2^-14; l_o sums the same scaled values, so O / l is unchanged
-            auto pexp = [](float v) { return EB == 1 ? ex2(v + 8.f) : ex2(v); };
-            const int sw = (p >> 2) & 1;
-            float av[16], pv[16];
-            float cm[16];  // chunk row max
-            if (HG == 1) {  // 4-warp combine
+                const float4* r4 = reinterpret_cast<const float4*>(red + b * 64);
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
                     const float4 w0 = r4[g], w1 = r4[4 + g], w2 = r4[8 + g], w3 = r4[12 + g];
@@ -697,32 +643,26 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                 for (int i = 0; i < 16; ++i) cm[i] = __shfl_sync(0xffffffffu, rm, 2 * i);
             }
-            // Release S^T_b (loaded above) and the row-max partials red[b] (read just above: the
-            // owner of chunk seq + kSB rewrites them once MMA1 refilled S^T_b).  Releasing after the
-            // P-tile wait also keeps the pempty phases exact: MMA1(seq + kSB) then implies the
-            // correction consumed chunk seq - kSB.
+            // S^T_b and red[b] are read: MMA1 may refill buffer b (its next chunk is this
+            // warpgroup's own, so red[b] is rewritten only after this chunk's combine)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(B::sfree(b)));
-            if (flags & 1) {  // item's first chunk: m_o = floor, l_o = 0, nothing to rescale (alpha = 0)
+            if (p == 0) lap(3);
+            // fp8 P: E scaled by 2^8 (exponent offset) so that [0, 1] lands in e4m3's normal range
+            // [2^-6, 448] down to 2^-14; l sums the same scaled values, so O / l is unchanged
+            auto pexp = [](float v) { return EB == 1 ? ex2(v + 8.f) : ex2(v); };
+            float pv[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    m[i] = fmaxf(kMFloor, cm[i]);
-                    pv[i] = (expt & 1) ? x[i] : pexp(x[i] - m[i]);  // E_i = e^{S_i - m_i} (l.17); 0 where masked
-                    l[i] = pv[i];
-                    av[i] = 0.f;
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float mn = fmaxf(m[i], cm[i]);
-                    av[i] = (expt & 1) ? 1.f : ex2(m[i] - mn);  // e^{m_o - m_i} (l.18, l.21)
-                    m[i] = mn;
-                    pv[i] = (expt & 1) ? x[i] : pexp(x[i] - mn);
-                    l[i] = fmaf(l[i], av[i], pv[i]);  // l_o (l.18)
-                }
+            for (int i = 0; i < 16; ++i) {
+                cm[i] = fmaxf(kMFloor, cm[i]);                    // m_c (reading c5)
+                pv[i] = (expt & 1) ? x[i] : pexp(x[i] - cm[i]);   // E = e^{S - m_c} (l.17); 0 where masked
             }
+            const float rl = rowreduce16(pv, lane, OpAdd());      // this warp's part of rowsum(E) (l.18)
             if (p == 0) lap(6);
+            // P_b / corr_b are free once the correction group consumed chunk seq - kSB
+            mbar_wait(bar(B::pempty(b)), bph ^ 1);
+            if (p == 0) lap(4);
             if constexpr (EB == 1) {
                 // E cast to e4m3 (satfinite, round to nearest even) into the K-major 128B-swizzled
                 // [16 x 128] B tile: byte p of row i, 16-byte chunk (p >> 4) ^ (i & 7)
@@ -731,7 +671,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 for (int i = 0; i < 16; ++i)
                     pt[(i >> 3) * 1024 + (i & 7) * 128 + ((((p >> 4) ^ (i & 7)) & 7) << 4)] =
                         (uint8_t)__nv_cvt_float_to_fp8(pv[i], __NV_SATFINITE, __NV_E4M3);
-            } else {  // E cast to the input dtype into SMEM (l.19): two 16-byte stores
+            } else {
+                // E cast to the input dtype (l.19): P^T is the MN-major B operand of MMA2 with a
+                // 32-byte swizzle: compacted column p owns one 32-byte row (its 16 query rows), 8
+                // rows per 256-byte atom, the two 16-byte halves swapped when bit 2 of p is set
+                uint4* prow = reinterpret_cast<uint4*>(smem + C::oP + b * C::kPBytes + (p >> 3) * 256 + (p & 7) * 32);
+                const int sw = (p >> 2) & 1;
                 const uint4 lo = make_uint4(pack2<T>(pv[0], pv[1]), pack2<T>(pv[2], pv[3]), pack2<T>(pv[4], pv[5]),
                                             pack2<T>(pv[6], pv[7]));
                 const uint4 hi = make_uint4(pack2<T>(pv[8], pv[9]), pack2<T>(pv[10], pv[11]), pack2<T>(pv[12], pv[13]),
@@ -739,12 +684,11 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 prow[sw] = lo;
                 prow[sw ^ 1] = hi;
             }
+            if (!(lane & 1)) corr[b].lpart[q][(lane >> 1) & 15] = rl;
             if (p == 0) {
-                float4* a4 = reinterpret_cast<float4*>(corr[b].alpha);
-                a4[0] = make_float4(av[0], av[1], av[2], av[3]);
-                a4[1] = make_float4(av[4], av[5], av[6], av[7]);
-                a4[2] = make_float4(av[8], av[9], av[10], av[11]);
-                a4[3] = make_float4(av[12], av[13], av[14], av[15]);
+                float4* m4 = reinterpret_cast<float4*>(corr[b].m);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) m4[g] = make_float4(cm[4 * g], cm[4 * g + 1], cm[4 * g + 2], cm[4 * g + 3]);
                 reinterpret_cast<int4*>(&corr[b].rows)[0] = make_int4(rows, flags, rw, hd);
                 if (kDiag) {
                     corr[b].t_s = t_s;
@@ -754,35 +698,26 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (p == 0) lap(7);
             fence_proxy_async_smem();
             tc_fence_before();
-            if (F3S_TRACE_EV0 == 3 && kDiag && lane == 0) corr[b].tq[q] = globaltimer_ns();
             mbar_arrive(bar(B::pfull(b)));
-            if (p == 0) lap(4);
-            if (flags & 2) {
-                // l_o partial sums of the item (l.18) -> correction group
-                const int ib = item % C::kLB;
-                const float rl = rowreduce16(l, lane, OpAdd());
-                mbar_wait(bar(B::lempty(ib)), ((item / C::kLB) & 1) ^ 1);
-                if (!(lane & 1)) lred[(ib * 4 + q) * 16 + ((lane >> 1) & 15)] = rl;
-                if (p == 0 && sp) {  // a piece of a split window also hands over its row max
-                    float4* m4 = reinterpret_cast<float4*>(smem + C::oLm + ib * 64);
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) m4[g] = make_float4(m[4 * g], m[4 * g + 1], m[4 * g + 2], m[4 * g + 3]);
-                }
-                mbar_arrive(bar(B::lfull(ib)));
-                if (p == 0) lap(5);
-            }
-            ++seq;
+            if (p == 0) lap(5);
         }
     } else {
         // ===== correction / epilogue warpgroup =======================================
+        // Chunks in order: merge chunk c's (m_c, l_c, O_c = E_c V_c) into the item's running
+        // (m, l, O) with the rescaling of Alg.1 l.18/l.21:
+        //   M = max(m, m_c),  l = 2^(m - M) l + 2^(m_c - M) l_c,  O = 2^(m - M) O + 2^(m_c - M) O_c
+        // and at the item's last chunk write O = O / l (l.24; rows with l = 0 -> 0, reading c4)
+        // through a shared-memory tile and one TMA store, or a split piece's (m, l, O) partial.
+        // O^T lives in fp32 registers: thread (warp q, lane) holds one feature for the 16 rows.
         const int q = warp & 3;
         const uint32_t tl = (uint32_t)(32 * q) << 16;
-        const float* lred = reinterpret_cast<const float*>(smem + C::oLred);
+        const int ri = lane & 15;        // the row whose statistics this lane keeps (lanes 16..31 mirror)
         float oacc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) oacc[i] = 0.f;
-        int32_t seq = 0, item = 0;
-        for (;;) {
+        float m_run = kMFloor, l_run = 0.f;
+        int32_t item = 0;
+        for (int32_t seq = 0;; ++seq) {
             const int b = seq % C::kSB;
             const uint32_t bph = (seq / C::kSB) & 1;
             mbar_wait(bar(B::pfull(b)), bph);
@@ -795,28 +730,21 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 if (lead) prof_flush(24);
                 break;
             }
-            // O_i = diag(alpha) O_i + E_i V_j (l.21-22): the chunk's O^T arrives in TMEM
+            // the chunk's O_c^T arrives in TMEM
             mbar_wait(bar(B::ofull(b)), bph);
             tc_fence_after();
             if (lead) {
                 if (kDiag && trace != nullptr && seq < trace_chunks) {
                     trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 3] = corr[b].t_s;
                     trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 4] = corr[b].t_p;
-                    if (F3S_TRACE_EV0 == 3) {
-                        trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 0] = corr[b].tq[3];
-                        trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 2] = corr[b].tq[1];
-                        trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 7] = corr[b].tq[2];
-                        trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 3] = corr[b].tq[0];
-                    }
                 }
                 stamp(seq, 6);
                 lap(1);
             }
             if constexpr (HG > 1) {
                 // head groups: one chunk per item (every window <= 32 columns), so O_g = O^T_g / l_g
-                // for each head g of the group, staged as one [16 x HG*D] tile and stored by one TMA
-                const int ib = item % C::kLB;
-                mbar_wait(bar(B::lfull(ib)), (item / C::kLB) & 1);
+                // for each head g of the group (warp g's row sums are head g's), staged as one
+                // [16 x HG*D] tile and stored by one TMA
                 float* ost = reinterpret_cast<float*>(smem + C::oOst);
                 if (lead) bulk_wait_group_read<0>();  // the previous item's store has read the tile
                 named_bar_sync(1 + C::kSoftmaxWGs, 128);
@@ -826,7 +754,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 for (int g = 0; g < HG; ++g) {
                     float ov[16];
                     tmem_ld_32x32b_x16(tmem + tl + 16 * C::kSB * HG + (b * HG + g) * 16, ov);
-                    const float4* l4 = reinterpret_cast<const float4*>(lred + (ib * 4 + g) * 16);  // head g's row sums
+                    const float4* l4 = reinterpret_cast<const float4*>(corr[b].lpart[g]);  // head g's row sums
                     if (has) {
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
@@ -842,109 +770,83 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
                 tc_fence_before();
                 mbar_arrive(bar(B::pempty(b)));
-                mbar_arrive(bar(B::lempty(ib)));
                 fence_proxy_async_smem();
                 named_bar_sync(1 + C::kSoftmaxWGs, 128);
                 if (lead) {
                     if (!(expt & 64)) tma_store_2d(&tmO, sb + C::oOst, hd * D, 16 * rw);
                     bulk_commit_group();
-                    if (F3S_TRACE_EV0 < 3) stamp(seq, 7);
+                    stamp(seq, 7);
                 }
                 ++item;
-                ++seq;
                 continue;
             }
-            const float4* a4 = reinterpret_cast<const float4*>(corr[b].alpha);
+            // merge factors of row ri: O = fa * O + fb * O_c
+            const float mc = corr[b].m[ri];
+            const float lc = (corr[b].lpart[0][ri] + corr[b].lpart[1][ri]) + (corr[b].lpart[2][ri] + corr[b].lpart[3][ri]);
+            float fa, fb;
+            if (flags & 1) {  // the item's first chunk: (m, l) = (m_c, l_c)
+                m_run = mc;
+                l_run = lc;
+                fa = 0.f;
+                fb = 1.f;
+            } else {
+                const float M = fmaxf(m_run, mc);
+                fa = ex2(m_run - M);
+                fb = ex2(mc - M);
+                l_run = fmaf(l_run, fa, lc * fb);
+                m_run = M;
+            }
             if (expt & 128) {  // diagnostics: the correction group only keeps the barrier protocol
                 tc_fence_before();
                 mbar_arrive(bar(B::pempty(b)));
-                if (flags & 2) {
-                    const int ib = item % C::kLB;
-                    mbar_wait(bar(B::lfull(ib)), (item / C::kLB) & 1);
-                    mbar_arrive(bar(B::lempty(ib)));
-                    ++item;
-                }
-                ++seq;
+                if (flags & 2) ++item;
                 continue;
             }
             if (rows > 0) {
                 float ov[16];
                 tmem_ld_32x32b_x16(tmem + tl + 16 * C::kSB + b * 16, ov);
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    const float4 a = a4[g];
-                    oacc[4 * g] = oacc[4 * g] * a.x + ov[4 * g];
-                    oacc[4 * g + 1] = oacc[4 * g + 1] * a.y + ov[4 * g + 1];
-                    oacc[4 * g + 2] = oacc[4 * g + 2] * a.z + ov[4 * g + 2];
-                    oacc[4 * g + 3] = oacc[4 * g + 3] * a.w + ov[4 * g + 3];
-                }
+                for (int i = 0; i < 16; ++i)
+                    oacc[i] = fmaf(oacc[i], __shfl_sync(0xffffffffu, fa, i), ov[i] * __shfl_sync(0xffffffffu, fb, i));
             } else {
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    const float4 a = a4[g];
-                    oacc[4 * g] *= a.x; oacc[4 * g + 1] *= a.y; oacc[4 * g + 2] *= a.z; oacc[4 * g + 3] *= a.w;
-                }
+                for (int i = 0; i < 16; ++i) oacc[i] *= __shfl_sync(0xffffffffu, fa, i);
             }
             tc_fence_before();
             mbar_arrive(bar(B::pempty(b)));
             if (lead) lap(2);
             if (flags & 2) {
-                // O_i = diag(l_o)^-1 O_i (l.24)
-                const int ib = item % C::kLB;
-                mbar_wait(bar(B::lfull(ib)), (item / C::kLB) & 1);
-                if (lead) lap(3);
-                const float4* l4 = reinterpret_cast<const float4*>(lred + ib * 64);
-                float inv[16];
-                auto row_sum = [&](int g, float (&lt)[4]) {  // l_o of rows 4g..4g+3: the 4 warps' partials
-                    const float4 a = l4[g], b4 = l4[4 + g], c = l4[8 + g], e = l4[12 + g];
-                    lt[0] = (a.x + b4.x) + (c.x + e.x);
-                    lt[1] = (a.y + b4.y) + (c.y + e.y);
-                    lt[2] = (a.z + b4.z) + (c.z + e.z);
-                    lt[3] = (a.w + b4.w) + (c.w + e.w);
-                };
+                // O_i = diag(l)^-1 O_i (l.24); empty row (l = 0) -> 0 (reading c4)
+                const float linv = l_run > 0.f ? rcp_approx(l_run) : 0.f;
+                float li[16];  // 1 / l of the 16 rows, broadcast to every lane (outside the lane-divergent stores)
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    float lt[4];
-                    row_sum(g, lt);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) inv[4 * g + u] = lt[u] > 0.f ? rcp_approx(lt[u]) : 0.f;  // empty row -> 0
-                }
+                for (int i = 0; i < 16; ++i) li[i] = __shfl_sync(0xffffffffu, linv, i);
                 const bool has = D == 128 || lane < 16;
                 const int f = D == 128 ? 32 * q + lane : 16 * q + lane;  // O^T lane -> feature (M = 64 layout)
-                bool do_store = true;
                 if (split) {
                     // piece of a split row window: leave (m, l, unnormalised O) in the scratch
                     // record of its global piece; k_split_merge combines the pieces after the
                     // kernel, in piece order (deterministic)
                     const int64_t rec_floats = 32 + 16 * D;
                     float* rec = scratch + ((int64_t)(split - 1) * H + hd) * rec_floats;
-                    if (lead) {
-                        const float* lm = reinterpret_cast<const float*>(smem + C::oLm + ib * 64);
-#pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            float lt[4];
-                            row_sum(g, lt);
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) { rec[4 * g + u] = lm[4 * g + u]; rec[16 + 4 * g + u] = lt[u]; }
-                        }
+                    if (q == 0 && lane < 16) {
+                        rec[lane] = m_run;
+                        rec[16 + lane] = l_run;
                     }
                     if (has) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) rec[32 + i * D + f] = oacc[i];
                     }
-                    do_store = false;
-                }
-                mbar_arrive(bar(B::lempty(ib)));
-                // O tile [16 x D] fp32 staged in shared memory and written by one TMA store (rows
-                // past n_rows of a ragged last window are clipped by the tensor map, reading c14)
-                const int ob = item % C::kNO;
-                float* ost = reinterpret_cast<float*>(smem + C::oOst + ob * C::kOBytes);
-                if (do_store) {
+                } else {
+                    // O tile [16 x D] fp32 staged in shared memory and written by one TMA store
+                    // (rows past n_rows of a ragged last window are clipped by the tensor map, c14)
+                    const int ob = item % C::kNO;
+                    float* ost = reinterpret_cast<float*>(smem + C::oOst + ob * C::kOBytes);
                     if (threadIdx.x == 32 * C::kCorr0) bulk_wait_group_read<C::kNO - 1>();  // staging tile ob free
                     named_bar_sync(1 + C::kSoftmaxWGs, 128);
                     if (has) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) ost[i * D + f] = oacc[i] * inv[i];
+                        for (int i = 0; i < 16; ++i) ost[i * D + f] = oacc[i] * li[i];
                     }
                     fence_proxy_async_smem();
                     named_bar_sync(1 + C::kSoftmaxWGs, 128);
@@ -955,10 +857,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) oacc[i] = 0.f;
-                if (lead) { if (F3S_TRACE_EV0 < 3) stamp(seq, 7); lap(4); }
+                if (lead) { stamp(seq, 7); lap(3); }
                 ++item;
             }
-            ++seq;
         }
         if (threadIdx.x == 32 * C::kCorr0) bulk_wait_group<0>();
     }
@@ -1074,8 +975,6 @@ f3s_status make_map(CUtensorMap* map, const void* base, f3s_dtype dtype, int64_t
                     inner, rows, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-std::atomic<uint32_t> g_call{0};
-
 template <int D, typename T, int HG>
 f3s_status launch(const AttnArgs& a) {
     using C = Cfg<D, HG, (int)sizeof(T)>;
@@ -1085,33 +984,34 @@ f3s_status launch(const AttnArgs& a) {
         F3S_CUDA_TRY(cudaMemsetAsync(a.O, 0, (size_t)out_bytes, a.stream));
         return F3S_OK;
     }
-    CUtensorMap mq, mk, mv, mo;
+    CUtensorMap mq, mo;
     f3s_status st;
     if ((st = make_map(&mq, a.Q, a.dtype, (int64_t)a.heads * D, p.n_rows, 16)) != F3S_OK) return st;
-    if ((st = make_map(&mk, a.K, a.dtype, (int64_t)a.heads * D, p.n_cols, 1)) != F3S_OK) return st;
-    if ((st = make_map(&mv, a.V, a.dtype, (int64_t)a.heads * D, p.n_cols, 1)) != F3S_OK) return st;
     if ((st = make_map(&mo, a.O, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (int64_t)a.heads * D, p.n_rows, D * HG, 16,
                        CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK)
         return st;
 
-    static int num_sms[64] = {0};
+    // per-device launch state: SM count and the raised dynamic shared-memory limit (a function
+    // attribute is per device, so it is set once on every device the library launches on)
+    static std::atomic<int> num_sms[64];
+    static std::atomic<uint64_t> attr_set{0};
+    static std::mutex attr_mu;
     const int dev = p.device;
-    if (dev < 64 && num_sms[dev] == 0) {
-        int v = 0;
-        F3S_CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
-        num_sms[dev] = v;
+    if (dev < 0 || dev >= 64) { set_error("device ordinal >= 64"); return F3S_ERR_UNSUPPORTED; }
+    if (!(attr_set.load() >> dev & 1)) {
+        std::lock_guard<std::mutex> lock(attr_mu);
+        if (!(attr_set.load() >> dev & 1)) {
+            int v = 0;
+            F3S_CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+            num_sms[dev].store(v);
+            F3S_CUDA_TRY(cudaFuncSetAttribute(k_f3s_sm100<D, T, false, HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              C::kSmemBytes));
+            F3S_CUDA_TRY(cudaFuncSetAttribute(k_f3s_sm100<D, T, true, HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              C::kSmemBytes));
+            attr_set.fetch_or(uint64_t(1) << dev);
+        }
     }
-    const int sms = dev < 64 ? num_sms[dev] : 148;
-    static std::once_flag attr_once;
-    cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [&] {
-        attr_err = cudaFuncSetAttribute(k_f3s_sm100<D, T, false, HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        C::kSmemBytes);
-        if (attr_err == cudaSuccess)
-            attr_err = cudaFuncSetAttribute(k_f3s_sm100<D, T, true, HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            C::kSmemBytes);
-    });
-    F3S_CUDA_TRY(attr_err);
+    const int sms = num_sms[dev].load();
     // default variant: the LPT list with heavy row windows split into pieces (Plan::meta_sub)
     const bool split = a.lpt && p.n_groups > 0;
     if (split && HG > 1) { set_error("internal: head groups with split windows"); return F3S_ERR_INTERNAL; }
@@ -1119,48 +1019,48 @@ f3s_status launch(const AttnArgs& a) {
     if (n_items64 > 0x7FFFFFFF) { set_error("too many work items"); return F3S_ERR_UNSUPPORTED; }
     const int32_t n_items = (int32_t)n_items64;
     const int grid = a.grid_override > 0 ? a.grid_override : (int)std::min<int64_t>(n_items, (int64_t)sms * C::kCtasPerSm);
-    // compacted columns per chunk: smaller chunks keep more tiles in flight in the ring
-    int chunk_rows = 128;
-    if (const char* env = getenv("F3S_CHUNK_ROWS"))
-        if (HG == 1) chunk_rows = std::max(16, std::min(128, atoi(env) / 16 * 16));  // (HG > 1: one chunk per item)
-    int32_t* counter = p.counters + (g_call.fetch_add(1) % kNumCounterSlots);
-    F3S_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int32_t), a.stream));
-    auto kern = a.trace ? k_f3s_sm100<D, T, true, HG> : k_f3s_sm100<D, T, false, HG>;
-    // split pieces: per-call scratch (a stream-ordered allocation, so concurrent calls on other
-    // streams never share it): one (m[16], l[16], O[16][D]) fp32 record per piece and head
-    float* scratch = nullptr;
-    if (split)
-        F3S_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                                     sizeof(float) * (size_t)p.n_pieces * a.heads * (32 + 16 * D), a.stream));
-    kern<<<grid, C::kThreads, C::kSmemBytes, a.stream>>>(
-        mq, mk, mv, mo, a.lpt ? p.meta_sub : p.meta_nat, p.kcols, p.kmasks, counter,
-        n_items, a.heads, p.n_rows, chunk_rows, static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.O,
-        a.scale * 1.4426950408889634f, a.trace, a.trace_chunks, a.expt, scratch);
-    count_launch();
-    F3S_CUDA_TRY(cudaGetLastError());
-    if (split) {
-        k_split_merge<D><<<(int)((int64_t)p.n_groups * a.heads), 256, 0, a.stream>>>(p.ginfo, scratch, a.O, a.heads,
-                                                                                     p.n_rows);
+    // per-call scratch, stream-ordered (so calls in flight on other streams, or replays of a
+    // captured graph, never share it): the work-queue counter, then for split plans one
+    // (m[16], l[16], O[16][D]) fp32 record per piece and head
+    const size_t rec_bytes = split ? sizeof(float) * (size_t)p.n_pieces * a.heads * (32 + 16 * D) : 0;
+    char* scratch = nullptr;
+    F3S_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&scratch), 256 + rec_bytes, a.stream));
+    int32_t* counter = reinterpret_cast<int32_t*>(scratch);
+    cudaError_t err = cudaMemsetAsync(counter, 0, sizeof(int32_t), a.stream);
+    if (err == cudaSuccess) {
+        auto kern = (a.trace || a.expt) ? k_f3s_sm100<D, T, true, HG> : k_f3s_sm100<D, T, false, HG>;
+        kern<<<grid, C::kThreads, C::kSmemBytes, a.stream>>>(
+            mq, mo, a.lpt ? p.meta_sub : p.meta_nat, p.kcols, p.kmasks, counter, n_items, a.heads,
+            (a.kv_ld > 0 ? a.kv_ld : (int64_t)a.heads * D) * (int64_t)sizeof(T),
+            static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.scale * 1.4426950408889634f, a.trace,
+            a.trace_chunks, a.expt, split ? reinterpret_cast<float*>(scratch + 256) : nullptr);
         count_launch();
-        F3S_CUDA_TRY(cudaGetLastError());
-        F3S_CUDA_TRY(cudaFreeAsync(scratch, a.stream));
+        err = cudaGetLastError();
     }
+    if (err == cudaSuccess && split) {
+        k_split_merge<D><<<(int)((int64_t)p.n_groups * a.heads), 256, 0, a.stream>>>(
+            p.ginfo, reinterpret_cast<const float*>(scratch + 256), a.O, a.heads, p.n_rows);
+        count_launch();
+        err = cudaGetLastError();
+    }
+    const cudaError_t ferr = scratch_free(scratch, a.stream);
+    F3S_CUDA_TRY(err);
+    F3S_CUDA_TRY(ferr);
     return F3S_OK;
 }
 
 }  // namespace
 
 f3s_status launch_attention_sm100(const AttnArgs& a) {
-    // head groups of 4 when every row window fits one 32-column block (d = 64): the per-chunk
-    // pipeline cost is shared by 4 heads (batched small graphs).  F3S_HG1=1 forces HG = 1.
-    static const bool hg1 = getenv("F3S_HG1") != nullptr;
     const Plan& p = *a.plan;
     if (a.dtype == F3S_E4M3) {
         // d = 64: the Q box (128 elements) also covers the next head's 64 (zero-filled past the
         // last head by the tensor map); MMA1 reads only the first 64 bytes of each row
         return a.d == 128 ? launch<128, __nv_fp8_e4m3, 1>(a) : launch<64, __nv_fp8_e4m3, 1>(a);
     }
-    const bool hg4 = !hg1 && !a.one_head && a.d == 64 && a.heads % 4 == 0 && p.max_width <= 32 && p.n_groups == 0;
+    // head groups of 4 when every row window fits one 32-column block (d = 64): the per-chunk
+    // pipeline cost is shared by 4 heads (batched small graphs)
+    const bool hg4 = !a.one_head && a.d == 64 && a.heads % 4 == 0 && p.max_width <= 32 && p.n_groups == 0;
     if (a.dtype == F3S_FP16) {
         if (hg4) return launch<64, __half, 4>(a);
         return a.d == 64 ? launch<64, __half, 1>(a) : launch<128, __half, 1>(a);

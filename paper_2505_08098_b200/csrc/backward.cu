@@ -351,10 +351,11 @@ int grid_for(int64_t n, int block) {
 struct Scratch {
     void* p = nullptr;
     cudaStream_t s = nullptr;
-    ~Scratch() { if (p) cudaFreeAsync(p, s); }
+    ~Scratch() { if (p) scratch_free(p, s); }
 };
 
 f3s_status build_transpose(Plan& p, cudaStream_t stream) {
+    std::lock_guard<std::mutex> lock(p.transpose_mu);  // concurrent first backward calls build it once
     if (p.col_ptr) return F3S_OK;
     const int64_t W = p.total_cols, nnz = p.nnz;
     int32_t *col_ptr = nullptr, *col_rows = nullptr;
@@ -362,11 +363,11 @@ f3s_status build_transpose(Plan& p, cudaStream_t stream) {
     F3S_CUDA_TRY(cudaMalloc(&col_rows, sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1)));
     Scratch pop, off, cnt, keys, keys2, tmp;
     pop.s = off.s = cnt.s = keys.s = keys2.s = tmp.s = stream;
-    F3S_CUDA_TRY(cudaMallocAsync(&pop.p, sizeof(int32_t) * (size_t)std::max<int64_t>(W, 1), stream));
-    F3S_CUDA_TRY(cudaMallocAsync(&off.p, sizeof(int32_t) * (size_t)std::max<int64_t>(W, 1), stream));
-    F3S_CUDA_TRY(cudaMallocAsync(&cnt.p, sizeof(int32_t) * ((size_t)p.n_cols + 1), stream));
-    F3S_CUDA_TRY(cudaMallocAsync(&keys.p, sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1), stream));
-    F3S_CUDA_TRY(cudaMallocAsync(&keys2.p, sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1), stream));
+    F3S_CUDA_TRY(scratch_alloc(&pop.p, sizeof(int32_t) * (size_t)std::max<int64_t>(W, 1), stream));
+    F3S_CUDA_TRY(scratch_alloc(&off.p, sizeof(int32_t) * (size_t)std::max<int64_t>(W, 1), stream));
+    F3S_CUDA_TRY(scratch_alloc(&cnt.p, sizeof(int32_t) * ((size_t)p.n_cols + 1), stream));
+    F3S_CUDA_TRY(scratch_alloc(&keys.p, sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1), stream));
+    F3S_CUDA_TRY(scratch_alloc(&keys2.p, sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1), stream));
     F3S_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * ((size_t)p.n_cols + 1), stream));
     if (W > 0) {
         k_entry_pop<<<grid_for(W, 256), 256, 0, stream>>>(p.cols, p.masks, W, (int32_t*)pop.p, (int32_t*)cnt.p);
@@ -377,7 +378,7 @@ f3s_status build_transpose(Plan& p, cudaStream_t stream) {
     F3S_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb_scan2, (int32_t*)cnt.p, col_ptr, (int64_t)p.n_cols + 1, stream));
     cub::DoubleBuffer<uint64_t> db((uint64_t*)keys.p, (uint64_t*)keys2.p);
     F3S_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb_sort, db, nnz, 0, 64, stream));
-    F3S_CUDA_TRY(cudaMallocAsync(&tmp.p, std::max(std::max(tb_scan, tb_scan2), tb_sort) + 16, stream));
+    F3S_CUDA_TRY(scratch_alloc(&tmp.p, std::max(std::max(tb_scan, tb_scan2), tb_sort) + 16, stream));
     const size_t tbmax = std::max(std::max(tb_scan, tb_scan2), tb_sort) + 16;
     size_t tb = tbmax;
     if (W > 0) F3S_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tb, (int32_t*)pop.p, (int32_t*)off.p, W, stream));
@@ -420,7 +421,7 @@ f3s_status build_transpose(Plan& p, cudaStream_t stream) {
     {
         Scratch degs;
         degs.s = stream;
-        F3S_CUDA_TRY(cudaMallocAsync(&degs.p, sizeof(int32_t) * h_deg.size() + 16, stream));
+        F3S_CUDA_TRY(scratch_alloc(&degs.p, sizeof(int32_t) * h_deg.size() + 16, stream));
         k_row_deg<<<grid_for((int64_t)p.num_rw * 16, 256), 256, 0, stream>>>(p.rw_ptr, p.num_rw, p.masks,
                                                                              (int32_t*)degs.p);
         count_launch();
@@ -465,7 +466,7 @@ f3s_status launch_bwd(Plan& p, const void* Q, const void* K, const void* V, cons
     if (st != F3S_OK) return st;
     Scratch stats;
     stats.s = stream;
-    F3S_CUDA_TRY(cudaMallocAsync(&stats.p, sizeof(float) * 2 * (size_t)p.n_rows * H, stream));
+    F3S_CUDA_TRY(scratch_alloc(&stats.p, sizeof(float) * 2 * (size_t)p.n_rows * H, stream));
     float* lse = (float*)stats.p;
     float* drow = lse + (size_t)p.n_rows * H;
     const int64_t blocks = (int64_t)p.num_rw * H;

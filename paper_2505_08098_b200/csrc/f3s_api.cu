@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <new>
+#include <mutex>
 #include <string>
 
 #include "internal.h"
@@ -16,6 +17,34 @@ static std::atomic<int64_t> g_launches{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t stream) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!pools[dev]) {
+            cudaMemPoolProps props = {};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            cudaMemPool_t np = nullptr;
+            if ((e = cudaMemPoolCreate(&np, &props)) != cudaSuccess) return e;
+            uint64_t keep = uint64_t(256) << 20;  // keep up to 256 MB reserved across synchronisations
+            if ((e = cudaMemPoolSetAttribute(np, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) return e;
+            pools[dev] = np;
+        }
+        pool = pools[dev];
+    }
+    return cudaMallocFromPoolAsync(ptr, bytes ? bytes : 16, pool, stream);
+}
+
+cudaError_t scratch_free(void* ptr, cudaStream_t stream) { return ptr ? cudaFreeAsync(ptr, stream) : cudaSuccess; }
 
 f3s_status cuda_fail(cudaError_t e, const char* what) {
     g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
@@ -48,11 +77,21 @@ static f3s_status check_attention_args(f3s_plan_t plan, const void* Q, const voi
 
 static f3s_status run_attention(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
                                 int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, cudaStream_t stream,
-                                uint64_t* trace = nullptr, int32_t trace_chunks = 0, int32_t grid = 0) {
+                                uint64_t* trace = nullptr, int32_t trace_chunks = 0, int32_t grid = 0,
+                                int64_t kv_ld = 0) {
     f3s_status st = check_attention_args(plan, Q, K, V, O, scale, heads, d, dtype, true);
     if (st != F3S_OK) return st;
+    if (kv_ld != 0) {
+        if (kv_ld < (int64_t)heads * d) { set_error("kv_row_stride < heads * d"); return F3S_ERR_INVALID_VALUE; }
+        if ((kv_ld * (dtype == F3S_E4M3 ? 1 : 2)) % 16 != 0) {
+            set_error("kv_row_stride must be a multiple of 16 bytes");
+            return F3S_ERR_UNSUPPORTED;
+        }
+        if (variant == F3S_VARIANT_SIMT) { set_error("kv_row_stride: tcgen05 variants only"); return F3S_ERR_UNSUPPORTED; }
+    }
     AttnArgs a{reinterpret_cast<const Plan*>(plan), Q, K, V, O, scale, heads, d, dtype,
                variant != F3S_VARIANT_NO_REORDER, stream};
+    a.kv_ld = kv_ld;
     a.trace = trace_chunks < 0 ? nullptr : trace;
     a.trace_chunks = trace_chunks < 0 ? 0 : trace_chunks;
     a.expt = trace_chunks < 0 ? -trace_chunks : 0;
@@ -63,6 +102,9 @@ static f3s_status run_attention(f3s_plan_t plan, const void* Q, const void* K, c
         set_error("F3S_E4M3: DEFAULT and NO_REORDER variants only");
         return F3S_ERR_UNSUPPORTED;
     }
+    // launch on the plan's device whatever the calling thread's current device is
+    DeviceScope scope;
+    F3S_CUDA_TRY(scope.enter(a.plan->device));
     switch (variant) {
         case F3S_VARIANT_DEFAULT:
         case F3S_VARIANT_NO_REORDER:
@@ -119,7 +161,6 @@ f3s_status f3s_plan_destroy(f3s_plan_t plan) {
     cudaFree(p->masks);
     cudaFree(p->rw_order);
     cudaFree(p->rw_natural);
-    cudaFree(p->counters);
     cudaFree(p->kcols);
     cudaFree(p->kmasks);
     cudaFree(p->meta_lpt);
@@ -138,9 +179,21 @@ f3s_status f3s_plan_destroy(f3s_plan_t plan) {
 
 f3s_status f3s_plan_set_split(f3s_plan_t plan, int32_t max_chunks) {
     if (!plan) { set_error("plan is NULL"); return F3S_ERR_INVALID_VALUE; }
-    Plan* p = reinterpret_cast<Plan*>(plan);
-    F3S_CUDA_TRY(cudaSetDevice(p->device));
-    return build_split(p, max_chunks);
+    try {
+        Plan* p = reinterpret_cast<Plan*>(plan);
+        DeviceScope scope;
+        F3S_CUDA_TRY(scope.enter(p->device));
+        return build_split(p, max_chunks);
+    } catch (const std::bad_alloc&) {
+        return F3S_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+int32_t f3s_default_split_chunks(int64_t total_chunks, int32_t num_sms) {
+    return default_split_chunks(total_chunks, num_sms);
 }
 
 f3s_status f3s_plan_get_info(f3s_plan_t plan, f3s_plan_info* info) {
@@ -158,6 +211,7 @@ f3s_status f3s_plan_get_info(f3s_plan_t plan, f3s_plan_info* info) {
     info->build_ms = p.build_ms;
     info->split_chunks = p.split_chunks;
     info->split_groups = p.n_groups;
+    info->total_chunks = p.total_chunks;
     return F3S_OK;
 }
 
@@ -193,8 +247,20 @@ f3s_status f3s_attention_backward(f3s_plan_t plan, const void* Q, const void* K,
         if (p.n_cols > 0 && (!dK || !dV)) { set_error("dK/dV is NULL"); return F3S_ERR_INVALID_VALUE; }
         auto mis = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) != 0; };
         if (mis(dO) || mis(dK) || mis(dV)) { set_error("dO/dK/dV must be 16-byte aligned"); return F3S_ERR_UNSUPPORTED; }
-        F3S_CUDA_TRY(cudaSetDevice(p.device));
+        DeviceScope scope;
+        F3S_CUDA_TRY(scope.enter(p.device));
         return launch_attention_backward(p, Q, K, V, dO, dQ, dK, dV, scale, heads, d, dtype, stream);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_kv(f3s_plan_t plan, const void* Q, const void* K, const void* V, int64_t kv_row_stride,
+                            float* O, float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
+    try {
+        return run_attention(plan, Q, K, V, O, scale, heads, d, dtype, F3S_VARIANT_DEFAULT, stream, nullptr, 0, 0,
+                             kv_row_stride);
     } catch (...) {
         set_error("internal error");
         return F3S_ERR_INTERNAL;
@@ -223,11 +289,13 @@ f3s_status f3s_attention_trace(f3s_plan_t plan, const void* Q, const void* K, co
     }
 }
 
-f3s_status f3s_attention_host_async(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O,
-                                    float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
+static f3s_status attention_host_async_impl(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O,
+                                            float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
     f3s_status st = check_attention_args(plan, Q, K, V, O, scale, heads, d, dtype, false);
     if (st != F3S_OK) return st;
     Plan& p = *reinterpret_cast<Plan*>(plan);
+    DeviceScope scope;
+    F3S_CUDA_TRY(scope.enter(p.device));
     size_t qn = (size_t)p.n_rows * heads * d, kn = (size_t)p.n_cols * heads * d;
     auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t es = dtype == F3S_E4M3 ? 1 : 2;  // bytes per input element
@@ -269,6 +337,18 @@ f3s_status f3s_attention_host_async(f3s_plan_t plan, const void* Q, const void* 
     if (st != F3S_OK) return st;
     if (qn) F3S_CUDA_TRY(cudaMemcpyAsync(O, dO, qn / es * 4, cudaMemcpyDeviceToHost, stream));
     return F3S_OK;
+}
+
+f3s_status f3s_attention_host_async(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O,
+                                    float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
+    try {
+        return attention_host_async_impl(plan, Q, K, V, O, scale, heads, d, dtype, stream);
+    } catch (const std::bad_alloc&) {
+        return F3S_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
 }
 
 f3s_status f3s_attention_host(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -32,13 +33,13 @@ struct Plan {
     uint16_t* kmasks = nullptr;   // [W8]
     int4* meta_lpt = nullptr;     // [R] {k, start8, width, 0} in LPT order
     int4* meta_nat = nullptr;     // [R] same, natural order (no-reorder ablation)
-    int32_t* counters = nullptr;  // work-queue counters, kNumCounterSlots
     // heavy row-window split: the default kernel walks
     // meta_sub, the LPT list with every window of more than split_chunks 128-column chunks cut
     // into pieces of split_chunks chunks (meta_sub[i].w = 1 + global piece index, 0 for an
     // unsplit window); each piece leaves (m, l, O) partials and k_split_merge combines the
     // pieces of split window g, in piece order (ginfo[g] = {first global piece, pieces, k, 0})
     int32_t split_chunks = 0, n_sub = 0, n_groups = 0, n_pieces = 0;
+    int64_t total_chunks = 0;     // sum over windows of max(1, ceil(w / 128)): one head's kernel chunks
     int4* meta_sub = nullptr;     // [n_sub]
     int4* ginfo = nullptr;        // [n_groups]
     std::vector<int32_t> h_rw, h_rw8, h_order;  // host copies used to (re)build meta_sub
@@ -60,9 +61,34 @@ struct Plan {
     };
     std::mutex staging_mu;
     std::vector<Staging> staging;
+    std::mutex transpose_mu;  // the backward's transposed index is built once, under this lock
 };
 
-constexpr int kNumCounterSlots = 64;
+// Switch the calling thread to `dev` for the scope of a call and restore its device after.
+struct DeviceScope {
+    int prev = -1;
+    cudaError_t enter(int dev) {
+        cudaError_t e = cudaGetDevice(&prev);
+        if (e != cudaSuccess) { prev = -1; return e; }
+        if (prev == dev) { prev = -1; return cudaSuccess; }
+        return cudaSetDevice(dev);
+    }
+    ~DeviceScope() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+// Default heavy-window split bound (f3s.h, f3s_plan_set_split): a window is cut into pieces
+// when it alone exceeds half of an SM's even share of all chunks of the (global) problem.
+inline int32_t default_split_chunks(int64_t total_chunks, int32_t num_sms) {
+    const int64_t sms = num_sms > 0 ? num_sms : 148;
+    const int64_t t = std::max<int64_t>(16, (total_chunks + 2 * sms - 1) / (2 * sms));
+    return (int32_t)std::min<int64_t>(t, 0x7FFFFFFF);
+}
+
+// Stream-ordered per-call scratch from the library's own memory pool on the current device
+// (release threshold 256 MB, so steady-state calls reuse pool memory instead of mapping new
+// pages at every call; a pool of its own leaves the caller's default-pool settings alone).
+cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t stream);
+cudaError_t scratch_free(void* ptr, cudaStream_t stream);
 
 // error reporting (thread-local detail)
 void set_error(const std::string& msg);
@@ -88,6 +114,7 @@ struct AttnArgs {
     int32_t grid_override = 0;
     int32_t expt = 0;           // sensitivity experiments (diagnostics only)
     bool one_head = false;      // F3S_VARIANT_ONE_HEAD: no head groups
+    int64_t kv_ld = 0;          // elements between consecutive K (and V) rows; 0 = heads * d
 };
 
 f3s_status launch_attention_sm100(const AttnArgs& a);

@@ -137,7 +137,7 @@ f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_
     if (!plan) return F3S_ERR_OUT_OF_MEMORY;
     struct Guard { Plan*& p; bool ok = false; ~Guard() { if (!ok && p) {
         cudaFree(p->rw_ptr); cudaFree(p->cols); cudaFree(p->masks); cudaFree(p->rw_order);
-        cudaFree(p->rw_natural); cudaFree(p->counters); cudaFree(p->kcols); cudaFree(p->kmasks);
+        cudaFree(p->rw_natural); cudaFree(p->kcols); cudaFree(p->kmasks);
         cudaFree(p->meta_lpt); cudaFree(p->meta_nat); cudaFree(p->meta_sub); cudaFree(p->ginfo); cudaFree(p->col_ptr); cudaFree(p->col_rows); cudaFree(p->col_lists); cudaFree(p->heavy_rows); cudaFree(p->heavy_row_flag); delete p; p = nullptr; } } } guard{plan};
     F3S_CUDA_TRY(cudaGetDevice(&plan->device));
     const int32_t R = (n_rows + kRowsPerWindow - 1) / kRowsPerWindow;
@@ -231,8 +231,6 @@ f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_
     F3S_CUDA_TRY(cudaMalloc(&plan->rw_ptr, sizeof(int32_t) * (size_t)(R + 1)));
     F3S_CUDA_TRY(cudaMalloc(&plan->rw_order, sizeof(int32_t) * (size_t)std::max(R, 1)));
     F3S_CUDA_TRY(cudaMalloc(&plan->rw_natural, sizeof(int32_t) * (size_t)std::max(R, 1)));
-    F3S_CUDA_TRY(cudaMalloc(&plan->counters, sizeof(int32_t) * kNumCounterSlots));
-    F3S_CUDA_TRY(cudaMemsetAsync(plan->counters, 0, sizeof(int32_t) * kNumCounterSlots, stream));
     {
         size_t tb_scan = 0;
         F3S_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb_scan, widths.as<int32_t>(), plan->rw_ptr, R + 1, stream));
@@ -314,20 +312,22 @@ f3s_status build_plan(const int32_t* row_ptr, const int32_t* col_idx, int32_t n_
     F3S_CUDA_TRY(cudaStreamSynchronize(stream));
     {
         // default: a window is split when it alone exceeds half of an SM's even share of all
-        // chunks (counted for one head; more heads only make the share larger)
+        // chunks (counted for one head; more heads only make the share larger).  A row-shard
+        // plan counts only its own chunks; multi-GPU callers reset the bound from the global
+        // count (f3s_default_split_chunks + f3s_plan_set_split) so shards split like the 1-GPU plan.
         int64_t chunks = 0;
         for (int32_t k = 0; k < R; ++k)
             chunks += std::max<int64_t>(1, (plan->h_rw[k + 1] - plan->h_rw[k] + kSplitChunkCols - 1) / kSplitChunkCols);
+        plan->total_chunks = chunks;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
-        const int64_t t = std::max<int64_t>(16, (chunks + 2 * sms - 1) / (2 * (int64_t)sms));
-        f3s_status st = build_split(plan, (int32_t)std::min<int64_t>(t, 0x7FFFFFFF));
+        f3s_status st = build_split(plan, default_split_chunks(chunks, sms));
         if (st != F3S_OK) return st;
     }
     F3S_CUDA_TRY(cudaEventRecord(ev1, stream));
     F3S_CUDA_TRY(cudaStreamSynchronize(stream));  // the plan is complete when f3s_plan returns
     F3S_CUDA_TRY(cudaEventElapsedTime(&plan->build_ms, ev0, ev1));
-    plan->device_bytes = (int64_t)sizeof(int32_t) * (2 * R + 1 + R + kNumCounterSlots) + (int64_t)sizeof(int4) * 2 * R +
+    plan->device_bytes = (int64_t)sizeof(int32_t) * (2 * R + 1 + R) + (int64_t)sizeof(int4) * 2 * R +
                          (int64_t)(sizeof(int32_t) + sizeof(uint16_t)) * (std::max<int64_t>(W, 1) + h_w8);
     guard.ok = true;
     *out = plan;
@@ -355,16 +355,20 @@ f3s_status build_split(Plan* p, int32_t chunks) {
         }
         ++groups;
     }
+    // build the new lists completely before swapping them in: on failure the plan keeps its
+    // previous (consistent) split
+    DevBuf nmeta, ninfo;
+    F3S_CUDA_TRY(nmeta.alloc(sizeof(int4) * std::max<size_t>(meta.size(), 1)));
+    F3S_CUDA_TRY(ninfo.alloc(sizeof(int4) * std::max<size_t>(info.size(), 1)));
+    if (!meta.empty())
+        F3S_CUDA_TRY(cudaMemcpy(nmeta.p, meta.data(), sizeof(int4) * meta.size(), cudaMemcpyHostToDevice));
+    if (!info.empty())
+        F3S_CUDA_TRY(cudaMemcpy(ninfo.p, info.data(), sizeof(int4) * info.size(), cudaMemcpyHostToDevice));
     cudaFree(p->meta_sub);
     cudaFree(p->ginfo);
-    p->meta_sub = nullptr;
-    p->ginfo = nullptr;
-    F3S_CUDA_TRY(cudaMalloc(&p->meta_sub, sizeof(int4) * std::max<size_t>(meta.size(), 1)));
-    F3S_CUDA_TRY(cudaMalloc(&p->ginfo, sizeof(int4) * std::max<size_t>(info.size(), 1)));
-    if (!meta.empty())
-        F3S_CUDA_TRY(cudaMemcpy(p->meta_sub, meta.data(), sizeof(int4) * meta.size(), cudaMemcpyHostToDevice));
-    if (!info.empty())
-        F3S_CUDA_TRY(cudaMemcpy(p->ginfo, info.data(), sizeof(int4) * info.size(), cudaMemcpyHostToDevice));
+    p->meta_sub = nmeta.as<int4>();
+    p->ginfo = ninfo.as<int4>();
+    nmeta.p = ninfo.p = nullptr;
     p->split_chunks = chunks;
     p->n_sub = (int32_t)meta.size();
     p->n_groups = groups;

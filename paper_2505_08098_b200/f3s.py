@@ -32,7 +32,8 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("n_rows", ctypes.c_int32), ("n_cols", ctypes.c_int32), ("num_rw", ctypes.c_int32),
                 ("max_width", ctypes.c_int32), ("nnz", ctypes.c_int64), ("total_cols", ctypes.c_int64),
                 ("total_tcb8", ctypes.c_int64), ("device_bytes", ctypes.c_int64), ("build_ms", ctypes.c_float),
-                ("reserved", ctypes.c_float), ("split_chunks", ctypes.c_int32), ("split_groups", ctypes.c_int32)]
+                ("reserved", ctypes.c_float), ("split_chunks", ctypes.c_int32), ("split_groups", ctypes.c_int32),
+                ("total_chunks", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -46,6 +47,7 @@ _lib.f3s_plan_get_info.argtypes = [_vp, ctypes.POINTER(PlanInfo)]
 _lib.f3s_plan_export.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.f3s_plan_set_split.argtypes = [_vp, _i32]
 _lib.f3s_attention.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_kv.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_trace.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]
 _lib.f3s_attention_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
@@ -53,18 +55,21 @@ _lib.f3s_attention_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _
 _lib.f3s_attention_host_async.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_partition_rows.argtypes = [_vp, _i32, _i32, _vp]
 _lib.f3s_partition_at.argtypes = [_vp, _i32, _vp, _i32, _i32, _vp]
+_lib.f3s_default_split_chunks.argtypes = [_i64, _i32]
+_lib.f3s_default_split_chunks.restype = _i32
 _lib.f3s_status_string.argtypes = [_i32]
 _lib.f3s_status_string.restype = ctypes.c_char_p
 _lib.f3s_last_error.restype = ctypes.c_char_p
 _lib.f3s_launch_count.restype = _i64
 for _name in ("f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
-              "f3s_attention", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows",
+              "f3s_attention", "f3s_attention_kv", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows",
               "f3s_partition_at", "f3s_attention_backward", "f3s_attention_host_async"):
     getattr(_lib, _name).restype = _i32
 
 EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
-            "f3s_attention", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows", "f3s_partition_at",
-            "f3s_attention_backward", "f3s_attention_host_async",
+            "f3s_attention", "f3s_attention_kv", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host",
+            "f3s_partition_rows", "f3s_partition_at",
+            "f3s_attention_backward", "f3s_attention_host_async", "f3s_default_split_chunks",
             "f3s_status_string", "f3s_last_error", "f3s_launch_count"]
 
 
@@ -96,6 +101,43 @@ def _dtype_code(t) -> int:
     if t.dtype == torch.float8_e4m3fn:
         return E4M3
     raise TypeError(f"Q/K/V must be float16, bfloat16 or float8_e4m3fn, got {t.dtype}")
+
+
+def _check_tensors(p: "Plan", Q, K, V, O=None, *, out_dtype=None, what="f3s_attention", strided_kv=False):
+    """The C ABI sees raw pointers only: check here that the tensors match the plan and each
+    other (device, contiguity, dtype, [rows, H, d] shapes) before any pointer crosses it."""
+    import torch
+    inf = p.info()
+    for name, t in (("Q", Q), ("K", K), ("V", V)):
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{what}: {name} must be a torch.Tensor")
+        if not t.is_cuda:
+            raise ValueError(f"{what}: {name} must be a CUDA tensor")
+        if not t.is_contiguous() and not (strided_kv and name != "Q"):
+            raise ValueError(f"{what}: {name} must be contiguous")
+        if t.dim() != 3:
+            raise ValueError(f"{what}: {name} must be [rows, heads, d], got shape {tuple(t.shape)}")
+    if not (K.dtype == V.dtype == Q.dtype):
+        raise ValueError(f"{what}: Q, K, V dtypes differ ({Q.dtype}, {K.dtype}, {V.dtype})")
+    if not (K.device == V.device == Q.device):
+        raise ValueError(f"{what}: Q, K, V on different devices")
+    H, d = Q.shape[1], Q.shape[2]
+    if tuple(K.shape[1:]) != (H, d) or tuple(V.shape[1:]) != (H, d):
+        raise ValueError(f"{what}: K/V heads and d must match Q's ({H}, {d})")
+    if Q.shape[0] != inf["n_rows"]:
+        raise ValueError(f"{what}: Q has {Q.shape[0]} rows, the plan {inf['n_rows']}")
+    if K.shape[0] < inf["n_cols"] or V.shape[0] < inf["n_cols"]:
+        raise ValueError(f"{what}: K/V need at least n_cols = {inf['n_cols']} rows")
+    if O is not None:
+        if not O.is_cuda or not O.is_contiguous() or O.device != Q.device:
+            raise ValueError(f"{what}: O must be a contiguous CUDA tensor on Q's device")
+        if O.dtype != (out_dtype or torch.float32) or tuple(O.shape) != tuple(Q.shape):
+            raise ValueError(f"{what}: O must be float32 of shape {tuple(Q.shape)}")
+
+
+def default_split_chunks(total_chunks: int, num_sms: int) -> int:
+    """f3s_default_split_chunks: the heavy-window split bound for a problem of total_chunks chunks."""
+    return int(_lib.f3s_default_split_chunks(int(total_chunks), int(num_sms)))
 
 
 class Plan:
@@ -161,6 +203,7 @@ def plan_rows(row_ptr, col_idx, n_rows: int, n_cols: int, stream=None) -> Plan:
 def attention(p: Plan, Q, K, V, O=None, *, scale: float = 1.0, variant: str | int = "default", stream=None):
     """f3s_attention(_ex) on device tensors Q [n_rows,H,d], K/V [n_cols,H,d] (fp16/bf16); O float32."""
     import torch
+    _check_tensors(p, Q, K, V, O)
     H, d = Q.shape[1], Q.shape[2]
     if O is None:
         O = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
@@ -169,6 +212,29 @@ def attention(p: Plan, Q, K, V, O=None, *, scale: float = 1.0, variant: str | in
                                _dtype_code(Q), v, _stream(stream))
     _check(st, "f3s_attention")
     return O
+
+
+def attention_kv(p: Plan, Q, KV, O=None, *, scale: float = 1.0, stream=None):
+    """f3s_attention_kv on an interleaved [n_cols, 2, H, d] buffer (K = KV[:, 0], V = KV[:, 1]),
+    the layout one all-gather of [K || V] shards produces."""
+    import torch
+    if KV.dim() != 4 or KV.shape[1] != 2 or not KV.is_contiguous():
+        raise ValueError("attention_kv: KV must be a contiguous [n_cols, 2, heads, d] tensor")
+    _check_tensors(p, Q, KV[:, 0], KV[:, 1], O, what="f3s_attention_kv", strided_kv=True)
+    H, d = Q.shape[1], Q.shape[2]
+    if O is None:
+        O = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
+    es = KV.element_size()
+    _check(_lib.f3s_attention_kv(p.handle, Q.data_ptr(), KV.data_ptr(), KV.data_ptr() + H * d * es, 2 * H * d,
+                                 O.data_ptr(), float(scale), H, d, _dtype_code(Q), _stream(stream)), "f3s_attention_kv")
+    return O
+
+
+def attention_kv_raw(p: Plan, q_ptr: int, k_ptr: int, v_ptr: int, kv_row_stride: int, o_ptr: int, scale: float,
+                     heads: int, d: int, dtype: int, stream: int) -> None:
+    """Pointer-level f3s_attention_kv (bench loops)."""
+    _check(_lib.f3s_attention_kv(p.handle, q_ptr, k_ptr, v_ptr, int(kv_row_stride), o_ptr, float(scale), heads, d,
+                                 dtype, stream), "f3s_attention_kv")
 
 
 def attention_raw(p: Plan, q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, scale: float, heads: int, d: int,
@@ -181,7 +247,7 @@ def attention_raw(p: Plan, q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, scale
 def attention_backward(p: Plan, Q, K, V, dO, *, scale: float, stream=None):
     """f3s_attention_backward: (dQ, dK, dV) fp32 device tensors for dO = dL/dO (fp32 [N, H, d])."""
     import torch
-    assert dO.dtype == torch.float32 and dO.is_contiguous()
+    _check_tensors(p, Q, K, V, dO, what="f3s_attention_backward")
     H, d = Q.shape[1], Q.shape[2]
     dQ = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
     dK = torch.empty(K.shape, dtype=torch.float32, device=K.device)

@@ -118,10 +118,11 @@ def test_row_shards_bitwise_equal_single_gpu(dist_mod, world):
     Qb, Kb, Vb = make_qkv(n, n, H, d, "fp16", seed=21)
     Q, K, V = to_dev(Qb, "fp16"), to_dev(Kb, "fp16"), to_dev(Vb, "fp16")
     rp, ci = csr_to_dev(g)
-    O1 = f3s.attention(f3s.plan(rp, ci, n), Q, K, V, scale=0.125)
+    p1 = f3s.plan(rp, ci, n)
+    O1 = f3s.attention(p1, Q, K, V, scale=0.125)
     parts = []
     for r in range(world):
-        sh = dist_mod.make_shard(g.row_ptr, g.col_idx, r, world)
+        sh = dist_mod.make_shard(g.row_ptr, g.col_idx, r, world, global_chunks=p1.info()["total_chunks"])
         s = sh.spec
         Ol = dist_mod.attention(sh, Q[s.row_begin:s.row_end].contiguous(), K, V,
                                 torch.empty((s.row_end - s.row_begin, H, d), dtype=torch.float32, device="cuda"),
@@ -150,3 +151,57 @@ def test_batched_graph_shards(dist_mod, oracle_mod):
                                 scale=0.125)
         outs.append(Ol.cpu().numpy())
     assert_close(np.concatenate(outs), ref)
+
+
+def _hub_window_graph(n_windows=10000, hub_cols=3200, seed=3):
+    """~1 chunk per row window plus one window (rows 0..15) of hub_cols distinct columns: its
+    chunk count (25) lies between a 2-shard plan's own split bound (17) and the global one (34)."""
+    rng = np.random.default_rng(seed)
+    n = 16 * n_windows
+    deg = rng.integers(2, 9, n)
+    deg[:16] = hub_cols // 16
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    ci = rng.integers(0, n, rp[-1]).astype(np.int32)
+    ci[:hub_cols] = rng.choice(n, hub_cols, replace=False)
+    for r in range(n):  # sorted unique rows (A is binary)
+        row = np.unique(ci[rp[r]:rp[r + 1]])
+        ci[rp[r]:rp[r] + len(row)] = row
+        ci[rp[r] + len(row):rp[r + 1]] = row[-1]
+    return n, rp, ci
+
+
+@pytest.mark.gpu
+def test_shard_split_bound_is_global(dist_mod):
+    """A row-shard plan takes the heavy-window split bound of the global problem, so a window the
+    1-GPU plan leaves whole is left whole on its shard and the O rows stay bitwise equal
+    (f3s.h f3s_plan_set_split)."""
+    import torch
+
+    from helpers import to_dev
+    from paper_2505_08098_b200 import f3s
+    n, rp_h, ci_h = _hub_window_graph()
+    H, d = 1, 64
+    Qb, Kb, Vb = make_qkv(n, n, H, d, "fp16", seed=3)
+    Q, K, V = to_dev(Qb, "fp16"), to_dev(Kb, "fp16"), to_dev(Vb, "fp16")
+    p1 = f3s.plan(torch.from_numpy(rp_h).cuda(), torch.from_numpy(ci_h).cuda(), n)
+    i1 = p1.info()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert i1["split_chunks"] == f3s.default_split_chunks(i1["total_chunks"], sms)
+    assert i1["split_groups"] == 0  # the 25-chunk hub window is whole in the 1-GPU plan
+    O1 = f3s.attention(p1, Q, K, V, scale=0.125)
+    own = []
+    parts = []
+    for r in range(2):
+        spec = dist_mod.shard_spec(rp_h, ci_h, r, 2)
+        local = f3s.plan_rows(torch.from_numpy(spec.row_ptr).cuda(), torch.from_numpy(spec.col_idx).cuda(),
+                              spec.row_end - spec.row_begin, n)
+        own.append(local.info())
+        sh = dist_mod.make_shard(rp_h, ci_h, r, 2, global_chunks=i1["total_chunks"])
+        assert sh.plan.info()["split_chunks"] == i1["split_chunks"]
+        parts.append(dist_mod.attention(sh, Q[spec.row_begin:spec.row_end].contiguous(), K, V,
+                                        torch.empty((spec.row_end - spec.row_begin, H, d), dtype=torch.float32,
+                                                    device="cuda"), scale=0.125))
+    # the shard holding the hub would have split it with its own bound
+    assert own[0]["split_groups"] == 1 and own[0]["split_chunks"] < 25 < i1["split_chunks"]
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts), O1)

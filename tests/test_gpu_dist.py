@@ -1,0 +1,87 @@
+"""SURVEY §8(e) row a12 on a real GPU: the multi-GPU exchange and the fused kernel running
+together on device memory.  Two ranks (processes) share the one GPU of the test box over a gloo
+process group (NCCL needs one GPU per rank): each builds its row-shard plan with the global split
+bound (all-reduced chunk count), uploads its padded [K||V] shard, replicates it with ONE
+all-gather, and runs f3s_attention_kv on the gathered buffer.  Each rank's O rows must equal the
+single-GPU call bit for bit and the fp64 oracle within BASELINE.json's tolerances."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import f3s_inputs as fi
+from helpers import TOL_MAX_ABS, TOL_REL_FRO, errors, make_qkv
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, graph, q):
+    import torch
+    import torch.distributed as tdist
+
+    import oracle
+    from paper_2505_08098_b200 import dist as f3sdist
+    from paper_2505_08098_b200 import f3s
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        if graph == "power":
+            g = fi.chung_lu(30000, 200000, gamma=2.2, max_deg=3000, seed=41)
+            H, d = 4, 64
+        else:  # dense communities: long row windows
+            g = fi.dcsbm(12000, 1500000, comm_size=3000, mu=0.9, gamma=2.1, max_deg=2000, seed=43)
+            H, d = 2, 128
+        n = g.n_rows
+        Qb, Kb, Vb = make_qkv(n, n, H, d, "fp16", seed=41)
+        f16 = lambda b: torch.from_numpy(np.ascontiguousarray(b).view(np.int16)).to(dev).view(torch.float16)
+        shard = f3sdist.make_shard(g.row_ptr, g.col_idx, rank, world, device=dev)  # global split bound via gloo
+        spec = shard.spec
+        KV_sh = f16(f3sdist.kv_shard(spec, Kb, Vb, n))
+        KV = torch.empty((world * spec.kv_rows, 2, H, d), dtype=torch.float16, device=dev)
+        f3sdist.allgather_kv_into(KV, KV_sh)
+        Ol = f3sdist.attention_kv(shard, f16(Qb[spec.row_begin:spec.row_end]), KV, scale=1.0 / d ** 0.5)
+        # the single-GPU call on the full problem, in this process
+        p1 = f3s.plan(torch.from_numpy(g.row_ptr).to(dev), torch.from_numpy(g.col_idx).to(dev), n)
+        O1 = f3s.attention(p1, f16(Qb), f16(Kb), f16(Vb), scale=1.0 / d ** 0.5)
+        torch.cuda.synchronize()
+        same = bool(torch.equal(Ol, O1[spec.row_begin:spec.row_end]))
+        same_split = shard.plan.info()["split_chunks"] == p1.info()["split_chunks"]
+        ref = oracle.attention(g.row_ptr, g.col_idx, Qb, Kb, Vb, scale=1.0 / d ** 0.5,
+                               rows=np.arange(spec.row_begin, spec.row_end, dtype=np.int32))
+        max_abs, rel = errors(Ol.cpu().numpy(), ref)
+        q.put((rank, same, same_split, max_abs, rel, spec.row_begin, spec.row_end, n))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("graph", ["power", "communities"])
+def test_two_ranks_allgather_then_kernel(graph):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, graph, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    for r in res:
+        assert len(r) == 8, f"rank {r[0]} failed: {r[1]}"
+    assert [r[1] for r in res] == [True, True], "shard rows != single-GPU rows (bitwise)"
+    assert [r[2] for r in res] == [True, True], "shard split bound != single-GPU bound"
+    for r in res:
+        assert r[3] <= TOL_MAX_ABS and r[4] <= TOL_REL_FRO, r
+    assert res[0][5] == 0 and res[0][6] == res[1][5] and res[1][6] == res[1][7]

@@ -1,41 +1,79 @@
-"""Parity at BASELINE.json's full sizes, in the configuration bench.py times: the products- and
-Reddit-shaped workloads (123.7M / 114.9M nnz) are too large for a full fp64 comparison in a test,
-so sampled rows (random, the heaviest row window, the last ragged window, empty rows) are checked
-element by element against the oracle, plus the plan's size invariants on the whole graph."""
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (the default
+variant: LPT queue, heavy-window split, head groups where they apply):
+
+  * the device plan of every one of the five workloads equals the oracle's independent block
+    builder bit for bit (rw_ptr, cols, masks, rw_order; SURVEY.md §8(d) "checked bit-exactly
+    against oracle_plan on every config");
+  * every output element of every workload -- including products' 627M and Reddit's 14.9M -- is
+    compared with the fp64 oracle, for fp16 AND bf16 inputs (SURVEY.md §8(d) "Full comparison of
+    all N·H·d outputs"), within BASELINE.json's max-abs 1e-2 and relative-Frobenius 5e-3 taken
+    over the whole output.  The oracle runs on row blocks so the host holds one block at a time.
+"""
 import numpy as np
 import pytest
 
-from helpers import assert_close, to_dev
+from helpers import TOL_MAX_ABS, TOL_REL_FRO, to_dev
 
 pytestmark = pytest.mark.gpu
 
+CONFIGS = ["cora", "arxiv", "products", "reddit", "batched"]
 
-@pytest.mark.parametrize("name", ["products", "reddit"])
-def test_full_size_sampled_parity(oracle_mod, name):
+
+@pytest.fixture(scope="module")
+def graphs():
+    from f3s_inputs import configs
+    cache = {}
+
+    def get(name):
+        if name not in cache:  # (all five CSRs together: ~1.1 GB of host memory)
+            w = configs.get(name)
+            cache[name] = (w, w.graph())
+        return cache[name]
+    return get
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_full_size_plan_bitexact(oracle_mod, graphs, name):
     import torch
 
-    from f3s_inputs import configs
     from paper_2505_08098_b200 import f3s
-    w = configs.get(name)
-    csr = w.graph()
-    Qb, Kb, Vb = w.qkv(csr)
-    rp = torch.from_numpy(csr.row_ptr).cuda()
-    ci = torch.from_numpy(csr.col_idx).cuda()
-    plan = f3s.plan(rp, ci, csr.n_rows)
-    info = plan.info()
-    assert info["nnz"] == csr.nnz and info["num_rw"] == (csr.n_rows + 15) // 16
-    O = f3s.attention(plan, to_dev(Qb, w.dtype), to_dev(Kb, w.dtype), to_dev(Vb, w.dtype), scale=w.scale)
+    w, csr = graphs(name)
+    p = f3s.plan(torch.from_numpy(csr.row_ptr).cuda(), torch.from_numpy(csr.col_idx).cuda(), csr.n_rows)
+    rw_ptr, cols, masks, order = p.export()
+    ref = oracle_mod.plan(csr.row_ptr, csr.col_idx, csr.n_cols)
+    assert np.array_equal(rw_ptr, ref.rw_ptr)
+    assert np.array_equal(cols, ref.cols)
+    assert np.array_equal(masks, ref.masks)
+    assert np.array_equal(order, ref.rw_order)
+    info = p.info()
+    assert info["nnz"] == csr.nnz and info["total_tcb8"] == int(ref.tcb8.sum())
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("name", CONFIGS)
+def test_full_size_parity_all_outputs(oracle_mod, graphs, name, dtype):
+    import torch
+
+    from paper_2505_08098_b200 import f3s
+    w, csr = graphs(name)
+    Qb, Kb, Vb = w.qkv(csr, dtype=dtype)
+    p = f3s.plan(torch.from_numpy(csr.row_ptr).cuda(), torch.from_numpy(csr.col_idx).cuda(), csr.n_rows)
+    O = f3s.attention(p, to_dev(Qb, dtype), to_dev(Kb, dtype), to_dev(Vb, dtype), scale=w.scale)
     torch.cuda.synchronize()
-    rw_ptr, _, _, order = plan.export()
-    heavy = int(order[0])  # the widest row window (LPT first)
-    rng = np.random.default_rng(5)
-    deg = np.diff(csr.row_ptr)
-    rows = np.concatenate([rng.choice(csr.n_rows, 3000, replace=False), np.arange(16 * heavy, 16 * heavy + 16),
-                           np.arange(max(0, csr.n_rows - 20), csr.n_rows), np.nonzero(deg == 0)[0][:50]])
-    rows = np.unique(rows).astype(np.int32)
-    ref = oracle_mod.attention(csr.row_ptr, csr.col_idx, Qb, Kb, Vb, scale=w.scale, dtype=w.dtype, rows=rows)
-    got = O[torch.from_numpy(rows).cuda().long()].cpu().numpy()
-    assert_close(got, ref)
-    assert np.all(np.isfinite(O.cpu().numpy()))
-    # the heaviest window really is wide (several 128-column chunks)
-    assert rw_ptr[heavy + 1] - rw_ptr[heavy] > 256
+    n = csr.n_rows
+    block = max(16, (1 << 26) // (w.H * w.d))  # ~0.5 GB of fp64 reference per block
+    max_abs, sq_diff, sq_ref, worst = 0.0, 0.0, 0.0, -1
+    for b in range(0, n, block):
+        rows = np.arange(b, min(n, b + block), dtype=np.int32)
+        ref = oracle_mod.attention(csr.row_ptr, csr.col_idx, Qb, Kb, Vb, scale=w.scale, dtype=dtype, rows=rows)
+        got = O[b:b + len(rows)].double().cpu().numpy()
+        assert np.all(np.isfinite(got)), f"non-finite output in rows {b}..{b + len(rows)}"
+        diff = got - ref
+        a = np.abs(diff).max(axis=(1, 2))
+        if a.max() > max_abs:
+            max_abs, worst = float(a.max()), int(b + a.argmax())
+        sq_diff += float((diff * diff).sum())
+        sq_ref += float((ref * ref).sum())
+    rel = (sq_diff / sq_ref) ** 0.5 if sq_ref > 0 else sq_diff ** 0.5
+    print(f"{name} {dtype}: {n * w.H * w.d} outputs, max_abs {max_abs:.3e} (row {worst}), rel_fro {rel:.3e}")
+    assert max_abs <= TOL_MAX_ABS and rel <= TOL_REL_FRO, (max_abs, worst, rel)

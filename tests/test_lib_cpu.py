@@ -22,7 +22,7 @@ def f3s():
 
 def test_exports_every_declared_symbol(f3s):
     header = open(os.path.join(ROOT, "include", "f3s.h")).read()
-    declared = set(re.findall(r"^\s*(?:const char\*|f3s_status|int64_t)\s+(f3s_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:const char\*|f3s_status|int64_t|int32_t)\s+(f3s_\w+)\s*\(", header, re.M))
     assert len(declared) >= 13
     lib = ctypes.CDLL(f3s.LIB_PATH)
     for name in declared:

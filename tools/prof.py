@@ -5,10 +5,9 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 NAMES = {0: "index: wait slot", 1: "index: queue fetch", 2: "index: issue",
          8: "prod: wait ids", 9: "prod: wait Q slot", 10: "prod: wait ring", 11: "prod: issue",
-         16: "mma: idle", 17: "mma: MMA1", 18: "mma: MMA2", 19: "mma: S-buffer blocked", 20: "mma: wait P/V",
-         24: "smax: wait K", 25: "smax: wait S", 26: "smax: S->max", 27: "smax: bar+pempty", 28: "smax: fence+arrive",
-         29: "smax: l", 30: "smax: exp loop", 31: "smax: P/alpha stores",
-         32: "corr: wait P", 33: "corr: wait O", 34: "corr: fold", 35: "corr: wait l", 36: "corr: store"}
+         24: "smax: wait idx", 25: "smax: wait S", 26: "smax: S->max", 27: "smax: bar+combine", 28: "smax: wait pempty",
+         29: "smax: fence+arrive", 30: "smax: exp+rowsum", 31: "smax: P/m/l stores",
+         32: "corr: wait P", 33: "corr: wait O", 34: "corr: merge", 35: "corr: store"}
 
 def main():
     ap = argparse.ArgumentParser()
