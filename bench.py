@@ -56,6 +56,9 @@ def parse_args():
                     help="also time N calls captured in one CUDA graph (default 100 for cora, else 0)")
     ap.add_argument("--kv-interleaved", action="store_true",
                     help="N = 1: K and V in one [n, 2, H, d] buffer (the layout of the multi-GPU all-gather)")
+    ap.add_argument("--overlap", action="store_true",
+                    help="N > 1 (f2): ring exchange of the [K||V] blocks on a side stream overlapped with "
+                         "f3s_attention_partial on the blocks present, then f3s_attention_merge")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU/gloo run of the multi-rank orchestration (partition, [K||V] all-gather, timing "
                          "reduction, JSON line) without the CUDA kernel; value is null")
@@ -369,7 +372,7 @@ def main():
         return torch.from_numpy(np.ascontiguousarray(bits)).view(ht).to(dev).view(tdt)
 
     # ---- plan (one-time preprocessing; timed separately) ----
-    KV_sh = KV = None
+    KV_sh = KV = ovl = None
     kv_ld = 0
     if world == 1:
         rp = torch.from_numpy(csr.row_ptr).to(dev)
@@ -393,6 +396,9 @@ def main():
         if batched:  # whole graphs per rank: own K/V rows, no collective
             K = dev_tensor(Kb[row_b:row_e])
             V = dev_tensor(Vb[row_b:row_e])
+        elif args.overlap:  # f2: the blocks stream in while the kernel works on those present
+            ovl = f3sdist.OverlappedShard(spec, H, d, tdt, device=dev)
+            ovl.own_block().copy_(dev_tensor(f3sdist.kv_shard(spec, Kb, Vb, csr.n_cols)))
         else:  # equal padded [K||V] shards, replicated by ONE all-gather (NCCL over NVLink)
             KV_sh = dev_tensor(f3sdist.kv_shard(spec, Kb, Vb, csr.n_cols))
             KV = torch.empty((world * spec.kv_rows, 2, H, d), dtype=tdt, device=dev)
@@ -405,6 +411,9 @@ def main():
         raise SystemExit("--variant needs separate K/V (N = 1 without --kv-interleaved)")
 
     def attn(s=sp):
+        if ovl is not None:
+            ovl.run(Q, O, w.scale)
+            return
         if n_loc == 0:
             return
         if kv_ld:
@@ -548,9 +557,9 @@ def main():
                           "call -> host O; one step's uploads overlap the previous step's read-back)"}
         else:
             Qh = torch.from_numpy(np.ascontiguousarray(Qb[row_b:row_e])).view(ht).pin_memory()
-            if KV_sh is not None:
+            if KV_sh is not None or ovl is not None:
                 KVh = torch.from_numpy(f3sdist.kv_shard(spec, Kb, Vb, csr.n_cols)).view(ht).pin_memory()
-                h2d = [(Q, Qh), (KV_sh, KVh)]
+                h2d = [(Q, Qh), (KV_sh if ovl is None else ovl.own_block(), KVh)]
             else:
                 Kh = torch.from_numpy(np.ascontiguousarray(Kb[row_b:row_e])).view(ht).pin_memory()
                 Vh = torch.from_numpy(np.ascontiguousarray(Vb[row_b:row_e])).view(ht).pin_memory()
@@ -619,7 +628,9 @@ def main():
                              f"{'>' if kv_bytes > 126e6 else '<'} 126 MB L2)",
                        "parallelism": "single-gpu" if world == 1 else
                        ("graphs sharded by nnz, no collective" if batched else
-                        f"rows sharded by nnz over {world} + one NCCL [K||V] all-gather")},
+                        (f"rows sharded by nnz over {world}; ring exchange of [K||V] blocks overlapped with "
+                         "per-block partial kernels + merge (f2); kernel_ms includes the exchange") if ovl is not None
+                        else f"rows sharded by nnz over {world} + one NCCL [K||V] all-gather")},
             "timing": {"step_ms": percentiles(step_list), "kernel_ms": percentiles(kern_list),
                        "region_ms_incl_flush": round(region_ms, 3),
                        "warm_l2_kernel_ms": round(warm_ms, 4) if warm_ms is not None else None,

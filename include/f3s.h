@@ -174,6 +174,45 @@ f3s_status f3s_attention_kv(f3s_plan_t plan, const void* Q, const void* K, const
                             float* O, float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
 
 /*
+ * f3s_attention on row-strided inputs: row i of Q is Q + i*q_row_stride elements, row j of K (V)
+ * is K + j*kv_row_stride (V + j*kv_row_stride); each stride >= heads*d and a multiple of 16 bytes
+ * (0 = heads*d).  Lets the fused pass read Q, K, V straight out of one projection GEMM output
+ * [n, 3, heads, d] (Q = buf, K = buf + heads*d, V = buf + 2*heads*d, both strides 3*heads*d) --
+ * the Graph Transformer layer of PAPER.md:683-694.  Default variant; otherwise as f3s_attention.
+ */
+f3s_status f3s_attention_strided(f3s_plan_t plan, const void* Q, int64_t q_row_stride, const void* K, const void* V,
+                                 int64_t kv_row_stride, float* O, float scale, int32_t heads, int32_t d,
+                                 f3s_dtype dtype, cudaStream_t stream);
+
+/*
+ * Column-block form for overlapping the multi-GPU K/V exchange with compute (
+ * rows are independent, and the online softmax of Alg.1 l.16-21 is order-independent
+ * up to rounding): `plan` covers only the columns of one K/V block (f3s_plan_rows over the CSR
+ * entries whose column lies in the block, global column ids), so the block can be processed as
+ * soon as its K/V rows have arrived.  Writes, for every row i and head h of the plan,
+ *   O_part[i, h, :] = sum_j 2^(s_ij - m_ih) v_j   (unnormalised; s in log2 units incl. scale)
+ *   ml_part[i, h]   = (m_ih, l_ih = sum_j 2^(s_ij - m_ih))    (two floats; m = -8.5e37, l = 0 and
+ *                     O = 0 for a row with no entry in the block)
+ * f3s_attention_merge then combines the blocks.  K/V rows at kv_row_stride elements (0: heads*d).
+ * max_ctas > 0 caps the persistent grid (leaving SMs to a collective running concurrently).
+ *  O_part  device float [n_rows, heads, d];  ml_part device float [n_rows, heads, 2] (8-byte aligned)
+ * Errors: as f3s_attention; INVALID_VALUE for NULL ml_part, max_ctas < 0 or a bad stride.
+ */
+f3s_status f3s_attention_partial(f3s_plan_t plan, const void* Q, const void* K, const void* V, int64_t kv_row_stride,
+                                 float* O_part, float* ml_part, float scale, int32_t heads, int32_t d, f3s_dtype dtype,
+                                 int32_t max_ctas, cudaStream_t stream);
+
+/*
+ * O = merge of `parts` column-block partials, in part order (deterministic):
+ *   M = max_g m_g,  l = sum_g 2^(m_g - M) l_g,  O = sum_g 2^(m_g - M) O_g / l   (0 if l = 0),
+ * i.e. Alg.1's rescaling (l.18, l.21) and final division (l.24) applied once per block.
+ *  O_parts  device float [parts][n_rows][heads][d];  ml_parts device float [parts][n_rows][heads][2]
+ *  O        device float [n_rows][heads][d];  1 <= parts <= 32;  d in {64, 128}.
+ */
+f3s_status f3s_attention_merge(int32_t parts, const float* O_parts, const float* ml_parts, int64_t n_rows,
+                               int32_t heads, int32_t d, float* O, cudaStream_t stream);
+
+/*
  * Backward of f3s_attention ("SpMM and SDDMM operations in reverse order",
  * PAPER.md:752): for O = softmax_row(scale * (Q K^T) (.) A) V and dO = dL/dO,
  *   dp_ij = dO_i . v_j,  D_i = sum_j p_ij dp_ij,  ds_ij = p_ij (dp_ij - D_i),

@@ -221,7 +221,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             int32_t* __restrict__ counter, int32_t n_items, int32_t H, int64_t ldkv,
             const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float scale_log2,
             uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt_arg,
-            float* __restrict__ scratch) {
+            float* __restrict__ scratch, float2* __restrict__ ml_out, int32_t n_rows) {
     constexpr int EB = (int)sizeof(T);
     using C = Cfg<D, HG, EB>;
     using B = Bars<D, HG, EB>;
@@ -816,8 +816,10 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             mbar_arrive(bar(B::pempty(b)));
             if (lead) lap(2);
             if (flags & 2) {
-                // O_i = diag(l)^-1 O_i (l.24); empty row (l = 0) -> 0 (reading c4)
-                const float linv = l_run > 0.f ? rcp_approx(l_run) : 0.f;
+                // O_i = diag(l)^-1 O_i (l.24); empty row (l = 0) -> 0 (reading c4).  Partial mode
+                // (ml_out != nullptr, f3s_attention_partial): O stays unnormalised and the row's
+                // (m, l) go to ml_out, for f3s_attention_merge to combine column blocks
+                const float linv = ml_out ? 1.f : l_run > 0.f ? rcp_approx(l_run) : 0.f;
                 float li[16];  // 1 / l of the 16 rows, broadcast to every lane (outside the lane-divergent stores)
 #pragma unroll
                 for (int i = 0; i < 16; ++i) li[i] = __shfl_sync(0xffffffffu, linv, i);
@@ -838,6 +840,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         for (int i = 0; i < 16; ++i) rec[32 + i * D + f] = oacc[i];
                     }
                 } else {
+                    if (ml_out && q == 0 && lane < 16 && 16 * rw + lane < n_rows)
+                        ml_out[(int64_t)(16 * rw + lane) * H + hd] = make_float2(m_run, l_run);
                     // O tile [16 x D] fp32 staged in shared memory and written by one TMA store
                     // (rows past n_rows of a ragged last window are clipped by the tensor map, c14)
                     const int ob = item % C::kNO;
@@ -877,7 +881,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 // which is the online-softmax rescaling of Alg.1 l.18/l.21 applied once per piece.
 template <int D>
 __global__ void __launch_bounds__(256) k_split_merge(const int4* __restrict__ ginfo, const float* __restrict__ scratch,
-                                                     float* __restrict__ O, int32_t H, int32_t n_rows) {
+                                                     float* __restrict__ O, int32_t H, int32_t n_rows,
+                                                     float2* __restrict__ ml_out) {
     const int g = blockIdx.x / H, h = blockIdx.x - (blockIdx.x / H) * H;
     const int4 gi = ginfo[g];
     const int64_t rec_floats = 32 + 16 * D, stride = (int64_t)H * rec_floats;
@@ -894,9 +899,47 @@ __global__ void __launch_bounds__(256) k_split_merge(const int4* __restrict__ gi
             acc = fmaf(w, rj[32 + i * D + f], acc);
         }
         const int64_t row = 16 * (int64_t)gi.z + i;
-        if (row < n_rows) O[(row * H + h) * D + f] = l > 0.f ? acc / l : 0.f;  // empty row -> 0 (reading c4)
+        if (row >= n_rows) continue;
+        if (ml_out) {  // partial mode: the window's unnormalised O and its (m, l)
+            O[(row * H + h) * D + f] = acc;
+            if (f == 0) ml_out[row * H + h] = make_float2(M, l);
+        } else {
+            O[(row * H + h) * D + f] = l > 0.f ? acc / l : 0.f;  // empty row -> 0 (reading c4)
+        }
     }
 }
+
+}  // namespace
+
+// Merge of column-block partials (K/V blocks that arrive one by one are processed
+// as they land, each leaving the unnormalised (m, l, O) of every row): in part order
+//   M = max_g m_g,  l = sum_g 2^(m_g - M) l_g,  O = sum_g 2^(m_g - M) O_g / l   (0 if l = 0),
+// the rescaling of Alg.1 l.18/l.21 applied once per block.  One warp per (row, head); fixed order,
+// so the result is deterministic.
+__global__ void __launch_bounds__(256) k_parts_merge(int32_t parts, const float* __restrict__ Op,
+                                                     const float2* __restrict__ mlp, int64_t rows_heads, int32_t D,
+                                                     float* __restrict__ O) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t rh = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; rh < rows_heads; rh += nw) {
+        const float2 ml = lane < parts ? mlp[(int64_t)lane * rows_heads + rh] : make_float2(-INFINITY, 0.f);
+        float M = ml.x;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float wgt = lane < parts ? exp2f(ml.x - M) : 0.f;
+        float l = 0.f;
+        for (int g = 0; g < parts; ++g) l = fmaf(__shfl_sync(0xffffffffu, wgt, g), __shfl_sync(0xffffffffu, ml.y, g), l);
+        const float inv = l > 0.f ? 1.f / l : 0.f;  // empty row -> 0 (reading c4)
+        for (int f = lane; f < D; f += 32) {
+            float acc = 0.f;
+            for (int g = 0; g < parts; ++g)
+                acc = fmaf(__shfl_sync(0xffffffffu, wgt, g), Op[((int64_t)g * rows_heads + rh) * D + f], acc);
+            O[rh * D + f] = acc * inv;
+        }
+    }
+}
+
+namespace {
 
 // ---- host side ------------------------------------------------------------------------------------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -922,28 +965,29 @@ EncodeTiledFn get_encode() {
 // launches (cora); the last few encodings are reused (per host thread) for identical arguments.
 struct MapKey {
     const void* base;
-    int64_t inner, rows;
+    int64_t inner, rows, ld;
     uint32_t type, box_inner, box_rows, swz;
     bool operator==(const MapKey& o) const {
-        return base == o.base && inner == o.inner && rows == o.rows && type == o.type && box_inner == o.box_inner &&
-               box_rows == o.box_rows && swz == o.swz;
+        return base == o.base && inner == o.inner && rows == o.rows && ld == o.ld && type == o.type &&
+               box_inner == o.box_inner && box_rows == o.box_rows && swz == o.swz;
     }
 };
 f3s_status make_map_uncached(CUtensorMap* map, const void* base, CUtensorMapDataType type, int64_t inner,
-                             int64_t rows, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz);
+                             int64_t rows, int64_t ld, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz);
+// ld: elements between consecutive rows (>= inner)
 f3s_status make_map(CUtensorMap* map, const void* base, CUtensorMapDataType type, int64_t inner, int64_t rows,
-                    uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz) {
+                    int64_t ld, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz) {
     constexpr int kCache = 8;
     thread_local MapKey keys[kCache];
     thread_local CUtensorMap maps[kCache];
     thread_local int used = 0, next = 0;
-    const MapKey k{base, inner, rows, (uint32_t)type, box_inner, box_rows, (uint32_t)swz};
+    const MapKey k{base, inner, rows, ld, (uint32_t)type, box_inner, box_rows, (uint32_t)swz};
     for (int i = 0; i < used; ++i)
         if (keys[i] == k) {
             *map = maps[i];
             return F3S_OK;
         }
-    f3s_status st = make_map_uncached(map, base, type, inner, rows, box_inner, box_rows, swz);
+    f3s_status st = make_map_uncached(map, base, type, inner, rows, ld, box_inner, box_rows, swz);
     if (st != F3S_OK) return st;
     keys[next] = k;
     maps[next] = *map;
@@ -952,12 +996,12 @@ f3s_status make_map(CUtensorMap* map, const void* base, CUtensorMapDataType type
     return F3S_OK;
 }
 f3s_status make_map_uncached(CUtensorMap* map, const void* base, CUtensorMapDataType type, int64_t inner,
-                             int64_t rows, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz) {
+                             int64_t rows, int64_t ld, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz) {
     EncodeTiledFn enc = get_encode();
     if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return F3S_ERR_CUDA; }
     const int esz = type == CU_TENSOR_MAP_DATA_TYPE_FLOAT32 ? 4 : type == CU_TENSOR_MAP_DATA_TYPE_UINT8 ? 1 : 2;
     cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)inner * esz};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * esz};
     cuuint32_t box[2] = {box_inner, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, type, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -968,11 +1012,13 @@ f3s_status make_map_uncached(CUtensorMap* map, const void* base, CUtensorMapData
     }
     return F3S_OK;
 }
-f3s_status make_map(CUtensorMap* map, const void* base, f3s_dtype dtype, int64_t inner, int64_t rows, uint32_t box_rows) {
+f3s_status make_map(CUtensorMap* map, const void* base, f3s_dtype dtype, int64_t inner, int64_t rows, int64_t ld,
+                    uint32_t box_rows) {
     if (dtype == F3S_E4M3)  // 8-bit elements: 128-element (128-byte) boxes
-        return make_map(map, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, inner, rows, 128, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
+        return make_map(map, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, inner, rows, ld, 128, box_rows,
+                        CU_TENSOR_MAP_SWIZZLE_128B);
     return make_map(map, base, dtype == F3S_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                    inner, rows, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
+                    inner, rows, ld, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 template <int D, typename T, int HG>
@@ -986,8 +1032,11 @@ f3s_status launch(const AttnArgs& a) {
     }
     CUtensorMap mq, mo;
     f3s_status st;
-    if ((st = make_map(&mq, a.Q, a.dtype, (int64_t)a.heads * D, p.n_rows, 16)) != F3S_OK) return st;
-    if ((st = make_map(&mo, a.O, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (int64_t)a.heads * D, p.n_rows, D * HG, 16,
+    if ((st = make_map(&mq, a.Q, a.dtype, (int64_t)a.heads * D, p.n_rows, a.q_ld > 0 ? a.q_ld : (int64_t)a.heads * D,
+                       16)) != F3S_OK)
+        return st;
+    if ((st = make_map(&mo, a.O, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (int64_t)a.heads * D, p.n_rows, (int64_t)a.heads * D,
+                       D * HG, 16,
                        CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK)
         return st;
 
@@ -1018,7 +1067,10 @@ f3s_status launch(const AttnArgs& a) {
     const int64_t n_items64 = (int64_t)(a.lpt ? p.n_sub : p.num_rw) * (a.heads / HG);
     if (n_items64 > 0x7FFFFFFF) { set_error("too many work items"); return F3S_ERR_UNSUPPORTED; }
     const int32_t n_items = (int32_t)n_items64;
-    const int grid = a.grid_override > 0 ? a.grid_override : (int)std::min<int64_t>(n_items, (int64_t)sms * C::kCtasPerSm);
+    if (a.ml_out && HG > 1) { set_error("internal: partial mode with head groups"); return F3S_ERR_INTERNAL; }
+    int64_t ctas = (int64_t)sms * C::kCtasPerSm;
+    if (a.max_ctas > 0) ctas = std::min<int64_t>(ctas, a.max_ctas);  // SMs left free for a concurrent collective
+    const int grid = a.grid_override > 0 ? a.grid_override : (int)std::min<int64_t>(n_items, ctas);
     // per-call scratch, stream-ordered (so calls in flight on other streams, or replays of a
     // captured graph, never share it): the work-queue counter, then for split plans one
     // (m[16], l[16], O[16][D]) fp32 record per piece and head
@@ -1033,13 +1085,15 @@ f3s_status launch(const AttnArgs& a) {
             mq, mo, a.lpt ? p.meta_sub : p.meta_nat, p.kcols, p.kmasks, counter, n_items, a.heads,
             (a.kv_ld > 0 ? a.kv_ld : (int64_t)a.heads * D) * (int64_t)sizeof(T),
             static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.scale * 1.4426950408889634f, a.trace,
-            a.trace_chunks, a.expt, split ? reinterpret_cast<float*>(scratch + 256) : nullptr);
+            a.trace_chunks, a.expt, split ? reinterpret_cast<float*>(scratch + 256) : nullptr,
+            reinterpret_cast<float2*>(a.ml_out), p.n_rows);
         count_launch();
         err = cudaGetLastError();
     }
     if (err == cudaSuccess && split) {
         k_split_merge<D><<<(int)((int64_t)p.n_groups * a.heads), 256, 0, a.stream>>>(
-            p.ginfo, reinterpret_cast<const float*>(scratch + 256), a.O, a.heads, p.n_rows);
+            p.ginfo, reinterpret_cast<const float*>(scratch + 256), a.O, a.heads, p.n_rows,
+            reinterpret_cast<float2*>(a.ml_out));
         count_launch();
         err = cudaGetLastError();
     }
@@ -1060,13 +1114,38 @@ f3s_status launch_attention_sm100(const AttnArgs& a) {
     }
     // head groups of 4 when every row window fits one 32-column block (d = 64): the per-chunk
     // pipeline cost is shared by 4 heads (batched small graphs)
-    const bool hg4 = !a.one_head && a.d == 64 && a.heads % 4 == 0 && p.max_width <= 32 && p.n_groups == 0;
+    const bool hg4 = !a.one_head && !a.ml_out && a.d == 64 && a.heads % 4 == 0 && p.max_width <= 32 && p.n_groups == 0;
     if (a.dtype == F3S_FP16) {
         if (hg4) return launch<64, __half, 4>(a);
         return a.d == 64 ? launch<64, __half, 1>(a) : launch<128, __half, 1>(a);
     }
     if (hg4) return launch<64, __nv_bfloat16, 4>(a);
     return a.d == 64 ? launch<64, __nv_bfloat16, 1>(a) : launch<128, __nv_bfloat16, 1>(a);
+}
+
+__global__ void k_fill_ml(float2* __restrict__ ml, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        ml[i] = make_float2(kMFloor, 0.f);
+}
+
+f3s_status launch_fill_ml(float* ml, int64_t rows_heads, cudaStream_t stream) {
+    if (rows_heads == 0) return F3S_OK;
+    k_fill_ml<<<(int)std::min<int64_t>((rows_heads + 255) / 256, 148 * 8), 256, 0, stream>>>(
+        reinterpret_cast<float2*>(ml), rows_heads);
+    count_launch();
+    F3S_CUDA_TRY(cudaGetLastError());
+    return F3S_OK;
+}
+
+f3s_status launch_parts_merge(int32_t parts, const float* O_parts, const float* ml_parts, int64_t rows_heads, int32_t d,
+                              float* O, cudaStream_t stream) {
+    if (rows_heads == 0) return F3S_OK;
+    const int64_t blocks = std::min<int64_t>((rows_heads + 7) / 8, 148 * 16);
+    k_parts_merge<<<(int)blocks, 256, 0, stream>>>(parts, O_parts, reinterpret_cast<const float2*>(ml_parts), rows_heads,
+                                                   d, O);
+    count_launch();
+    F3S_CUDA_TRY(cudaGetLastError());
+    return F3S_OK;
 }
 
 }  // namespace f3s

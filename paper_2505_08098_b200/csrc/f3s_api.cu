@@ -78,9 +78,14 @@ static f3s_status check_attention_args(f3s_plan_t plan, const void* Q, const voi
 static f3s_status run_attention(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float scale,
                                 int32_t heads, int32_t d, f3s_dtype dtype, f3s_variant variant, cudaStream_t stream,
                                 uint64_t* trace = nullptr, int32_t trace_chunks = 0, int32_t grid = 0,
-                                int64_t kv_ld = 0) {
+                                int64_t kv_ld = 0, int64_t q_ld = 0) {
     f3s_status st = check_attention_args(plan, Q, K, V, O, scale, heads, d, dtype, true);
     if (st != F3S_OK) return st;
+    if (q_ld != 0 && (q_ld < (int64_t)heads * d || (q_ld * (dtype == F3S_E4M3 ? 1 : 2)) % 16 != 0)) {
+        set_error("q_row_stride must be >= heads * d and a multiple of 16 bytes");
+        return F3S_ERR_INVALID_VALUE;
+    }
+    if (q_ld != 0 && variant == F3S_VARIANT_SIMT) { set_error("q_row_stride: tcgen05 variants only"); return F3S_ERR_UNSUPPORTED; }
     if (kv_ld != 0) {
         if (kv_ld < (int64_t)heads * d) { set_error("kv_row_stride < heads * d"); return F3S_ERR_INVALID_VALUE; }
         if ((kv_ld * (dtype == F3S_E4M3 ? 1 : 2)) % 16 != 0) {
@@ -92,6 +97,7 @@ static f3s_status run_attention(f3s_plan_t plan, const void* Q, const void* K, c
     AttnArgs a{reinterpret_cast<const Plan*>(plan), Q, K, V, O, scale, heads, d, dtype,
                variant != F3S_VARIANT_NO_REORDER, stream};
     a.kv_ld = kv_ld;
+    a.q_ld = q_ld;
     a.trace = trace_chunks < 0 ? nullptr : trace;
     a.trace_chunks = trace_chunks < 0 ? 0 : trace_chunks;
     a.expt = trace_chunks < 0 ? -trace_chunks : 0;
@@ -261,6 +267,64 @@ f3s_status f3s_attention_kv(f3s_plan_t plan, const void* Q, const void* K, const
     try {
         return run_attention(plan, Q, K, V, O, scale, heads, d, dtype, F3S_VARIANT_DEFAULT, stream, nullptr, 0, 0,
                              kv_row_stride);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_strided(f3s_plan_t plan, const void* Q, int64_t q_row_stride, const void* K, const void* V,
+                                 int64_t kv_row_stride, float* O, float scale, int32_t heads, int32_t d,
+                                 f3s_dtype dtype, cudaStream_t stream) {
+    try {
+        return run_attention(plan, Q, K, V, O, scale, heads, d, dtype, F3S_VARIANT_DEFAULT, stream, nullptr, 0, 0,
+                             kv_row_stride, q_row_stride);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_partial(f3s_plan_t plan, const void* Q, const void* K, const void* V, int64_t kv_row_stride,
+                                 float* O_part, float* ml_part, float scale, int32_t heads, int32_t d, f3s_dtype dtype,
+                                 int32_t max_ctas, cudaStream_t stream) {
+    try {
+        f3s_status st = check_attention_args(plan, Q, K, V, O_part, scale, heads, d, dtype, true);
+        if (st != F3S_OK) return st;
+        const Plan& p = *reinterpret_cast<const Plan*>(plan);
+        if (p.n_rows > 0 && !ml_part) { set_error("ml_part is NULL"); return F3S_ERR_INVALID_VALUE; }
+        if (reinterpret_cast<uintptr_t>(ml_part) & 7) { set_error("ml_part must be 8-byte aligned"); return F3S_ERR_UNSUPPORTED; }
+        if (max_ctas < 0) { set_error("max_ctas < 0"); return F3S_ERR_INVALID_VALUE; }
+        if (kv_row_stride != 0 && (kv_row_stride < (int64_t)heads * d ||
+                                   (kv_row_stride * (dtype == F3S_E4M3 ? 1 : 2)) % 16 != 0)) {
+            set_error("kv_row_stride must be >= heads * d and a multiple of 16 bytes");
+            return F3S_ERR_INVALID_VALUE;
+        }
+        if (p.n_rows == 0) return F3S_OK;
+        AttnArgs a{&p, Q, K, V, O_part, scale, heads, d, dtype, true, stream};
+        a.kv_ld = kv_row_stride;
+        a.ml_out = ml_part;
+        a.max_ctas = max_ctas;
+        DeviceScope scope;
+        F3S_CUDA_TRY(scope.enter(p.device));
+        if (p.nnz == 0 || p.n_cols == 0) {  // no entries in this block: O = 0, (m, l) = (floor, 0)
+            F3S_CUDA_TRY(cudaMemsetAsync(O_part, 0, sizeof(float) * (size_t)p.n_rows * heads * d, stream));
+            return launch_fill_ml(ml_part, (int64_t)p.n_rows * heads, stream);
+        }
+        return launch_attention_sm100(a);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_merge(int32_t parts, const float* O_parts, const float* ml_parts, int64_t n_rows,
+                               int32_t heads, int32_t d, float* O, cudaStream_t stream) {
+    try {
+        if (parts < 1 || parts > 32) { set_error("parts must be in [1, 32]"); return F3S_ERR_INVALID_VALUE; }
+        if (n_rows < 0 || heads < 1 || (d != 64 && d != 128)) { set_error("bad sizes"); return F3S_ERR_INVALID_VALUE; }
+        if (n_rows > 0 && (!O_parts || !ml_parts || !O)) { set_error("NULL pointer"); return F3S_ERR_INVALID_VALUE; }
+        return launch_parts_merge(parts, O_parts, ml_parts, n_rows * heads, d, O, stream);
     } catch (...) {
         set_error("internal error");
         return F3S_ERR_INTERNAL;

@@ -115,9 +115,15 @@ struct AttnArgs {
     int32_t expt = 0;           // sensitivity experiments (diagnostics only)
     bool one_head = false;      // F3S_VARIANT_ONE_HEAD: no head groups
     int64_t kv_ld = 0;          // elements between consecutive K (and V) rows; 0 = heads * d
+    int64_t q_ld = 0;           // elements between consecutive Q rows; 0 = heads * d
+    float* ml_out = nullptr;    // partial mode: [n_rows, heads] (m, l) pairs; O left unnormalised
+    int32_t max_ctas = 0;       // > 0: at most this many CTAs (SMs left for a concurrent collective)
 };
 
 f3s_status launch_attention_sm100(const AttnArgs& a);
+f3s_status launch_fill_ml(float* ml, int64_t rows_heads, cudaStream_t stream);
+f3s_status launch_parts_merge(int32_t parts, const float* O_parts, const float* ml_parts, int64_t rows_heads, int32_t d,
+                              float* O, cudaStream_t stream);
 // (re)build meta_sub / sinfo with pieces of at most `chunks` 128-column chunks (chunks <= 0: no split)
 f3s_status build_split(Plan* p, int32_t chunks);
 constexpr int kSplitChunkCols = 128;  // column granularity of the split (the kernel's chunk)

@@ -159,3 +159,129 @@ def attention(shard: Shard, Q_local, K_full, V_full, O_local=None, *, scale: flo
     if shard.spec.row_end == shard.spec.row_begin:
         return O_local
     return f3s.attention(shard.plan, Q_local, K_full, V_full, O_local, scale=scale, stream=stream, variant=variant)
+
+
+# ---- f2: K/V exchange overlapped with compute ------------------------------
+def column_block_csr(spec: ShardSpec, parts: int) -> list:
+    """The rank's local CSR split by K/V source block: block r holds the entries whose (global)
+    column lies in [r*S, (r+1)*S), S = spec.kv_rows.  Host only; global column ids are kept."""
+    rp, ci = spec.row_ptr, spec.col_idx
+    n_loc = len(rp) - 1
+    rows = np.repeat(np.arange(n_loc, dtype=np.int64), np.diff(rp))
+    owner = ci // max(spec.kv_rows, 1)
+    out = []
+    for r in range(parts):
+        sel = owner == r
+        cnt = np.bincount(rows[sel], minlength=n_loc)
+        out.append((np.concatenate([[0], np.cumsum(cnt)]).astype(np.int32), np.ascontiguousarray(ci[sel], np.int32)))
+    return out
+
+
+def ring_schedule(rank: int, world: int) -> list:
+    """Round t = 1 .. world-1 of the ring exchange: (send to, receive from) = (rank+t, rank-t).
+    After round t this rank holds block (rank - t) % world; its own block needs no transfer."""
+    return [((rank + t) % world, (rank - t) % world) for t in range(1, world)]
+
+
+def ring_exchange(KV_full, S: int, rank: int, world: int, group=None, on_block=None) -> None:
+    """Replicate every rank's [K||V] shard (rows [r*S, (r+1)*S) of KV_full) with world-1 rounds of
+    paired send/recv; on_block(r) is called (on the current stream) as soon as block r is present,
+    own block first.  NCCL moves device tensors; gloo (CPU test rigs) moves host copies."""
+    import torch
+    import torch.distributed as dist
+    if on_block is not None:
+        on_block(rank)
+    via_host = KV_full.is_cuda and dist.get_backend(group) == "gloo"
+    tv = torch.float16 if KV_full.element_size() == 2 else torch.uint8
+    for dst, src in ring_schedule(rank, world):
+        send = KV_full[rank * S:(rank + 1) * S]
+        recv = KV_full[src * S:(src + 1) * S]
+        if via_host:
+            hs, hr = send.view(tv).cpu(), torch.empty(recv.shape, dtype=tv)
+            reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, hs, dst, group), dist.P2POp(dist.irecv, hr, src, group)])
+            for q in reqs:
+                q.wait()
+            recv.view(tv).copy_(hr)
+        else:
+            reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, send, dst, group),
+                                           dist.P2POp(dist.irecv, recv, src, group)])
+            for q in reqs:
+                q.wait()
+        if on_block is not None:
+            on_block(src)
+
+
+class OverlappedShard:
+    """One rank of the overlapped multi-GPU pass: the K/V blocks arrive over a side stream in ring
+    order while f3s_attention_partial runs on the blocks already present (own block first, with
+    `reserve_sms` SMs left to the transfers until the last block), then f3s_attention_merge
+    combines the block partials in block order (deterministic; tolerance-equal to the one-GPU
+    result, not bitwise: the blocks change where the online softmax rescales)."""
+
+    def __init__(self, spec: ShardSpec, heads: int, d: int, dtype, *, device=None, reserve_sms: int = 16,
+                 group=None):
+        import torch
+
+        from . import f3s
+        assert not spec.batched, "batched mode has no exchange"
+        self.spec, self.H, self.d, self.group = spec, heads, d, group
+        self.world, self.rank = spec.world, spec.rank
+        self.dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.tdt = dtype
+        self.code = {torch.float16: f3s.FP16, torch.bfloat16: f3s.BF16, torch.float8_e4m3fn: f3s.E4M3}[dtype]
+        n_loc = spec.row_end - spec.row_begin
+        self.n_loc = n_loc
+        self.plans = []
+        for rp, ci in column_block_csr(spec, self.world):
+            self.plans.append(f3s.plan_rows(torch.from_numpy(rp).to(self.dev),
+                                            torch.from_numpy(ci if len(ci) else np.zeros(1, np.int32)).to(self.dev),
+                                            n_loc, spec.n_cols))
+        S = spec.kv_rows
+        self.KV = torch.empty((self.world * S, 2, heads, d), dtype=dtype, device=self.dev)
+        self.Op = torch.empty((self.world, max(n_loc, 1), heads, d), dtype=torch.float32, device=self.dev)
+        self.mlp = torch.empty((self.world, max(n_loc, 1), heads, 2), dtype=torch.float32, device=self.dev)
+        self.comm = torch.cuda.Stream(device=self.dev)
+        sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
+        self.cap = max(1, sms - reserve_sms) if self.world > 1 else 0
+
+    def own_block(self):
+        """The rows of KV this rank fills before run() (its padded [K||V] shard)."""
+        S = self.spec.kv_rows
+        return self.KV[self.rank * S:(self.rank + 1) * S]
+
+    def run(self, Q, O, scale: float) -> None:
+        import torch
+
+        from . import f3s
+        comp = torch.cuda.current_stream(self.dev)
+        es = self.KV.element_size()
+        kv = self.KV.data_ptr()
+        H, d = self.H, self.d
+        arrived = []
+
+        def partial(r, cap):
+            if self.n_loc == 0:
+                return
+            f3s.attention_partial_raw(self.plans[r], Q.data_ptr(), kv, kv + H * d * es, 2 * H * d,
+                                      self.Op[r].data_ptr(), self.mlp[r].data_ptr(), scale, H, d, self.code, cap,
+                                      comp.cuda_stream)
+
+        events = {}
+
+        def on_block(r):  # block r is present once the comm stream reaches this point
+            if r == self.rank:
+                return
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.dev))
+            events[r] = ev
+            arrived.append(r)
+
+        self.comm.wait_stream(comp)          # the own shard (uploaded on comp) is in place
+        partial(self.rank, self.cap)         # own block first: no transfer needed
+        with torch.cuda.stream(self.comm):
+            ring_exchange(self.KV, self.spec.kv_rows, self.rank, self.world, self.group, on_block)
+        for i, r in enumerate(arrived):
+            comp.wait_event(events[r])
+            partial(r, self.cap if i < len(arrived) - 1 else 0)
+        if self.n_loc:
+            f3s.attention_merge(self.Op, self.mlp, O, stream=comp)

@@ -48,6 +48,9 @@ _lib.f3s_plan_export.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.f3s_plan_set_split.argtypes = [_vp, _i32]
 _lib.f3s_attention.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_kv.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _f32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_strided.argtypes = [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _f32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_partial.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_merge.argtypes = [_i32, _vp, _vp, _i64, _i32, _i32, _vp, _vp]
 _lib.f3s_attention_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_trace.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]
 _lib.f3s_attention_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
@@ -62,12 +65,14 @@ _lib.f3s_status_string.restype = ctypes.c_char_p
 _lib.f3s_last_error.restype = ctypes.c_char_p
 _lib.f3s_launch_count.restype = _i64
 for _name in ("f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
-              "f3s_attention", "f3s_attention_kv", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows",
+              "f3s_attention", "f3s_attention_kv", "f3s_attention_strided", "f3s_attention_partial",
+              "f3s_attention_merge", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows",
               "f3s_partition_at", "f3s_attention_backward", "f3s_attention_host_async"):
     getattr(_lib, _name).restype = _i32
 
 EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
-            "f3s_attention", "f3s_attention_kv", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host",
+            "f3s_attention", "f3s_attention_kv", "f3s_attention_strided", "f3s_attention_partial",
+            "f3s_attention_merge", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host",
             "f3s_partition_rows", "f3s_partition_at",
             "f3s_attention_backward", "f3s_attention_host_async", "f3s_default_split_chunks",
             "f3s_status_string", "f3s_last_error", "f3s_launch_count"]
@@ -235,6 +240,49 @@ def attention_kv_raw(p: Plan, q_ptr: int, k_ptr: int, v_ptr: int, kv_row_stride:
     """Pointer-level f3s_attention_kv (bench loops)."""
     _check(_lib.f3s_attention_kv(p.handle, q_ptr, k_ptr, v_ptr, int(kv_row_stride), o_ptr, float(scale), heads, d,
                                  dtype, stream), "f3s_attention_kv")
+
+
+def attention_qkv(p: Plan, QKV, O=None, *, scale: float = 1.0, stream=None):
+    """f3s_attention_strided on a packed projection output QKV [n, 3, H, d] (Q, K, V = QKV[:, 0/1/2]):
+    the fused pass reads the three row-strided operands in place (no split copies)."""
+    import torch
+    if QKV.dim() != 4 or QKV.shape[1] != 3 or not QKV.is_contiguous() or not QKV.is_cuda:
+        raise ValueError("attention_qkv: QKV must be a contiguous CUDA [n, 3, heads, d] tensor")
+    inf = p.info()
+    n, _, H, d = QKV.shape
+    if n != inf["n_rows"] or n < inf["n_cols"]:
+        raise ValueError(f"attention_qkv: {n} rows for a plan of {inf['n_rows']} x {inf['n_cols']}")
+    if O is None:
+        O = torch.empty((n, H, d), dtype=torch.float32, device=QKV.device)
+    elif O.dtype != torch.float32 or tuple(O.shape) != (n, H, d) or not O.is_contiguous():
+        raise ValueError("attention_qkv: O must be float32 [n, heads, d]")
+    es, base = QKV.element_size(), QKV.data_ptr()
+    _check(_lib.f3s_attention_strided(p.handle, base, 3 * H * d, base + H * d * es, base + 2 * H * d * es, 3 * H * d,
+                                      O.data_ptr(), float(scale), H, d, _dtype_code(QKV), _stream(stream)),
+           "f3s_attention_strided")
+    return O
+
+
+def attention_partial_raw(p: Plan, q_ptr: int, k_ptr: int, v_ptr: int, kv_row_stride: int, o_part_ptr: int,
+                          ml_part_ptr: int, scale: float, heads: int, d: int, dtype: int, max_ctas: int,
+                          stream: int) -> None:
+    """f3s_attention_partial: one column block's unnormalised O and per-row (m, l)."""
+    _check(_lib.f3s_attention_partial(p.handle, q_ptr, k_ptr, v_ptr, int(kv_row_stride), o_part_ptr, ml_part_ptr,
+                                      float(scale), heads, d, dtype, int(max_ctas), stream), "f3s_attention_partial")
+
+
+def attention_merge(O_parts, ml_parts, O=None, stream=None):
+    """f3s_attention_merge of [parts, n, H, d] partials and [parts, n, H, 2] (m, l) into O [n, H, d]."""
+    import torch
+    if O_parts.dtype != torch.float32 or ml_parts.dtype != torch.float32 or not O_parts.is_contiguous() \
+            or not ml_parts.is_contiguous() or tuple(ml_parts.shape) != tuple(O_parts.shape[:3]) + (2,):
+        raise ValueError("attention_merge: float32 contiguous O_parts [P, n, H, d] and ml_parts [P, n, H, 2]")
+    P, n, H, d = O_parts.shape
+    if O is None:
+        O = torch.empty((n, H, d), dtype=torch.float32, device=O_parts.device)
+    _check(_lib.f3s_attention_merge(P, O_parts.data_ptr(), ml_parts.data_ptr(), n, H, d, O.data_ptr(), _stream(stream)),
+           "f3s_attention_merge")
+    return O
 
 
 def attention_raw(p: Plan, q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, scale: float, heads: int, d: int,

@@ -205,3 +205,51 @@ def test_shard_split_bound_is_global(dist_mod):
     assert own[0]["split_groups"] == 1 and own[0]["split_chunks"] < 25 < i1["split_chunks"]
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(parts), O1)
+
+
+def _ring_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2505_08098_b200 import dist as f3sdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = fi.chung_lu(2000, 9000, gamma=2.4, max_deg=300, seed=13)
+        n, H, d = g.n_rows, 2, 64
+        Qb, Kb, Vb = make_qkv(n, n, H, d, "fp16", seed=13)
+        spec = f3sdist.shard_spec(g.row_ptr, g.col_idx, rank, world)
+        S = spec.kv_rows
+        KV = torch.zeros((world * S, 2, H, d), dtype=torch.float16)
+        KV[rank * S:(rank + 1) * S] = torch.from_numpy(f3sdist.kv_shard(spec, Kb, Vb, n).view(np.float16))
+        order = []
+        f3sdist.ring_exchange(KV, S, rank, world, on_block=order.append)
+        got = KV.numpy().view(np.uint16)[:n]
+        ok = bool(np.array_equal(got[:, 0], Kb) and np.array_equal(got[:, 1], Vb))
+        # the column blocks of the local CSR partition its entries by K/V owner
+        blocks = f3sdist.column_block_csr(spec, world)
+        part_ok = sum(len(b[1]) for b in blocks) == len(spec.col_idx) and all(
+            len(ci) == 0 or (ci.min() >= r * S and ci.max() < (r + 1) * S) for r, (_, ci) in enumerate(blocks))
+        q.put((rank, ok, order, bool(part_ok)))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ring_exchange_order_and_blocks(dist_mod, world):
+    """f2 host logic: the ring exchange (world-1 rounds of paired send/recv) replicates every
+    [K||V] shard bit for bit, announces the own block first and then block rank-t in round t, and
+    the column-block CSRs split the local entries by owner."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ring_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, order, part_ok in res:
+        assert ok and part_ok
+        assert order == [rank] + [(rank - t) % world for t in range(1, world)]
