@@ -12,7 +12,44 @@ from typing import Callable
 
 import numpy as np
 
-from . import CSR, chung_lu, dcsbm, molecules, values
+from . import CSR, chung_lu, dcsbm, dcsbm_w, molecules, values
+
+# Tab.tcb_deciles, Reddit: min / decile boundaries / max of TCBs (16x8) per row window
+REDDIT_DECILES = (4, 46, 88, 135, 190, 265, 367, 503, 718, 1113.5, 9857)
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+
+
+def _uniform(count: int, seed: int) -> np.ndarray:
+    """u[i] in [0, 1): 53 bits of the i-th output of a splitmix64 stream started at `seed`."""
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + (np.arange(count, dtype=np.uint64) + np.uint64(1)) * _GOLDEN
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def reddit_weights(n: int, *, seed: int, jitter: float, tail_alpha: float) -> np.ndarray:
+    """Node weights whose 16-row windows follow the paper's TCB/RW deciles.
+
+    Each window k gets a target t_k = Q(u_k) with u_k = (rank_k + 0.5) / R, ranks a seeded
+    permutation (so every decile holds exactly R/10 windows); Q is log-linear between the
+    decile boundaries and a Pareto(tail_alpha) truncated at the table's maximum in the last
+    decile.  A row's weight is t_k * exp(jitter * z), z ~ N(0, 1) from a seeded stream."""
+    R = (n + 15) // 16
+    rank = np.argsort(_uniform(R, seed ^ 0x77), kind="stable").argsort(kind="stable")
+    u = (rank + 0.5) / R
+    kn = np.log(np.asarray(REDDIT_DECILES, dtype=np.float64))
+    i = np.minimum((u * 10).astype(np.int64), 9)
+    f = u * 10 - i
+    t = np.exp(kn[i] + f * (kn[np.minimum(i + 1, 10)] - kn[i]))
+    lo, hi = REDDIT_DECILES[9], REDDIT_DECILES[10]
+    tail = i == 9
+    c = 1.0 - (lo / hi) ** tail_alpha
+    t[tail] = lo * (1.0 - f[tail] * c) ** (-1.0 / tail_alpha)
+    u1, u2 = _uniform(n, seed ^ 0x99), _uniform(n, seed ^ 0xAA)
+    z = np.sqrt(-2.0 * np.log1p(-u1)) * np.cos(2.0 * np.pi * u2)  # Box-Muller
+    return t[np.arange(n) // 16] * np.exp(jitter * z)
 
 
 @dataclass

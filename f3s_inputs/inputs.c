@@ -321,10 +321,12 @@ int f3si_chung_lu(int32_t n, int64_t n_pairs, int32_t directed, double gamma, do
  * weight inside u's community, otherwise globally.  Symmetric, no self-loops, IDs not
  * permuted (communities stay contiguous, which is what gives Reddit its shared columns).
  */
+static int dcsbm_core(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, double* wn, uint64_t seed,
+                      int32_t** row_ptr, int32_t** col_idx, int64_t* nnz);
+
 int f3si_dcsbm(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, double gamma, double max_deg,
                uint64_t seed, int32_t** row_ptr, int32_t** col_idx, int64_t* nnz) {
     if (n <= 1 || comm_size < 2 || n_pairs < 0) return 1;
-    int32_t n_comm = (n + comm_size - 1) / comm_size;
     double* w = (double*)malloc((size_t)n * sizeof(double));
     if (!w) return 2;
     powerlaw_weights(w, n, gamma, max_deg, 2.0 * (double)n_pairs);
@@ -334,6 +336,28 @@ int f3si_dcsbm(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, double 
     for (int32_t i = 0; i < n; ++i) wn[q[i]] = w[i];
     free(q);
     free(w);
+    return dcsbm_core(n, n_pairs, comm_size, mu, wn, seed, row_ptr, col_idx, nnz);
+}
+
+/*
+ * Same block model with caller-given node weights w[n] (expected-degree shape; only ratios
+ * matter).  The Reddit-shaped workload passes weights that are constant-ish within each
+ * 16-row window and drawn per window from the paper's TCB/RW decile table,
+ * which is what gives the row windows their long-tailed widths.
+ */
+int f3si_dcsbm_w(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, const double* w, uint64_t seed,
+                 int32_t** row_ptr, int32_t** col_idx, int64_t* nnz) {
+    if (n <= 1 || comm_size < 2 || n_pairs < 0 || !w) return 1;
+    double* wn = (double*)malloc((size_t)n * sizeof(double));
+    if (!wn) return 2;
+    memcpy(wn, w, (size_t)n * sizeof(double));
+    return dcsbm_core(n, n_pairs, comm_size, mu, wn, seed, row_ptr, col_idx, nnz);
+}
+
+/* takes ownership of wn */
+static int dcsbm_core(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, double* wn, uint64_t seed,
+                      int32_t** row_ptr, int32_t** col_idx, int64_t* nnz) {
+    int32_t n_comm = (n + comm_size - 1) / comm_size;
     alias_t glob;
     if (alias_build(&glob, wn, n, 0)) return 2;
     alias_t* loc = (alias_t*)malloc((size_t)n_comm * sizeof(alias_t));

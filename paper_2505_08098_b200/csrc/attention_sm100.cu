@@ -242,7 +242,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     // [0 slot written, 1 gathers issued, 2 MMA1 issued, 3 S seen, 4 P written, 5 MMA2 issued, 6 O seen, 7 item stored]
     auto stamp = [&](int32_t c, int ev) {
         if (kDiag && trace != nullptr && c < trace_chunks)
-            trace[((size_t)blockIdx.x * trace_chunks + c) * 8 + ev] = globaltimer_ns();
+            trace[((size_t)blockIdx.x * trace_chunks + c) * 16 + ev] = globaltimer_ns();
     };
     // profile mode (trace_chunks == 0): each role accumulates SM cycles spent per phase in
     // registers and writes trace[cta][64] once at the end (no stores on the hot path)
@@ -332,7 +332,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     const int rows = w > 0 ? min(chunk_rows, w - chunk_rows * j) : 0;
                     const int s = seq % C::kNS;
                     if (lane == 0) {
-                        mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+                        mbar_wait_lazy(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
                         lap(0);
                         Slot& sl = slots[s];
                         sl.rw = k;
@@ -363,7 +363,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             // producer, loaders and MMA warps stop at the first.  rows = -1 - w.
             for (int w = 0; w < C::kSoftmaxWGs; ++w, ++seq) {
                 const int s = seq % C::kNS;
-                mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+                mbar_wait_lazy(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
                 slots[s].rows = -1 - w;
                 mbar_arrive(bar(B::idxfull(s)));
             }
@@ -378,8 +378,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         uint32_t headk = 0, headv = 0;
         for (;;) {
             const int s = seq % C::kNS;
-            mbar_wait(bar(B::idxfull(s)), (seq / C::kNS) & 1);
+            mbar_wait_lazy(bar(B::idxfull(s)), (seq / C::kNS) & 1);
             lap(0);
+            if (lane == 0) stamp(seq, 8);
             Slot& sl = slots[s];
             const int rows = sl.rows;
             if (rows < 0) {
@@ -391,7 +392,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             const int flags = sl.flags, k = sl.rw, h = sl.head, qs = sl.qslot;
             if (flags & 1) {  // Alg.1 l.5: Q_i for the item's first chunk
-                mbar_wait(bar(B::qempty(qs)), ((flags >> 2) & 1) ^ 1);
+                mbar_wait_lazy(bar(B::qempty(qs)), ((flags >> 2) & 1) ^ 1);
                 lap(1);
                 if (lane == 0) {
                     mbar_arrive_expect_tx(bar(B::qfull(qs)), C::kQBytes);
@@ -424,11 +425,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         head = off + tile;
                         return off;
                     }
-                    mbar_wait(bar(bar_base + tail % C::kNS), (tail / C::kNS) & 1);
+                    mbar_wait_lazy(bar(bar_base + tail % C::kNS), (tail / C::kNS) & 1);
                     ++tail;
                 }
             };
             const uint32_t offk = alloc(headk, tailk, regk, (uint32_t)C::kRingK, B::kempty(0));
+            if (lane == 0) stamp(seq, 12);
             const uint32_t offv = alloc(headv, tailv, regv, (uint32_t)C::kRingV, B::empty(0));
             lap(2);
             __syncwarp();
@@ -440,7 +442,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             __syncwarp();
             lap(3);
-            if (lane == 0) mbar_arrive(bar(B::rfull(s)));  // ring space assigned: loaders may gather
+            if (lane == 0) { stamp(seq, 9); mbar_arrive(bar(B::rfull(s))); }  // ring space assigned: loaders may gather
             ++seq;
         }
         __syncwarp();
@@ -458,7 +460,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         int32_t seq = 0;
         for (;;) {
             const int s = seq % C::kNS;
-            mbar_wait(bar(B::rfull(s)), (seq / C::kNS) & 1);
+            mbar_wait_lazy(bar(B::rfull(s)), (seq / C::kNS) & 1);
+            if (lw == 0 && lane == 0) stamp(seq, 10);
             const Slot& sl = slots[s];
             const int rows = sl.rows;
             const uint32_t kfb = bar(B::kfull(s)), vfb = bar(B::vfull(s));
@@ -507,6 +510,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             for (int32_t n1 = 0;; ++n1) {
                 const int s = n1 % C::kNS, b = n1 % C::kSB;
                 mbar_wait(bar(B::kfull(s)), (n1 / C::kNS) & 1);  // K_c landed
+                if (lane == 0) stamp(n1, 11);
                 const Slot& sl = slots[s];
                 const int rows = sl.rows, flags = sl.flags, qslot = sl.qslot, roff = sl.ring_off;
                 if (rows < 0) break;
@@ -546,7 +550,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const int rows = slots[s].rows;
                 if (rows < 0) break;
                 mbar_wait(bar(B::pfull(b)), (n2 / C::kSB) & 1);  // P_c written
+                if (lane == 0) stamp(n2, 13);
                 mbar_wait(bar(B::vfull(s)), (n2 / C::kNS) & 1);  // V_c landed
+                if (lane == 0) stamp(n2, 14);
                 tc_fence_after();
                 if (rows > 0 && !(expt & 2)) {
                     const uint64_t a0 = dV + ((sb + C::oRingV + slots[s].pad) >> 4);
@@ -662,7 +668,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (p == 0) lap(6);
             // P_b / corr_b are free once the correction group consumed chunk seq - kSB
             mbar_wait(bar(B::pempty(b)), bph ^ 1);
-            if (p == 0) lap(4);
+            if (p == 0) { lap(4); stamp(seq, 15); }
             if constexpr (EB == 1) {
                 // E cast to e4m3 (satfinite, round to nearest even) into the K-major 128B-swizzled
                 // [16 x 128] B tile: byte p of row i, 16-byte chunk (p >> 4) ^ (i & 7)
@@ -735,8 +741,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             tc_fence_after();
             if (lead) {
                 if (kDiag && trace != nullptr && seq < trace_chunks) {
-                    trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 3] = corr[b].t_s;
-                    trace[((size_t)blockIdx.x * trace_chunks + seq) * 8 + 4] = corr[b].t_p;
+                    trace[((size_t)blockIdx.x * trace_chunks + seq) * 16 + 3] = corr[b].t_s;
+                    trace[((size_t)blockIdx.x * trace_chunks + seq) * 16 + 4] = corr[b].t_p;
                 }
                 stamp(seq, 6);
                 lap(1);

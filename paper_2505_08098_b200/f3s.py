@@ -308,12 +308,12 @@ def attention_backward(p: Plan, Q, K, V, dO, *, scale: float, stream=None):
 
 def attention_trace(p: Plan, Q, K, V, O, *, scale: float, trace_chunks: int = 4096, grid: int = 0,
                     variant: str | int = "default", stream=None):
-    """Run the default kernel with F3S_TRACE on; returns uint64 [grid, trace_chunks, 8] globaltimer stamps."""
+    """Run the default kernel with F3S_TRACE on; returns uint64 [grid, trace_chunks, 16] globaltimer stamps."""
     import torch
     import math
     H, d = Q.shape[1], Q.shape[2]
     g = grid or torch.cuda.get_device_properties(Q.device).multi_processor_count * 2  # upper bound on the grid
-    tr = torch.zeros((g, max(trace_chunks, 8), 8), dtype=torch.int64, device=Q.device)
+    tr = torch.zeros((g, max(trace_chunks, 16), 16), dtype=torch.int64, device=Q.device)
     v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
     _check(_lib.f3s_attention_trace(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), O.data_ptr(), float(scale), H, d,
                                     _dtype_code(Q), v, tr.data_ptr(), trace_chunks, grid, _stream(stream)),
