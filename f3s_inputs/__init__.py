@@ -45,7 +45,7 @@ def _load():
                                       ctypes.c_double, i32, i32, i32, u64, pp, pp, ctypes.POINTER(i64)]
         lib.f3si_dcsbm.argtypes = [i32, i64, i32, ctypes.c_double, ctypes.c_double, ctypes.c_double, u64,
                                    pp, pp, ctypes.POINTER(i64)]
-        lib.f3si_dcsbm_w.argtypes = [i32, i64, i32, ctypes.c_double, vp, u64, pp, pp, ctypes.POINTER(i64)]
+        lib.f3si_dcsbm_w.argtypes = [i32, i64, i32, vp, vp, u64, pp, pp, ctypes.POINTER(i64)]
         lib.f3si_molecules.argtypes = [i32, i32, i32, i32, u64, pp, pp, ctypes.POINTER(i64),
                                        ctypes.POINTER(i32), pp]
         lib.f3si_random_csr.argtypes = [i32, i32, i32, i32, i32, i32, u64, pp, pp, ctypes.POINTER(i64)]
@@ -103,13 +103,15 @@ def dcsbm(n: int, n_pairs: int, *, comm_size: int, mu: float, gamma: float, max_
     return _csr_from(rp, ci, nnz, n, n)
 
 
-def dcsbm_w(n: int, n_pairs: int, *, comm_size: int, mu: float, weights: np.ndarray, seed: int) -> CSR:
-    """Block model with caller-given node weights (expected-degree shape)."""
+def dcsbm_w(n: int, n_pairs: int, *, comm_size: int, mu, weights: np.ndarray, seed: int) -> CSR:
+    """Block model with caller-given node weights (expected-degree shape) and local fraction mu
+    (a scalar or one value per node)."""
     lib = _load()
     w = np.ascontiguousarray(weights, dtype=np.float64)
+    m = np.ascontiguousarray(np.broadcast_to(np.asarray(mu, dtype=np.float64), (n,)))
     assert w.shape == (n,)
     rp, ci, nnz = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
-    rc = lib.f3si_dcsbm_w(n, n_pairs, comm_size, mu, w.ctypes.data, seed, ctypes.byref(rp), ctypes.byref(ci),
+    rc = lib.f3si_dcsbm_w(n, n_pairs, comm_size, m.ctypes.data, w.ctypes.data, seed, ctypes.byref(rp), ctypes.byref(ci),
                           ctypes.byref(nnz))
     if rc:
         raise RuntimeError(f"f3si_dcsbm_w failed ({rc})")

@@ -321,8 +321,8 @@ int f3si_chung_lu(int32_t n, int64_t n_pairs, int32_t directed, double gamma, do
  * weight inside u's community, otherwise globally.  Symmetric, no self-loops, IDs not
  * permuted (communities stay contiguous, which is what gives Reddit its shared columns).
  */
-static int dcsbm_core(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, double* wn, uint64_t seed,
-                      int32_t** row_ptr, int32_t** col_idx, int64_t* nnz);
+static int dcsbm_core(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, const double* mu_node, double* wn,
+                      uint64_t seed, int32_t** row_ptr, int32_t** col_idx, int64_t* nnz);
 
 int f3si_dcsbm(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, double gamma, double max_deg,
                uint64_t seed, int32_t** row_ptr, int32_t** col_idx, int64_t* nnz) {
@@ -336,7 +336,7 @@ int f3si_dcsbm(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, double 
     for (int32_t i = 0; i < n; ++i) wn[q[i]] = w[i];
     free(q);
     free(w);
-    return dcsbm_core(n, n_pairs, comm_size, mu, wn, seed, row_ptr, col_idx, nnz);
+    return dcsbm_core(n, n_pairs, comm_size, mu, NULL, wn, seed, row_ptr, col_idx, nnz);
 }
 
 /*
@@ -351,12 +351,12 @@ int f3si_dcsbm_w(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, const
     double* wn = (double*)malloc((size_t)n * sizeof(double));
     if (!wn) return 2;
     memcpy(wn, w, (size_t)n * sizeof(double));
-    return dcsbm_core(n, n_pairs, comm_size, mu, wn, seed, row_ptr, col_idx, nnz);
+    return dcsbm_core(n, n_pairs, comm_size, mu, NULL, wn, seed, row_ptr, col_idx, nnz);
 }
 
-/* takes ownership of wn */
-static int dcsbm_core(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, double* wn, uint64_t seed,
-                      int32_t** row_ptr, int32_t** col_idx, int64_t* nnz) {
+/* takes ownership of wn; mu_node (optional) gives each first endpoint its own local fraction */
+static int dcsbm_core(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, const double* mu_node, double* wn,
+                      uint64_t seed, int32_t** row_ptr, int32_t** col_idx, int64_t* nnz) {
     int32_t n_comm = (n + comm_size - 1) / comm_size;
     alias_t glob;
     if (alias_build(&glob, wn, n, 0)) return 2;
@@ -380,7 +380,7 @@ static int dcsbm_core(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, 
             uint64_t z2 = rng_at(seed, 3 * (base + (uint64_t)i) + 1);
             uint64_t z3 = rng_at(seed, 3 * (base + (uint64_t)i) + 2);
             uint64_t u = (uint64_t)alias_draw(&glob, z1);
-            uint64_t v = (u01(z3) < mu) ? (uint64_t)alias_draw(&loc[u / (uint64_t)comm_size], z2)
+            uint64_t v = (u01(z3) < (mu_node ? mu_node[u] : mu)) ? (uint64_t)alias_draw(&loc[u / (uint64_t)comm_size], z2)
                                          : (uint64_t)alias_draw(&glob, z2);
             if (u > v) { uint64_t t = u; u = v; v = t; }
             keys[m + i] = (u == v) ? ~0ULL : ((u << 32) | v);

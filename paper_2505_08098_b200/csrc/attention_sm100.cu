@@ -4,18 +4,17 @@
 // re-designed for Blackwell:
 //
 //   * work items (window or piece of a split window, head group) in LPT order from a
-//     persistent queue; one CTA per SM, 20 warps with fixed roles;
-//   * warp 2 (index): pops items and bulk-copies each chunk's column ids and 16-bit row masks
-//     (the BSB bitmap) into a chunk slot;
-//   * warp 0 (producer): TMA-loads Q_w (16 x d per head, Alg.1 l.5) and allocates each chunk's
-//     K and V tiles in two shared-memory byte rings;
-//   * warps 3-6 (loaders): gather the chunk's K and V rows (sptd, l.7-8) with 16-byte cp.async
-//     into 128B-swizzled UMMA tiles;
-//   * warp 1 (MMA1) and warp 7 (MMA2): swap-AB contractions on tcgen05 with TMEM accumulators,
+//     persistent queue; one CTA per SM, warps with fixed roles;
+//   * warp 0 (index): pops items, bulk-copies each chunk's column ids and 16-bit row masks (the
+//     BSB bitmap) into a chunk slot and TMA-loads each item's Q_w (16 x d per head, l.5);
+//   * loader warps: gather the chunk's K and V rows (sptd, l.7-8) with 16-byte cp.async into
+//     128B-swizzled UMMA tiles: chunk n uses K tile n % kNK and V tile n % kNV (fixed slots, freed
+//     by the MMA that read them);
+//   * warp 1 (MMA1) and warp 2 (MMA2): swap-AB contractions on tcgen05 with TMEM accumulators,
 //       MMA1  S^T[C x 16]  = K_c[C x d] . Q_w^T        (SDDMM, l.13; M = 128, N = 16)
 //       MMA2  O^T[d x 16]  = V_c^T[d x C] . P^T[C x 16] (SpMM,  l.22; M = d,   N = 16)
 //     each sleeping in mbarrier try_wait on the barriers of its next instruction;
-//   * two softmax warpgroups (alternate items): tcgen05.ld S^T (lane = compacted column, whose
+//   * two softmax warpgroups (alternate chunks): tcgen05.ld S^T (lane = compacted column, whose
 //     mask is the bitmap row of l.14), chunk row max by warp shuffles (+ a 4-warp combine), online
 //     softmax in fp32 with exp2 (l.16-18), P cast to the input dtype into shared memory (l.19);
 //   * correction warpgroup: folds each chunk's O^T into fp32 registers with the running rescale
@@ -73,7 +72,9 @@ struct Cfg {
 #endif
     static constexpr int kSB = HG == 4 ? 4 : F3S_KSB;
     static_assert(kSB % kSoftmaxWGs == 0, "S/P/O buffers are owned by one warpgroup each");
-    static constexpr int kNS = D == 128 ? 20 : 22;   // chunk slots (ids, masks, descriptor, barriers)
+    static constexpr int kMaxRowsBytes = (kMaxRows / 8) * kGroupBytes;  // one gathered tile (K or V) of a chunk
+    // chunk slots (ids, masks, header, barriers): the index warp fills them ahead of the loaders
+    static constexpr int kNS = kMaxRowsBytes >= 32 * 1024 ? 18 : 16;
     // Q tile slots (items in flight per CTA); fp8 tiles are half as large and carry half the bytes
     // per chunk, so more items are kept in flight
 #ifndef F3S_NQ
@@ -84,51 +85,59 @@ struct Cfg {
     static constexpr int kPBytes = 16 * kMaxRows * EB;
     static constexpr int kNO = HG == 4 ? 1 : 2;      // O staging tiles (16 x HG*D fp32) for the TMA store
     static constexpr int kOBytes = 16 * D * 4 * HG;
-    static constexpr int kTmemCols = HG == 4 ? 512 : kSB <= 4 ? 128 : 256;  // S^T and O^T: kSB x HG buffers of 16 columns each
-    static_assert(2 * 16 * kSB * HG <= kTmemCols, "TMEM columns");
+    // Row sums l_c of the chunk's P (Alg.1 l.17) from the tensor core: MMA2 also multiplies a tile of
+    // ones by P^T, so l_c sums exactly the rounded P that multiplies V (16-bit inputs, one head per
+    // chunk); the softmax then needs no row-sum reduction.  fp8 and head groups sum in registers.
+#ifndef F3S_LSUM_MMA
+#define F3S_LSUM_MMA 0
+#endif
+#ifndef F3S_MAX_REDUX
+#define F3S_MAX_REDUX 1
+#endif
+    static constexpr bool kLsumMMA = F3S_LSUM_MMA && EB == 2 && HG == 1;
+    // TMEM: S^T, O^T (kSB x HG buffers of 16 columns each), then the l_c buffers (kSB x 16)
+    static constexpr int kTmemO = 16 * kSB * HG, kTmemL = 2 * 16 * kSB * HG;
+    static constexpr int kTmemUsed = kTmemL + (kLsumMMA ? 16 * kSB : 0);
+    static constexpr int kTmemCols = kTmemUsed <= 128 ? 128 : kTmemUsed <= 256 ? 256 : 512;
+    static_assert(kTmemUsed <= 512, "TMEM columns");
     static constexpr int kSlotBytes = 32 + 128 * 4 + 128 * 2;  // sizeof(Slot)
     static constexpr int kCorrBytes = 352;                  // sizeof(CorrSlot)
-    static constexpr int kNumBars = 6 * kNS + 2 * kNQ + 5 * kSB;
-    // everything but the two gather rings
+    static constexpr int kNumBars = 4 * kNS + 2 * kNQ + 5 * kSB + 2 * 16;
+    // everything but the gathered tiles
     static constexpr int kFixedBytes = kNQ * kQBytes + kSB * kPBytes + kNO * kOBytes + kNS * kSlotBytes +
-                                       kSB * 4 * 16 * 4 + kSB * kCorrBytes + 2 * kNS * 8 + kNumBars * 8 + 16;
-    // K tiles live until MMA1 completes, V tiles until MMA2 completes: two FIFO rings.  The V ring
-    // (tiles wait there for the softmax and MMA2) takes all the shared memory that is left, in
-    // whole allocation units (16 gathered rows)
-#ifndef F3S_RINGK_KB
-#define F3S_RINGK_KB 64
-#endif
-    static constexpr int kRingK = HG == 4 ? 48 * 1024 : F3S_RINGK_KB * 1024;
-    static constexpr int kRingV = HG == 4 ? 64 * 1024
-                                          : (227 * 1024 - kRingK - kFixedBytes) / (2 * kGroupBytes) * (2 * kGroupBytes);
-    static constexpr int kRingBytes = kRingK + kRingV;
-    static constexpr int oRing = 0;                  // K ring, then V ring
-    static constexpr int oRingV = kRingK;
-    static constexpr int oQ = oRing + kRingBytes;
+                                       kSB * 4 * 16 * 4 + kSB * kCorrBytes + kNumBars * 8 + 16 + (kLsumMMA ? 2048 : 0);
+    // Gathered tiles: fixed-size slots of one full chunk (128 rows) each, chunk n in K tile n % kNK
+    // (free again once MMA1 completed) and V tile n % kNV (free once MMA2 completed).  V tiles wait
+    // for the softmax and MMA2, so they take all the shared memory that is left.
+    static constexpr int kNK = kMaxRowsBytes >= 32 * 1024 ? 2 : HG == 4 ? 3 : 4;
+    static constexpr int kNVmax = (227 * 1024 - kNK * kMaxRowsBytes - kFixedBytes) / kMaxRowsBytes;
+    static constexpr int kNV = kNVmax > 8 ? 8 : kNVmax;
+    static_assert(kNV >= 2, "two V tiles at least");
+    static constexpr int oK = 0;                     // K tiles, then V tiles
+    static constexpr int oV = kNK * kMaxRowsBytes;
+    static constexpr int kTileBytes = (kNK + kNV) * kMaxRowsBytes;
+    static constexpr int oQ = kTileBytes;
     static constexpr int oP = oQ + kNQ * kQBytes;
     static constexpr int oOst = oP + kSB * kPBytes;
     static constexpr int oSlot = oOst + kNO * kOBytes;
     static constexpr int oRed = oSlot + kNS * kSlotBytes;  // float [kSB][4][16] chunk row-max partials
     static constexpr int oCorr = oRed + kSB * 4 * 16 * 4;  // CorrSlot [kSB]
-    static constexpr int oReg = oCorr + kSB * kCorrBytes;   // int2 [2][kNS] ring regions (K, V)
-    static constexpr int oBar = oReg + 2 * kNS * 8;
+    static constexpr int oBar = oCorr + kSB * kCorrBytes;
     static constexpr int oTmem = oBar + kNumBars * 8;
-    static constexpr int kSmemBytes = oTmem + 16;
+    static constexpr int oOnes = (oTmem + 16 + 1023) / 1024 * 1024;  // one 128B-swizzle atom of ones (A of the l_c MMA)
+    static constexpr int kSmemBytes = kLsumMMA ? oOnes + 1024 : oTmem + 16;
     static constexpr int kCtasPerSm = 1;
-    // MMA1 and MMA2 are issued by two warps that each sleep on their own barriers (mbarrier
-    // try_wait wakes ~60 cycles after the arrive); one warp polling four barriers with test_wait
-    // (~150 cycles each) reacted 0.9-2.8 us late (measured)
-    static constexpr int kLoaderWarps = 4;           // cp.async gather warps (20 warps in all keeps 96 registers)
-    static constexpr int kMma2Warp = 3 + kLoaderWarps;
-    static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps + 1,
-                         kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
-    static constexpr int kThreads = 32 * (kCorr0 + 4);  // control, MMA, index, loaders, softmax, correction
+    // warp roles: 0 index (work queue, chunk slots, Q tiles), 1 MMA1, 2 MMA2 (each sleeping on its
+    // own barriers: try_wait wakes ~60 cycles after the arrive), kLoaderWarps cp.async gather warps,
+    // two softmax warpgroups, the correction warpgroup
+#ifndef F3S_NLOAD
+#define F3S_NLOAD 6
+#endif
+    static constexpr int kLoaderWarps = F3S_NLOAD;
+    static constexpr int kMma2Warp = 2;
+    static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps, kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
+    static constexpr int kThreads = 32 * (kCorr0 + 4);
     static constexpr int kBatch = 8;                 // items fetched per queue round trip
-    static_assert(kRingK >= (kMaxRows / 8) * kGroupBytes && kRingV >= (kMaxRows / 8) * kGroupBytes,
-                  "each ring must hold one full tile");
-    // MMA1 (M = 128) may read up to 12 row groups past a short tile; those lanes are masked
-    // (the K ring is followed by the V ring, the V ring by Q/P/slots: valid shared memory)
-    static_assert(oRed >= kRingBytes + 12 * kGroupBytes && kRingV >= 12 * kGroupBytes, "over-read pad");
     static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 };
 
@@ -145,25 +154,25 @@ template <int D, int HG, int EB = 2> struct Bars {
     __host__ __device__ static constexpr int pfull(int b) { return kB0 + C::kSB + b; }
     __host__ __device__ static constexpr int ofull(int b) { return kB0 + 2 * C::kSB + b; }
     __host__ __device__ static constexpr int pempty(int b) { return kB0 + 3 * C::kSB + b; }
-    __host__ __device__ static constexpr int rfull(int s) { return kB0 + 4 * C::kSB + s; }
-    __host__ __device__ static constexpr int kempty(int s) { return kB0 + 4 * C::kSB + C::kNS + s; }
     // S^T buffer b may be overwritten by MMA1: its owner warpgroup's 4 warps read it (and the
     // row-max partials) for the buffer's previous chunk
-    __host__ __device__ static constexpr int sfree(int b) { return kB0 + 4 * C::kSB + 2 * C::kNS + b; }
+    __host__ __device__ static constexpr int sfree(int b) { return kB0 + 4 * C::kSB + b; }
+    // gathered tile slots: K tile t free (MMA1 that read it completed), V tile t free (MMA2)
+    __host__ __device__ static constexpr int ktfree(int t) { return kB0 + 5 * C::kSB + t; }
+    __host__ __device__ static constexpr int vtfree(int t) { return kB0 + 5 * C::kSB + 16 + t; }
 };
 
-// One chunk of one work item: written by the index warp (ids/masks by cp.async.bulk), the
-// ring offset by the producer; read by the MMA and softmax warps.
+// One chunk of one work item: written by the index warp (header; ids/masks by cp.async.bulk);
+// read by the loader, MMA and softmax warps.
 struct __align__(16) Slot {
     int32_t rw;        // row window k
     int32_t head;      // head h
     int32_t rows;      // valid compacted columns in this chunk (0 for an empty RW; < 0: stop)
-    int32_t ring_off;  // byte offset of the K tile in the ring (V tile follows)
+    int32_t reserved0;
     int32_t qslot;
     int32_t flags;     // bit0 first chunk of item, bit1 last chunk, bit2 Q-slot phase, bits 8..31 split:
                        // 0, or 1 + global piece index of a split row window (Plan::meta_sub)
-    int32_t ralloc;    // rows allocated in the ring (multiple of 16)
-    int32_t pad;       // byte offset of the V tile in the V ring
+    int32_t reserved1, reserved2;
     int32_t cols[128];     // gathered row ids (tail repeats the last column)
     uint16_t masks[128];   // 16-bit row masks (bitmap)
 };
@@ -208,6 +217,11 @@ struct OpAdd { __device__ float operator()(float a, float b) const { return a + 
 template <typename T> __device__ __forceinline__ uint32_t pack2(float lo, float hi);
 template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) { return pack_f16x2(lo, hi); }
 template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) { return pack_bf16x2(lo, hi); }
+
+template <typename T> __device__ __forceinline__ float round_to(float v);  // v rounded RNE to T, as a float
+template <> __device__ __forceinline__ float round_to<__half>(float v) { return __half2float(__float2half_rn(v)); }
+template <> __device__ __forceinline__ float round_to<__nv_bfloat16>(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+template <> __device__ __forceinline__ float round_to<__nv_fp8_e4m3>(float v) { return v; }
 
 // Running row max starts at a finite floor instead of -inf so that every exponent is well
 // defined without branches: 2^(floor - m) = 0 for a real m, 2^(-inf - m) = 0 for masked scores,
@@ -262,19 +276,25 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     };
 
     // ---- setup -------------------------------------------------------------------------------
-    // Ring bytes that no gather overwrites are read by MMA2 (rows between the last gathered
-    // 4-row group and the 16-row MMA step, weighted by P = 0): they must be finite, so zero them.
-    for (int i = threadIdx.x; i < C::kRingBytes / 16; i += blockDim.x)
-        reinterpret_cast<int4*>(smem + C::oRing)[i] = make_int4(0, 0, 0, 0);
+    // Tile rows that no gather of the current chunk overwrites (past its last column) are read by
+    // the MMAs with weight 0 (masked / P = 0): they must be finite, so every tile starts zeroed and
+    // only ever holds gathered input rows.
+    for (int i = threadIdx.x; i < C::kTileBytes / 16; i += blockDim.x)
+        reinterpret_cast<int4*>(smem + C::oK)[i] = make_int4(0, 0, 0, 0);
+    if constexpr (C::kLsumMMA) {  // 1.0 in the input format, 1024 bytes
+        const uint32_t one2 = std::is_same<T, __nv_bfloat16>::value ? 0x3F803F80u : 0x3C003C00u;
+        for (int i = threadIdx.x; i < 64; i += blockDim.x)
+            reinterpret_cast<uint4*>(smem + C::oOnes)[i] = make_uint4(one2, one2, one2, one2);
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::kNS; ++s) {
             mbar_init(bar(B::idxfull(s)), 1);
             mbar_init(bar(B::kfull(s)), 32 * C::kLoaderWarps);  // one cp.async completion per loader lane
             mbar_init(bar(B::vfull(s)), 32 * C::kLoaderWarps);
-            mbar_init(bar(B::rfull(s)), 1);
-            mbar_init(bar(B::empty(s)), 1);   // V tile (and the slot) retired: MMA2 done
-            mbar_init(bar(B::kempty(s)), 1);  // K tile retired: MMA1 done
+            mbar_init(bar(B::empty(s)), 1);   // slot retired: MMA2 done
         }
+        for (int t = 0; t < C::kNK; ++t) mbar_init(bar(B::ktfree(t)), 1);
+        for (int t = 0; t < C::kNV; ++t) mbar_init(bar(B::vtfree(t)), 1);
         for (int q = 0; q < C::kNQ; ++q) {
             mbar_init(bar(B::qfull(q)), 1);
             mbar_init(bar(B::qempty(q)), 1);
@@ -302,10 +322,11 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     tc_fence_after();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + C::oTmem);
 
-    if (warp == 2) {
-        // ===== index warp: work queue (LPT order) -> chunk slots =========================
+    if (warp == 0) {
+        // ===== index warp: work queue (LPT order) -> chunk slots and Q tiles ==============
         // kBatch lanes each take one item per queue round trip; per chunk one lane issues two
-        // bulk copies (column ids, masks) straight into the slot.
+        // bulk copies (column ids, masks) straight into the slot, and at an item's first chunk the
+        // TMA load of Q_w (16 x d per head, Alg.1 l.5) into the item's Q slot.
         int32_t seq = 0, qseq = 0;
         bool done = false;
         while (!done) {
@@ -328,6 +349,16 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const int nch = w > 0 ? (w + chunk_rows - 1) / chunk_rows : 1;
                 const int qs = qseq % C::kNQ;
                 const int qph = (qseq / C::kNQ) & 1;
+                if (lane == 0) {  // Alg.1 l.5: Q_i of the item (the slot's previous item has left MMA1)
+                    mbar_wait_lazy(bar(B::qempty(qs)), qph ^ 1);
+                    mbar_arrive_expect_tx(bar(B::qfull(qs)), C::kQBytes);
+#pragma unroll
+                    for (int g = 0; g < HG; ++g)
+#pragma unroll
+                        for (int pp = 0; pp < C::P; ++pp)
+                            tma_load_2d(sb + C::oQ + qs * C::kQBytes + g * 16 * C::kRowPitch + pp * 2048, &tmQ,
+                                        bar(B::qfull(qs)), (h + g) * D + (128 / EB) * pp, 16 * k);
+                }
                 for (int j = 0; j < nch; ++j) {
                     const int rows = w > 0 ? min(chunk_rows, w - chunk_rows * j) : 0;
                     const int s = seq % C::kNS;
@@ -340,7 +371,6 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         sl.rows = rows;
                         sl.qslot = qs;
                         sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2) | (sp << 8);
-                        sl.ralloc = rows > 0 ? (HG == 1 ? ((rows + C::kRowAlign - 1) & ~(C::kRowAlign - 1)) : C::kMaxRows) : 0;
                         const uint32_t fb = bar(B::idxfull(s));
                         if (rows > 0) {
                             const uint32_t r8 = (uint32_t)((rows + 7) & ~7);
@@ -370,82 +400,6 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             prof_flush(0);
         }
         __syncwarp();
-    } else if (warp == 0) {
-        // ===== producer: Q tiles and K/V gathers into the ring ====================================
-        int2* regk = reinterpret_cast<int2*>(smem + C::oReg);
-        int2* regv = regk + C::kNS;
-        int32_t seq = 0, tailk = 0, tailv = 0;
-        uint32_t headk = 0, headv = 0;
-        for (;;) {
-            const int s = seq % C::kNS;
-            mbar_wait_lazy(bar(B::idxfull(s)), (seq / C::kNS) & 1);
-            lap(0);
-            if (lane == 0) stamp(seq, 8);
-            Slot& sl = slots[s];
-            const int rows = sl.rows;
-            if (rows < 0) {
-                if (lane == 0) {
-                    mbar_arrive(bar(B::rfull(s)));
-                    prof_flush(6);
-                }
-                break;
-            }
-            const int flags = sl.flags, k = sl.rw, h = sl.head, qs = sl.qslot;
-            if (flags & 1) {  // Alg.1 l.5: Q_i for the item's first chunk
-                mbar_wait_lazy(bar(B::qempty(qs)), ((flags >> 2) & 1) ^ 1);
-                lap(1);
-                if (lane == 0) {
-                    mbar_arrive_expect_tx(bar(B::qfull(qs)), C::kQBytes);
-#pragma unroll
-                    for (int g = 0; g < HG; ++g)
-#pragma unroll
-                        for (int pp = 0; pp < C::P; ++pp)
-                            tma_load_2d(sb + C::oQ + qs * C::kQBytes + g * 16 * C::kRowPitch + pp * 2048, &tmQ,
-                                        bar(B::qfull(qs)), (h + g) * D + (128 / EB) * pp, 16 * k);
-                }
-            }
-            const uint32_t tile = (uint32_t)(sl.ralloc / 8) * C::kGroupBytes;
-            // the index warp reused this slot, so chunk seq - kNS (and all before it) retired
-            if (tailk < seq - (C::kNS - 1)) tailk = seq - (C::kNS - 1);
-            if (tailv < seq - (C::kNS - 1)) tailv = seq - (C::kNS - 1);
-            // FIFO byte rings: chunks [tail, seq) occupy the cyclic span [start(tail), head); a tile
-            // goes at head, or at 0 if it does not fit before the end; retire the oldest until free.
-            auto alloc = [&](uint32_t& head, int32_t& tail, const int2* reg, uint32_t cap, int bar_base) -> uint32_t {
-                if (tile == 0) return head;  // zero-byte chunks (empty row windows) sit at head
-                for (;;) {
-                    const bool wrap = head + tile > cap;
-                    const uint32_t off = wrap ? 0u : head;
-                    bool ok = true;
-                    if (tail != seq) {
-                        const uint32_t ts = (uint32_t)reg[tail % C::kNS].x;
-                        ok = ts < head ? (!wrap || off + tile <= ts) : (!wrap && off + tile <= ts);
-                        if (ts == head) ok = false;  // full
-                    }
-                    if (ok) {
-                        head = off + tile;
-                        return off;
-                    }
-                    mbar_wait_lazy(bar(bar_base + tail % C::kNS), (tail / C::kNS) & 1);
-                    ++tail;
-                }
-            };
-            const uint32_t offk = alloc(headk, tailk, regk, (uint32_t)C::kRingK, B::kempty(0));
-            if (lane == 0) stamp(seq, 12);
-            const uint32_t offv = alloc(headv, tailv, regv, (uint32_t)C::kRingV, B::empty(0));
-            lap(2);
-            __syncwarp();
-            if (lane == 0) {
-                regk[s] = make_int2((int)offk, (int)(offk + tile));
-                regv[s] = make_int2((int)offv, (int)(offv + tile));
-                sl.ring_off = (int)offk;
-                sl.pad = (int)offv;
-            }
-            __syncwarp();
-            lap(3);
-            if (lane == 0) { stamp(seq, 9); mbar_arrive(bar(B::rfull(s))); }  // ring space assigned: loaders may gather
-            ++seq;
-        }
-        __syncwarp();
     } else if (warp >= C::kLoader0 && warp < C::kLoader0 + C::kLoaderWarps) {
         // ===== loader warps: gather the K and V rows of each chunk (Alg.1 l.8) ===================
         // Lane l of a warp copies 16-byte piece (l % pieces) of one gathered row straight into the
@@ -460,7 +414,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         int32_t seq = 0;
         for (;;) {
             const int s = seq % C::kNS;
-            mbar_wait_lazy(bar(B::rfull(s)), (seq / C::kNS) & 1);
+            mbar_wait(bar(B::idxfull(s)), (seq / C::kNS) & 1);  // the chunk's ids have landed
             if (lw == 0 && lane == 0) stamp(seq, 10);
             const Slot& sl = slots[s];
             const int rows = sl.rows;
@@ -471,26 +425,37 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 break;
             }
             const int h = sl.head;
-            const uint32_t kt = sb + C::oRing + sl.ring_off + pnl * 1024;
-            const uint32_t vt = sb + C::oRingV + sl.pad + pnl * 1024;
+            const int tk = seq % C::kNK, tv = seq % C::kNV;
+            const uint32_t kt = sb + C::oK + tk * C::kMaxRowsBytes + pnl * 1024;
+            const uint32_t vt = sb + C::oV + tv * C::kMaxRowsBytes + pnl * 1024;
             const uint8_t* kbase = Kg + (int64_t)h * C::RB + piece * 16;
             const uint8_t* vbase = Vg + (int64_t)h * C::RB + piece * 16;
             // HG = 1: tile row r = compacted column r.  HG = 4: tile row 32g + r = column r of head h + g.
             const int ops = (expt & 8) ? 0 : (HG == 1 ? (rows + kRowsPerOp - 1) / kRowsPerOp : C::kMaxRows / kRowsPerOp);
-#pragma unroll 2
-            for (int t = lw; t < ops; t += C::kLoaderWarps) {
+            mbar_wait(bar(B::ktfree(tk)), ((seq / C::kNK) & 1) ^ 1);
+            mbar_wait(bar(B::vtfree(tv)), ((seq / C::kNV) & 1) ^ 1);
+            // all of this lane's row ids first (independent shared loads), then the copies
+            constexpr int kIters = (C::kMaxRows / kRowsPerOp + C::kLoaderWarps - 1) / C::kLoaderWarps;
+            int64_t src[kIters];
+            uint32_t dst[kIters];
+            bool ok[kIters];
+#pragma unroll
+            for (int i = 0; i < kIters; ++i) {
+                const int t = lw + i * C::kLoaderWarps;
                 const int tr = t * kRowsPerOp + rsub;  // tile row
                 const int r = HG == 1 ? tr : (tr & 31);
-                if (r < rows) {
-                    const int64_t j = sl.cols[r];
-                    const int64_t src = j * ldb + (HG == 1 ? 0 : (int64_t)(tr >> 5) * C::RB);
-                    const uint32_t o = (uint32_t)(tr >> 3) * C::kGroupBytes + (uint32_t)(tr & 7) * 128 +
-                                       (uint32_t)((cc ^ (tr & 7)) << 4);
-                    cp_async_16(kt + o, kbase + src);
-                    cp_async_16(vt + o, vbase + src);
-                }
+                ok[i] = t < ops && r < rows;
+                const int64_t j = ok[i] ? sl.cols[r] : 0;
+                src[i] = j * ldb + (HG == 1 ? 0 : (int64_t)(tr >> 5) * C::RB);
+                dst[i] = (uint32_t)(tr >> 3) * C::kGroupBytes + (uint32_t)(tr & 7) * 128 + (uint32_t)((cc ^ (tr & 7)) << 4);
             }
+#pragma unroll
+            for (int i = 0; i < kIters; ++i)
+                if (ok[i]) cp_async_16(kt + dst[i], kbase + src[i]);
             cp_async_mbar_arrive(kfb);
+#pragma unroll
+            for (int i = 0; i < kIters; ++i)
+                if (ok[i]) cp_async_16(vt + dst[i], vbase + src[i]);
             cp_async_mbar_arrive(vfb);
             if (lw == 0 && lane == 0) stamp(seq, 1);
             ++seq;
@@ -512,12 +477,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 mbar_wait(bar(B::kfull(s)), (n1 / C::kNS) & 1);  // K_c landed
                 if (lane == 0) stamp(n1, 11);
                 const Slot& sl = slots[s];
-                const int rows = sl.rows, flags = sl.flags, qslot = sl.qslot, roff = sl.ring_off;
+                const int rows = sl.rows, flags = sl.flags, qslot = sl.qslot;
                 if (rows < 0) break;
                 mbar_wait(bar(B::sfree(b)), ((n1 / C::kSB) & 1) ^ 1);  // owner read chunk n1 - kSB
                 if (flags & 1) mbar_wait(bar(B::qfull(qslot)), (flags >> 2) & 1);
                 tc_fence_after();
-                const uint64_t a0 = dK + ((sb + C::oRing + roff) >> 4);
+                const uint64_t a0 = dK + ((sb + C::oK + (n1 % C::kNK) * C::kMaxRowsBytes) >> 4);
                 const uint64_t b0 = dQ + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
                 if (rows > 0 && !(expt & 4)) {
                     // HG > 1: one M = 128 MMA group per head g against its own Q tile into its own
@@ -533,7 +498,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                         }
                 }
                 mma_commit_warp(bar(B::sfull(b)));
-                mma_commit_warp(bar(B::kempty(s)));
+                mma_commit_warp(bar(B::ktfree(n1 % C::kNK)));
                 if (flags & 2) mma_commit_warp(bar(B::qempty(qslot)));
                 if (lane == 0) stamp(n1, 2);
             }
@@ -542,6 +507,10 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             // 16-bit P, K-major [16 x 128 bytes] with the 128-byte swizzle for fp8 P (8-bit
             // MN-major B would need 16-byte rows)
             constexpr uint32_t idesc2 = idesc_f16(fmt, 1, EB == 2 ? 1 : 0, D, 16);
+            // l_c = ones[64 x C] . P^T: every row of the M = 64 result is the row sum of P (each TMEM
+            // lane quadrant holds a copy); the ones operand is one atom read again for every K group
+            constexpr uint32_t idescL = idesc_f16(fmt, 1, 1, 64, 16);
+            const uint64_t dOnes = smem_desc_sw128(sb + C::oOnes, 1024, 0);
             const uint64_t dV = smem_desc_sw128(0, 1024, C::kGroupBytes);
             const uint64_t dP = EB == 2 ? smem_desc_sw32(0, 4096, 256) : smem_desc_sw128(0, 16, 1024);
             for (int32_t n2 = 0;; ++n2) {
@@ -555,23 +524,28 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 if (lane == 0) stamp(n2, 14);
                 tc_fence_after();
                 if (rows > 0 && !(expt & 2)) {
-                    const uint64_t a0 = dV + ((sb + C::oRingV + slots[s].pad) >> 4);
+                    const uint64_t a0 = dV + ((sb + C::oV + (n2 % C::kNV) * C::kMaxRowsBytes) >> 4);
                     const uint64_t b0 = dP + ((sb + C::oP + b * C::kPBytes) >> 4);
                     const int nsteps = (rows + C::kRowAlign - 1) / C::kRowAlign;
                     if (EB == 1) {
                         for (int st = 0; st < nsteps; ++st)  // 32 chunk rows = 4 row groups, 32 bytes of a P row
-                            mma_f8_ss_warp(tmem + 16 * C::kSB + b * 16, a0 + ((st * 4 * C::kGroupBytes) >> 4),
+                            mma_f8_ss_warp(tmem + C::kTmemO + b * 16, a0 + ((st * 4 * C::kGroupBytes) >> 4),
                                            b0 + ((st * 32) >> 4), idesc2, st > 0 ? 1u : 0u);
                     } else {
 #pragma unroll
                         for (int g = 0; g < HG; ++g)  // head g: tile rows / P^T columns 32g .. (HG > 1)
                             for (int st = 0; st < nsteps; ++st)
-                                mma_f16_ss_warp(tmem + 16 * C::kSB * HG + (b * HG + g) * 16,
+                                mma_f16_ss_warp(tmem + C::kTmemO + (b * HG + g) * 16,
                                                 a0 + ((g * 4 * C::kGroupBytes + st * 2 * C::kGroupBytes) >> 4),
                                                 b0 + ((g * 1024 + st * 512) >> 4), idesc2, st > 0 ? 1u : 0u);
+                        if constexpr (C::kLsumMMA)
+                            for (int st = 0; st < nsteps; ++st)
+                                mma_f16_ss_warp(tmem + C::kTmemL + b * 16, dOnes, b0 + ((st * 512) >> 4), idescL,
+                                                st > 0 ? 1u : 0u);
                     }
                 }
                 mma_commit_warp(bar(B::ofull(b)));
+                mma_commit_warp(bar(B::vtfree(n2 % C::kNV)));
                 mma_commit_warp(bar(B::empty(s)));
                 if (lane == 0) stamp(n2, 5);
                 __syncwarp();
@@ -628,24 +602,44 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                 for (int i = 0; i < 16; ++i) x[i] = ((mask >> i) & 1u) ? x[i] * scale_log2 : -INFINITY;  // Alg.1 l.14
             }
-            // chunk row max (Alg.1 l.16): warp butterfly (+ a 4-warp combine when the chunk's
-            // columns span the four warps, HG = 1)
-            const float rm = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
+            // chunk row max (Alg.1 l.16)
             float cm[16];
-            if (HG == 1) {
-                if (!(lane & 1)) red[(b * 4 + q) * 16 + ((lane >> 1) & 15)] = rm;
+            float mrow = kMFloor;  // HG = 1, lanes 0..15: the chunk max of row `lane` (reading c5 floor)
+            if constexpr (HG == 1 && F3S_MAX_REDUX) {
+                // the warp's 32 columns: one redux.sync.max per row (uniform datapath), then the
+                // 4-warp combine through shared memory; lane i < 16 finishes row i and broadcasts
+                float mine = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float wm = (expt & 32) ? 0.f : redux_max_f32(x[i]);
+                    mine = (lane & 15) == i ? wm : mine;
+                }
+                if (lane < 16) red[(b * 16 + lane) * 4 + q] = mine;
                 if (p == 0) lap(2);
                 named_bar_sync(1 + wg, 128);
-                const float4* r4 = reinterpret_cast<const float4*>(red + b * 64);
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    const float4 w0 = r4[g], w1 = r4[4 + g], w2 = r4[8 + g], w3 = r4[12 + g];
-                    cm[4 * g] = fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x));
-                    cm[4 * g + 1] = fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y));
-                    cm[4 * g + 2] = fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z));
-                    cm[4 * g + 3] = fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w));
+                if (lane < 16) {
+                    const float4 r = reinterpret_cast<const float4*>(red)[b * 16 + lane];
+                    mrow = fmaxf(fmaxf(fmaxf(r.x, r.y), fmaxf(r.z, r.w)), kMFloor);
                 }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) cm[i] = __shfl_sync(0xffffffffu, mrow, i);
+            } else if constexpr (HG == 1) {
+                // warp butterfly (lane 2i ends with row i's max over the warp), 4-warp combine
+                const float rm = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
+                if (!(lane & 1)) red[(((lane >> 1) & 15) + b * 16) * 4 + q] = rm;
+                if (p == 0) lap(2);
+                named_bar_sync(1 + wg, 128);
+                const float4* r4 = reinterpret_cast<const float4*>(red) + b * 16;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float4 r = r4[i];
+                    cm[i] = fmaxf(fmaxf(fmaxf(r.x, r.y), fmaxf(r.z, r.w)), kMFloor);
+                }
+                if (lane < 16) mrow = cm[0];
+#pragma unroll
+                for (int i = 1; i < 16; ++i) mrow = lane == i ? cm[i] : mrow;
             } else {  // the warp holds all columns of its head: lane 2i has row i's max
+                const float rm = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
 #pragma unroll
                 for (int i = 0; i < 16; ++i) cm[i] = __shfl_sync(0xffffffffu, rm, 2 * i);
             }
@@ -664,7 +658,16 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 cm[i] = fmaxf(kMFloor, cm[i]);                    // m_c (reading c5)
                 pv[i] = (expt & 1) ? x[i] : pexp(x[i] - cm[i]);   // E = e^{S - m_c} (l.17); 0 where masked
             }
-            const float rl = rowreduce16(pv, lane, OpAdd());      // this warp's part of rowsum(E) (l.18)
+            // this warp's part of the row sums (l.18) of the P that MMA2 multiplies: the rounded
+            // 16-bit P (reading c7), or fp8's unrounded E (reading c24); one-head 16-bit chunks get
+            // l_c from the tensor core instead (kLsumMMA)
+            float rl = 0.f;
+            if constexpr (!C::kLsumMMA) {
+                float pr[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pr[i] = EB == 1 ? pv[i] : round_to<T>(pv[i]);
+                rl = rowreduce16(pr, lane, OpAdd());
+            }
             if (p == 0) lap(6);
             // P_b / corr_b are free once the correction group consumed chunk seq - kSB
             mbar_wait(bar(B::pempty(b)), bph ^ 1);
@@ -690,11 +693,14 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 prow[sw] = lo;
                 prow[sw ^ 1] = hi;
             }
-            if (!(lane & 1)) corr[b].lpart[q][(lane >> 1) & 15] = rl;
+            if (!C::kLsumMMA && !(lane & 1)) corr[b].lpart[q][(lane >> 1) & 15] = rl;
+            if (HG == 1 && q == 0 && lane < 16) corr[b].m[lane] = mrow;
             if (p == 0) {
-                float4* m4 = reinterpret_cast<float4*>(corr[b].m);
+                if (HG > 1) {
+                    float4* m4 = reinterpret_cast<float4*>(corr[b].m);
 #pragma unroll
-                for (int g = 0; g < 4; ++g) m4[g] = make_float4(cm[4 * g], cm[4 * g + 1], cm[4 * g + 2], cm[4 * g + 3]);
+                    for (int g = 0; g < 4; ++g) m4[g] = make_float4(cm[4 * g], cm[4 * g + 1], cm[4 * g + 2], cm[4 * g + 3]);
+                }
                 reinterpret_cast<int4*>(&corr[b].rows)[0] = make_int4(rows, flags, rw, hd);
                 if (kDiag) {
                     corr[b].t_s = t_s;
@@ -759,7 +765,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll 1
                 for (int g = 0; g < HG; ++g) {
                     float ov[16];
-                    tmem_ld_32x32b_x16(tmem + tl + 16 * C::kSB * HG + (b * HG + g) * 16, ov);
+                    tmem_ld_32x32b_x16(tmem + tl + C::kTmemO + (b * HG + g) * 16, ov);
                     const float4* l4 = reinterpret_cast<const float4*>(corr[b].lpart[g]);  // head g's row sums
                     if (has) {
 #pragma unroll
@@ -788,7 +794,22 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             // merge factors of row ri: O = fa * O + fb * O_c
             const float mc = corr[b].m[ri];
-            const float lc = (corr[b].lpart[0][ri] + corr[b].lpart[1][ri]) + (corr[b].lpart[2][ri] + corr[b].lpart[3][ri]);
+            float lc;
+            if constexpr (C::kLsumMMA) {
+                // l_c from the ones MMA: lanes 0..15 of the warp's quadrant hold l_c[0..15] in the
+                // buffer's 16 columns; lane ri takes column ri (lanes 16..31 copy lanes 0..15)
+                lc = 0.f;
+                if (rows > 0) {
+                    float lv[16];
+                    tmem_ld_32x32b_x16(tmem + tl + C::kTmemL + b * 16, lv);
+                    lc = lv[0];
+#pragma unroll
+                    for (int i = 1; i < 16; ++i) lc = ri == i ? lv[i] : lc;
+                    lc = __shfl_sync(0xffffffffu, lc, ri);
+                }
+            } else {
+                lc = (corr[b].lpart[0][ri] + corr[b].lpart[1][ri]) + (corr[b].lpart[2][ri] + corr[b].lpart[3][ri]);
+            }
             float fa, fb;
             if (flags & 1) {  // the item's first chunk: (m, l) = (m_c, l_c)
                 m_run = mc;
@@ -810,7 +831,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             if (rows > 0) {
                 float ov[16];
-                tmem_ld_32x32b_x16(tmem + tl + 16 * C::kSB + b * 16, ov);
+                tmem_ld_32x32b_x16(tmem + tl + C::kTmemO + b * 16, ov);
 #pragma unroll
                 for (int i = 0; i < 16; ++i)
                     oacc[i] = fmaf(oacc[i], __shfl_sync(0xffffffffu, fa, i), ov[i] * __shfl_sync(0xffffffffu, fb, i));
