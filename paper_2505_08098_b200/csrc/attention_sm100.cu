@@ -83,7 +83,8 @@ struct Cfg {
     static constexpr int kNQ = HG == 4 ? 6 : EB == 1 ? 8 : F3S_NQ > 0 ? F3S_NQ : 4;
     static constexpr int kQBytes = 16 * kRowPitch * HG;  // HG head tiles of 16 x D
     static constexpr int kPBytes = 16 * kMaxRows * EB;
-    static constexpr int kNO = HG == 4 ? 1 : 2;      // O staging tiles (16 x HG*D fp32) for the TMA store
+    // O staging tiles (16 x HG*D fp32) for the TMA store (head groups: one per correction group)
+    static constexpr int kNO = 2;
     static constexpr int kOBytes = 16 * D * 4 * HG;
     // Row sums l_c of the chunk's P (Alg.1 l.17) from the tensor core: MMA2 also multiplies a tile of
     // ones by P^T, so l_c sums exactly the rounded P that multiplies V (16-bit inputs, one head per
@@ -136,7 +137,10 @@ struct Cfg {
     static constexpr int kLoaderWarps = F3S_NLOAD;
     static constexpr int kMma2Warp = 2;
     static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps, kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
-    static constexpr int kThreads = 32 * (kCorr0 + 4);
+    // correction warpgroups: head-group items are single chunks with no running state, so two
+    // groups take alternate chunks; one-head items merge chunks in order in one group
+    static constexpr int kCorrWGs = HG == 4 ? 2 : 1;
+    static constexpr int kThreads = 32 * (kCorr0 + 4 * kCorrWGs);
     static constexpr int kBatch = 8;                 // items fetched per queue round trip
     static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 };
@@ -235,7 +239,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             int32_t* __restrict__ counter, int32_t n_items, int32_t H, int64_t ldkv,
             const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float scale_log2,
             uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt_arg,
-            float* __restrict__ scratch, float2* __restrict__ ml_out, int32_t n_rows) {
+            float* __restrict__ scratch, float2* __restrict__ ml_out, int32_t n_rows, float* __restrict__ Og) {
     constexpr int EB = (int)sizeof(T);
     using C = Cfg<D, HG, EB>;
     using B = Bars<D, HG, EB>;
@@ -575,8 +579,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (p == 0) lap(0);
             const Slot& sl = slots[s];
             const int rows = sl.rows;
-            if (rows < 0) {  // the warpgroup that meets the first stop marker forwards it
-                if (rows == -1) {
+            if (rows < 0) {  // forward the stop to the correction group(s) that walk this chunk's parity
+                if (rows == -1 || (C::kCorrWGs == 2 && rows == -2)) {
                     mbar_wait(bar(B::pempty(b)), bph ^ 1);
                     if (p == 0) corr[b].rows = -1;
                     mbar_arrive(bar(B::pfull(b)));
@@ -724,12 +728,14 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         const int q = warp & 3;
         const uint32_t tl = (uint32_t)(32 * q) << 16;
         const int ri = lane & 15;        // the row whose statistics this lane keeps (lanes 16..31 mirror)
+        (void)Og;
         float oacc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) oacc[i] = 0.f;
         float m_run = kMFloor, l_run = 0.f;
         int32_t item = 0;
-        for (int32_t seq = 0;; ++seq) {
+        const int cw = (warp - C::kCorr0) >> 2;  // correction group (head groups: alternate chunks)
+        for (int32_t seq = cw;; seq += C::kCorrWGs) {
             const int b = seq % C::kSB;
             const uint32_t bph = (seq / C::kSB) & 1;
             mbar_wait(bar(B::pfull(b)), bph);
@@ -756,10 +762,11 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if constexpr (HG > 1) {
                 // head groups: one chunk per item (every window <= 32 columns), so O_g = O^T_g / l_g
                 // for each head g of the group (warp g's row sums are head g's), staged as one
-                // [16 x HG*D] tile and stored by one TMA
-                float* ost = reinterpret_cast<float*>(smem + C::oOst);
-                if (lead) bulk_wait_group_read<0>();  // the previous item's store has read the tile
-                named_bar_sync(1 + C::kSoftmaxWGs, 128);
+                // [16 x HG*D] tile per correction group and stored by one TMA
+                float* ost = reinterpret_cast<float*>(smem + C::oOst + cw * C::kOBytes);
+                const bool wlead = lane == 0 && q == 0;
+                if (wlead) bulk_wait_group_read<0>();  // this group's previous store has read the tile
+                named_bar_sync(1 + C::kSoftmaxWGs + cw, 128);
                 const bool has = lane < 16;           // O^T lane -> feature 16q + lane (M = 64 layout)
                 const int f = 16 * q + lane;
 #pragma unroll 1
@@ -783,9 +790,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 tc_fence_before();
                 mbar_arrive(bar(B::pempty(b)));
                 fence_proxy_async_smem();
-                named_bar_sync(1 + C::kSoftmaxWGs, 128);
-                if (lead) {
-                    if (!(expt & 64)) tma_store_2d(&tmO, sb + C::oOst, hd * D, 16 * rw);
+                named_bar_sync(1 + C::kSoftmaxWGs + cw, 128);
+                if (wlead) {
+                    if (!(expt & 64)) tma_store_2d(&tmO, smem_u32(ost), hd * D, 16 * rw);
                     bulk_commit_group();
                     stamp(seq, 7);
                 }
@@ -892,7 +899,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 ++item;
             }
         }
-        if (threadIdx.x == 32 * C::kCorr0) bulk_wait_group<0>();
+        if (lane == 0 && (HG > 1 ? q == 0 : threadIdx.x == 32 * C::kCorr0)) bulk_wait_group<0>();
     }
     tc_fence_before();
     __syncthreads();
@@ -1113,7 +1120,7 @@ f3s_status launch(const AttnArgs& a) {
             (a.kv_ld > 0 ? a.kv_ld : (int64_t)a.heads * D) * (int64_t)sizeof(T),
             static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.scale * 1.4426950408889634f, a.trace,
             a.trace_chunks, a.expt, split ? reinterpret_cast<float*>(scratch + 256) : nullptr,
-            reinterpret_cast<float2*>(a.ml_out), p.n_rows);
+            reinterpret_cast<float2*>(a.ml_out), p.n_rows, a.O);
         count_launch();
         err = cudaGetLastError();
     }
