@@ -46,6 +46,7 @@ def _load():
         lib.f3si_dcsbm.argtypes = [i32, i64, i32, ctypes.c_double, ctypes.c_double, ctypes.c_double, u64,
                                    pp, pp, ctypes.POINTER(i64)]
         lib.f3si_dcsbm_w.argtypes = [i32, i64, i32, vp, vp, u64, pp, pp, ctypes.POINTER(i64)]
+        lib.f3si_windows.argtypes = [i32, vp, vp, i32, ctypes.c_double, ctypes.c_double, u64, pp, pp, ctypes.POINTER(i64)]
         lib.f3si_molecules.argtypes = [i32, i32, i32, i32, u64, pp, pp, ctypes.POINTER(i64),
                                        ctypes.POINTER(i32), pp]
         lib.f3si_random_csr.argtypes = [i32, i32, i32, i32, i32, i32, u64, pp, pp, ctypes.POINTER(i64)]
@@ -115,6 +116,23 @@ def dcsbm_w(n: int, n_pairs: int, *, comm_size: int, mu, weights: np.ndarray, se
                           ctypes.byref(nnz))
     if rc:
         raise RuntimeError(f"f3si_dcsbm_w failed ({rc})")
+    return _csr_from(rp, ci, nnz, n, n)
+
+
+def windows(n: int, tcb: np.ndarray, ratio: np.ndarray, *, comm_size: int, mu: float, gamma: float,
+            seed: int) -> CSR:
+    """A built row window by row window with given TCB counts (8 * tcb distinct columns per window)
+    and mean nnz/TCB ratios (inputs.c: f3si_windows)."""
+    lib = _load()
+    R = (n + 15) // 16
+    t = np.ascontiguousarray(tcb, dtype=np.int32)
+    r = np.ascontiguousarray(ratio, dtype=np.float64)
+    assert t.shape == (R,) and r.shape == (R,)
+    rp, ci, nnz = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+    rc = lib.f3si_windows(n, t.ctypes.data, r.ctypes.data, comm_size, mu, gamma, seed, ctypes.byref(rp),
+                          ctypes.byref(ci), ctypes.byref(nnz))
+    if rc:
+        raise RuntimeError(f"f3si_windows failed ({rc})")
     return _csr_from(rp, ci, nnz, n, n)
 
 

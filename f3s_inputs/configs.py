@@ -12,7 +12,7 @@ from typing import Callable
 
 import numpy as np
 
-from . import CSR, chung_lu, dcsbm, dcsbm_w, molecules, values
+from . import CSR, chung_lu, dcsbm, molecules, values, windows
 
 # Tab.tcb_deciles, Reddit: min / decile boundaries / max of TCBs (16x8) per row window
 REDDIT_DECILES = (4, 46, 88, 135, 190, 265, 367, 503, 718, 1113.5, 9857)
@@ -29,13 +29,18 @@ def _uniform(count: int, seed: int) -> np.ndarray:
     return (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
 
 
-def reddit_weights(n: int, *, seed: int, jitter: float, tail_alpha: float) -> np.ndarray:
-    """Node weights whose 16-row windows follow the paper's TCB/RW deciles.
+def reddit_windows(n: int, seed: int, tail_alpha: float = 2.1, comm_size: int = 4500, mu: float = 0.8,
+                   gamma: float = 2.1, ratio_sd: float = 15.7) -> CSR:
+    """Reddit-shaped A built row window by row window (f3s_inputs.windows) from the paper's own
+    statistics: TCB/RW deciles of Tab.tcb_deciles and nnz/TCB mean 16.5, CV 0.95
+    (Tab.datasets, P:545).
 
-    Each window k gets a target t_k = Q(u_k) with u_k = (rank_k + 0.5) / R, ranks a seeded
-    permutation (so every decile holds exactly R/10 windows); Q is log-linear between the
-    decile boundaries and a Pareto(tail_alpha) truncated at the table's maximum in the last
-    decile.  A row's weight is t_k * exp(jitter * z), z ~ N(0, 1) from a seeded stream."""
+    Window k gets t_k = Q(u_k), u_k = (rank_k + 0.5) / R with ranks a seeded permutation (every
+    decile holds R/10 windows); Q is log-linear between the decile boundaries and, in the last
+    decile, a Pareto(tail_alpha) truncated at the table's maximum (tail_alpha = 2.1 gives the
+    table's mean 477).  Its nnz/TCB target is 8 + X, X lognormal with mean 8.5 and standard
+    deviation 15.7 (so 8 + X has the table's mean 16.5 and CV 0.95; 8 is the floor, one row per
+    column), clipped to 128 (all 16 rows)."""
     R = (n + 15) // 16
     rank = np.argsort(_uniform(R, seed ^ 0x77), kind="stable").argsort(kind="stable")
     u = (rank + 0.5) / R
@@ -47,9 +52,13 @@ def reddit_weights(n: int, *, seed: int, jitter: float, tail_alpha: float) -> np
     tail = i == 9
     c = 1.0 - (lo / hi) ** tail_alpha
     t[tail] = lo * (1.0 - f[tail] * c) ** (-1.0 / tail_alpha)
-    u1, u2 = _uniform(n, seed ^ 0x99), _uniform(n, seed ^ 0xAA)
+    tcb = np.rint(t).astype(np.int32)
+    mx, sx = 8.5, ratio_sd
+    sig2 = np.log1p((sx / mx) ** 2)
+    u1, u2 = _uniform(R, seed ^ 0x99), _uniform(R, seed ^ 0xAA)
     z = np.sqrt(-2.0 * np.log1p(-u1)) * np.cos(2.0 * np.pi * u2)  # Box-Muller
-    return t[np.arange(n) // 16] * np.exp(jitter * z)
+    ratio = np.minimum(8.0 + np.exp(np.log(mx) - sig2 / 2 + np.sqrt(sig2) * z), 128.0)
+    return windows(n, tcb, ratio, comm_size=comm_size, mu=mu, gamma=gamma, seed=seed)
 
 
 @dataclass

@@ -341,17 +341,17 @@ int f3si_dcsbm(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, double 
 
 /*
  * Same block model with caller-given node weights w[n] (expected-degree shape; only ratios
- * matter).  The Reddit-shaped workload passes weights that are constant-ish within each
+ * matter) and a local fraction per first endpoint (mu_node[n]).  The Reddit-shaped workload passes weights that are constant-ish within each
  * 16-row window and drawn per window from the paper's TCB/RW decile table,
  * which is what gives the row windows their long-tailed widths.
  */
-int f3si_dcsbm_w(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, const double* w, uint64_t seed,
-                 int32_t** row_ptr, int32_t** col_idx, int64_t* nnz) {
-    if (n <= 1 || comm_size < 2 || n_pairs < 0 || !w) return 1;
+int f3si_dcsbm_w(int32_t n, int64_t n_pairs, int32_t comm_size, const double* mu_node, const double* w,
+                 uint64_t seed, int32_t** row_ptr, int32_t** col_idx, int64_t* nnz) {
+    if (n <= 1 || comm_size < 2 || n_pairs < 0 || !w || !mu_node) return 1;
     double* wn = (double*)malloc((size_t)n * sizeof(double));
     if (!wn) return 2;
     memcpy(wn, w, (size_t)n * sizeof(double));
-    return dcsbm_core(n, n_pairs, comm_size, mu, NULL, wn, seed, row_ptr, col_idx, nnz);
+    return dcsbm_core(n, n_pairs, comm_size, 0.0, mu_node, wn, seed, row_ptr, col_idx, nnz);
 }
 
 /* takes ownership of wn; mu_node (optional) gives each first endpoint its own local fraction */
@@ -407,6 +407,121 @@ static int dcsbm_core(int32_t n, int64_t n_pairs, int32_t comm_size, double mu, 
     o = unique_sorted(out, o);
     int rc = keys_to_csr(out, o, n, row_ptr, col_idx);
     free(out);
+    *nnz = o;
+    return rc ? 2 : 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Row-window construction (Reddit-shaped: long-tailed window widths)         */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * Builds A window by window so that the 16x8 plan statistics of Tab.datasets / Tab.tcb_deciles
+ * hold by construction.  Window k (rows 16k .. 16k+15) gets exactly
+ * U_k = min(8 * tcb[k], n) distinct columns: each draw is, with probability mu, a node of the
+ * window's own community (contiguous IDs, comm_size nodes, uniform) and otherwise a node drawn
+ * by a global power-law popularity (exponent gamma, hubs at seeded random IDs); every column is
+ * then hit by m distinct rows of the window, m = 1 + Poisson(ratio[k] / 8 - 1) clipped to the
+ * window's rows, so that nnz_k / tcb_k has mean ratio[k].  Not symmetric (the statistics are
+ * those of the row windows).  Rows sorted, no duplicates.  Windows are independent: the
+ * result does not depend on the thread count.
+ */
+static inline uint64_t hash_probe(uint64_t x) { return mix64(x ^ 0x6A09E667F3BCC909ULL); }
+
+int f3si_windows(int32_t n, const int32_t* tcb, const double* ratio, int32_t comm_size, double mu, double gamma,
+                 uint64_t seed, int32_t** row_ptr, int32_t** col_idx, int64_t* nnz) {
+    if (n < 1 || comm_size < 1 || !tcb || !ratio || !row_ptr || !col_idx || !nnz) return 1;
+    const int32_t R = (n + 15) / 16;
+    double* w = (double*)malloc((size_t)n * sizeof(double));
+    if (!w) return 2;
+    double a = 1.0 / (gamma - 1.0);
+    for (int32_t i = 0; i < n; ++i) w[i] = pow((double)i + 10.0, -a);
+    int32_t* q = make_perm(n, seed ^ 0x1D1DULL);
+    double* wn = (double*)malloc((size_t)n * sizeof(double));
+    for (int32_t i = 0; i < n; ++i) wn[q[i]] = w[i];
+    free(q);
+    free(w);
+    alias_t glob;
+    if (alias_build(&glob, wn, n, 0)) return 2;
+    free(wn);
+    /* per-window entry counts are random: each window fills its own buffer */
+    uint64_t** bufs = (uint64_t**)calloc((size_t)R, sizeof(uint64_t*));
+    int64_t* cnt = (int64_t*)calloc((size_t)R, sizeof(int64_t));
+    int fail = 0;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int32_t k = 0; k < R; ++k) {
+        const int32_t r0 = 16 * k, nr = (r0 + 16 <= n) ? 16 : n - r0;
+        int64_t U = (int64_t)8 * tcb[k];
+        if (U > n) U = n;
+        if (U < 0) U = 0;
+        int64_t tsize = 64;
+        while (tsize < 2 * U) tsize <<= 1;
+        int32_t* table = (int32_t*)malloc((size_t)tsize * sizeof(int32_t));
+        int32_t* chosen = (int32_t*)malloc((size_t)(U > 0 ? U : 1) * sizeof(int32_t));
+        uint64_t* out = (uint64_t*)malloc((size_t)(U * nr > 0 ? U * nr : 1) * sizeof(uint64_t));
+        if (!table || !chosen || !out) { fail = 1; free(table); free(chosen); free(out); continue; }
+        for (int64_t t = 0; t < tsize; ++t) table[t] = -1;
+        const int32_t c0 = (r0 / comm_size) * comm_size;
+        const int32_t cs = (c0 + comm_size <= n) ? comm_size : n - c0;
+        uint64_t ctr = 0, wseed = mix64(seed + (uint64_t)k * GOLDEN);
+        int64_t got = 0, local_got = 0, tries = 0;
+        while (got < U && tries < 64 * U + 4096) {
+            ++tries;
+            const uint64_t z1 = rng_at(wseed, ctr++), z2 = rng_at(wseed, ctr++);
+            int32_t c;
+            /* local draws stop once the community is nearly exhausted */
+            if (u01(z1) < mu && local_got < (int64_t)cs * 7 / 8) c = c0 + (int32_t)(z2 % (uint64_t)cs);
+            else c = alias_draw(&glob, z2);
+            uint64_t hslot = hash_probe((uint64_t)c) & (uint64_t)(tsize - 1);
+            int dup = 0;
+            while (table[hslot] >= 0) {
+                if (table[hslot] == c) { dup = 1; break; }
+                hslot = (hslot + 1) & (uint64_t)(tsize - 1);
+            }
+            if (dup) continue;
+            table[hslot] = c;
+            chosen[got++] = c;
+            if (c >= c0 && c < c0 + cs) ++local_got;
+        }
+        /* rows hitting each column: m = 1 + Poisson(lambda), distinct rows (partial shuffle) */
+        const double lam = ratio[k] / 8.0 - 1.0 > 0.0 ? ratio[k] / 8.0 - 1.0 : 0.0;
+        const double el = exp(-lam);
+        int64_t o = 0;
+        for (int64_t u = 0; u < got; ++u) {
+            int32_t m = 1;
+            double prod = u01(rng_at(wseed, ctr++));
+            while (prod > el && m < nr) { ++m; prod *= u01(rng_at(wseed, ctr++)); }
+            int32_t perm[16];
+            for (int32_t i = 0; i < nr; ++i) perm[i] = i;
+            for (int32_t i = 0; i < m; ++i) {
+                int32_t j = i + (int32_t)(rng_at(wseed, ctr++) % (uint64_t)(nr - i));
+                int32_t t = perm[i]; perm[i] = perm[j]; perm[j] = t;
+                out[o++] = ((uint64_t)(r0 + perm[i]) << 32) | (uint64_t)(uint32_t)chosen[u];
+            }
+        }
+        free(table);
+        free(chosen);
+        bufs[k] = out;
+        cnt[k] = o;
+    }
+    alias_free(&glob);
+    if (fail) return 2;
+    int64_t total = 0;
+    for (int32_t k = 0; k < R; ++k) total += cnt[k];
+    uint64_t* all = (uint64_t*)malloc((size_t)(total > 0 ? total : 1) * sizeof(uint64_t));
+    if (!all) return 2;
+    int64_t o = 0;
+    for (int32_t k = 0; k < R; ++k) {
+        memcpy(all + o, bufs[k], (size_t)cnt[k] * sizeof(uint64_t));
+        o += cnt[k];
+        free(bufs[k]);
+    }
+    free(bufs);
+    free(cnt);
+    if (radix_sort_u64(all, o)) return 2;
+    o = unique_sorted(all, o);
+    int rc = keys_to_csr(all, o, n, row_ptr, col_idx);
+    free(all);
     *nnz = o;
     return rc ? 2 : 0;
 }

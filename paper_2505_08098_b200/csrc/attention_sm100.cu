@@ -132,9 +132,10 @@ struct Cfg {
     // own barriers: try_wait wakes ~60 cycles after the arrive), kLoaderWarps cp.async gather warps,
     // two softmax warpgroups, the correction warpgroup
 #ifndef F3S_NLOAD
-#define F3S_NLOAD 6
+#define F3S_NLOAD 0
 #endif
-    static constexpr int kLoaderWarps = F3S_NLOAD;
+    // gather warps: the cp.async issue rate bounds the pipeline (measured: 5-8 warps, profiles/r02_ab_*)
+    static constexpr int kLoaderWarps = F3S_NLOAD > 0 ? F3S_NLOAD : RB >= 256 ? 8 : 7;
     static constexpr int kMma2Warp = 2;
     static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps, kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
     // correction warpgroups: head-group items are single chunks with no running state, so two

@@ -1,7 +1,7 @@
 """Calibrate the Reddit-shaped generator against Tab.datasets (TCB/RW 477.2, CV 1.35;
 nnz/TCB 16.5, CV 0.95) and Tab.tcb_deciles.  Prints the plan statistics of one setting.
 
-  python tools/calib_reddit.py COMM MU JITTER ALPHA [WREF]   (mu_i = MU / (1 + w_i / WREF))
+  python tools/calib_reddit.py COMM MU GAMMA TAIL_ALPHA
 """
 import os
 import sys
@@ -10,7 +10,7 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from f3s_inputs import configs, dcsbm_w  # noqa: E402
+from f3s_inputs import configs  # noqa: E402
 
 
 def window_stats(csr):
@@ -31,10 +31,8 @@ def window_stats(csr):
 
 
 if __name__ == "__main__":
-    comm, mu, jitter, alpha = int(sys.argv[1]), float(sys.argv[2]), float(sys.argv[3]), float(sys.argv[4])
-    wref = float(sys.argv[5]) if len(sys.argv) > 5 else 0.0
+    comm, mu, gamma, alpha = int(sys.argv[1]), float(sys.argv[2]), float(sys.argv[3]), float(sys.argv[4])
     t0 = time.time()
-    w = configs.reddit_weights(232965, seed=1003, jitter=jitter, tail_alpha=alpha)
-    m = mu / (1.0 + w / wref) if wref > 0 else mu
-    csr = dcsbm_w(232965, 57_459_000, comm_size=comm, mu=m, weights=w, seed=1003)
+    sd = float(sys.argv[5]) if len(sys.argv) > 5 else 15.7
+    csr = configs.reddit_windows(232965, seed=1003, tail_alpha=alpha, comm_size=comm, mu=mu, gamma=gamma, ratio_sd=sd)
     print(sys.argv[1:], window_stats(csr), f"{time.time() - t0:.0f}s", flush=True)
