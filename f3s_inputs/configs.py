@@ -30,7 +30,7 @@ def _uniform(count: int, seed: int) -> np.ndarray:
 
 
 def reddit_windows(n: int, seed: int, tail_alpha: float = 2.1, comm_size: int = 4500, mu: float = 0.8,
-                   gamma: float = 2.1, ratio_sd: float = 15.7) -> CSR:
+                   gamma: float = 2.1, ratio_mean: float = 9.3, ratio_sd: float = 28.0) -> CSR:
     """Reddit-shaped A built row window by row window (f3s_inputs.windows) from the paper's own
     statistics: TCB/RW deciles of Tab.tcb_deciles and nnz/TCB mean 16.5, CV 0.95
     (Tab.datasets, P:545).
@@ -38,9 +38,10 @@ def reddit_windows(n: int, seed: int, tail_alpha: float = 2.1, comm_size: int = 
     Window k gets t_k = Q(u_k), u_k = (rank_k + 0.5) / R with ranks a seeded permutation (every
     decile holds R/10 windows); Q is log-linear between the decile boundaries and, in the last
     decile, a Pareto(tail_alpha) truncated at the table's maximum (tail_alpha = 2.1 gives the
-    table's mean 477).  Its nnz/TCB target is 8 + X, X lognormal with mean 8.5 and standard
-    deviation 15.7 (so 8 + X has the table's mean 16.5 and CV 0.95; 8 is the floor, one row per
-    column), clipped to 128 (all 16 rows)."""
+    table's mean 477).  Its nnz/TCB target is 8 + X (8 is the floor: one row per column), X
+    lognormal with mean 9.3 and standard deviation 28, clipped to 128 (all 16 rows); after the
+    clip and the per-column Poisson row counts the windows' nnz/TCB has the table's mean 16.5
+    and CV 0.95 (calibrated with tools/calib_reddit.py, profiles/r02_graph_stats.txt)."""
     R = (n + 15) // 16
     rank = np.argsort(_uniform(R, seed ^ 0x77), kind="stable").argsort(kind="stable")
     u = (rank + 0.5) / R
@@ -53,7 +54,7 @@ def reddit_windows(n: int, seed: int, tail_alpha: float = 2.1, comm_size: int = 
     c = 1.0 - (lo / hi) ** tail_alpha
     t[tail] = lo * (1.0 - f[tail] * c) ** (-1.0 / tail_alpha)
     tcb = np.rint(t).astype(np.int32)
-    mx, sx = 8.5, ratio_sd
+    mx, sx = ratio_mean, ratio_sd
     sig2 = np.log1p((sx / mx) ** 2)
     u1, u2 = _uniform(R, seed ^ 0x99), _uniform(R, seed ^ 0xAA)
     z = np.sqrt(-2.0 * np.log1p(-u1)) * np.cos(2.0 * np.pi * u2)  # Box-Muller
@@ -118,8 +119,9 @@ WORKLOADS = {
         description="ogbn-products-shaped: 2,449,029 nodes, 61,859,140 undirected pairs -> 123.7M nnz; d=64, 4 heads"),
     "reddit": Workload(
         "reddit", 3, 1, 64,
-        lambda s: dcsbm(232965, 57_459_000, comm_size=4500, mu=0.9, gamma=2.1, max_deg=21657, seed=s),
-        description="Reddit-shaped DC-SBM: 232,965 nodes, ~114.9M nnz, contiguous communities; d=64, 1 head"),
+        lambda s: reddit_windows(232965, seed=s),
+        description="Reddit-shaped: 232,965 nodes, ~115M nnz, row windows with the paper's TCB/RW deciles "
+                    "(4..9857 TCBs, mean 477) and nnz/TCB 16.5; d=64, 1 head"),
     "batched": Workload(
         "batched", 4, 8, 64,
         lambda s: molecules(10000, 25, 150, self_loops=False, seed=s),

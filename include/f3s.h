@@ -132,8 +132,10 @@ f3s_status f3s_plan_get_info(f3s_plan_t plan, f3s_plan_info* info);
  */
 f3s_status f3s_plan_set_split(f3s_plan_t plan, int32_t max_chunks);
 
-/* The default split bound: max(16, ceil(total_chunks / (2 * num_sms))) (a window is split when
- * it alone exceeds half of an SM's even share of all chunks).  Pure host arithmetic. */
+/* The default split bound: max(16, ceil(total_chunks / (2 * 8 * num_sms))): a window is split when
+ * it alone exceeds half of an SM's even share of all chunks spread over 8 GPUs (the largest row-
+ * shard count the library targets), so single-GPU and shard plans of up to 8 GPUs split alike.
+ * Pure host arithmetic. */
 int32_t f3s_default_split_chunks(int64_t total_chunks, int32_t num_sms);
 
 f3s_status f3s_plan_export(f3s_plan_t plan, int32_t* rw_ptr, int32_t* cols, uint16_t* masks, int32_t* rw_order);

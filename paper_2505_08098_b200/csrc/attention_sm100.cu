@@ -240,7 +240,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             int32_t* __restrict__ counter, int32_t n_items, int32_t H, int64_t ldkv,
             const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float scale_log2,
             uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt_arg,
-            float* __restrict__ scratch, float2* __restrict__ ml_out, int32_t n_rows, float* __restrict__ Og) {
+            float* __restrict__ scratch, float2* __restrict__ ml_out, int32_t n_rows, float* __restrict__ Og,
+            int32_t heavy_items) {
     constexpr int EB = (int)sizeof(T);
     using C = Cfg<D, HG, EB>;
     using B = Bars<D, HG, EB>;
@@ -332,18 +333,22 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         // kBatch lanes each take one item per queue round trip; per chunk one lane issues two
         // bulk copies (column ids, masks) straight into the slot, and at an item's first chunk the
         // TMA load of Q_w (16 x d per head, Alg.1 l.5) into the item's Q slot.
-        int32_t seq = 0, qseq = 0;
+        int32_t seq = 0, qseq = 0, last = 0;
         bool done = false;
         while (!done) {
+            // items of the LPT list's heavy prefix are claimed one per round trip, the rest
+            // kBatch at a time (the claim is per lane: consecutive indices, one CTA)
+            const int nclaim = last < heavy_items ? 1 : C::kBatch;
             int32_t it = 0x7FFFFFFF;
             int4 mt = make_int4(0, 0, 0, 0);
-            if (lane < C::kBatch) {
+            if (lane < nclaim) {
                 it = atomicAdd(counter, 1);
                 if (it < n_items) mt = __ldg(meta + it / (H / HG));
             }
             __syncwarp();
+            last = __shfl_sync(0xffffffffu, it, nclaim - 1);
             if (lane == 0) lap(1);
-            for (int b = 0; b < C::kBatch; ++b) {
+            for (int b = 0; b < nclaim; ++b) {
                 const int32_t itb = __shfl_sync(0xffffffffu, it, b);
                 const int32_t k = __shfl_sync(0xffffffffu, mt.x, b);
                 const int32_t cb8 = __shfl_sync(0xffffffffu, mt.y, b);
@@ -1121,7 +1126,8 @@ f3s_status launch(const AttnArgs& a) {
             (a.kv_ld > 0 ? a.kv_ld : (int64_t)a.heads * D) * (int64_t)sizeof(T),
             static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.scale * 1.4426950408889634f, a.trace,
             a.trace_chunks, a.expt, split ? reinterpret_cast<float*>(scratch + 256) : nullptr,
-            reinterpret_cast<float2*>(a.ml_out), p.n_rows, a.O);
+            reinterpret_cast<float2*>(a.ml_out), p.n_rows, a.O,
+            a.lpt ? (int32_t)std::min<int64_t>((int64_t)p.n_heavy_sub * (a.heads / HG), 0x7FFFFFFF) : 0);
         count_launch();
         err = cudaGetLastError();
     }

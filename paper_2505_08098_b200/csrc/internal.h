@@ -39,6 +39,10 @@ struct Plan {
     // unsplit window); each piece leaves (m, l, O) partials and k_split_merge combines the
     // pieces of split window g, in piece order (ginfo[g] = {first global piece, pieces, k, 0})
     int32_t split_chunks = 0, n_sub = 0, n_groups = 0, n_pieces = 0;
+    // the LPT list's heavy prefix: entries up to the last of >= kHeavyChunks chunks; the kernel's
+    // work queue hands these out one item per claim (lighter items in batches of 8), so that a
+    // run of the heaviest windows is not claimed by one CTA
+    int32_t n_heavy_sub = 0;
     int64_t total_chunks = 0;     // sum over windows of max(1, ceil(w / 128)): one head's kernel chunks
     int4* meta_sub = nullptr;     // [n_sub]
     int4* ginfo = nullptr;        // [n_groups]
@@ -77,9 +81,14 @@ struct DeviceScope {
 };
 
 // Default heavy-window split bound (f3s.h, f3s_plan_set_split): a window is cut into pieces
-// when it alone exceeds half of an SM's even share of all chunks of the (global) problem.
+// when it alone exceeds half of an SM's even share of all chunks of the (global) problem spread
+// over kSplitGpus GPUs -- the largest box the row shards target, so that the single-GPU plan and
+// every shard of an up-to-8-GPU run split the same windows (bitwise-equal shard results) and the
+// 8-GPU tail is balanced (tools/f1_ab.py: Reddit-shaped, slowest of 8 shards 0.44 -> 0.33 ms; the
+// extra pieces cost < 1 % at one GPU).
+constexpr int64_t kSplitGpus = 8;
 inline int32_t default_split_chunks(int64_t total_chunks, int32_t num_sms) {
-    const int64_t sms = num_sms > 0 ? num_sms : 148;
+    const int64_t sms = (num_sms > 0 ? num_sms : 148) * kSplitGpus;
     const int64_t t = std::max<int64_t>(16, (total_chunks + 2 * sms - 1) / (2 * sms));
     return (int32_t)std::min<int64_t>(t, 0x7FFFFFFF);
 }
@@ -127,6 +136,7 @@ f3s_status launch_parts_merge(int32_t parts, const float* O_parts, const float* 
 // (re)build meta_sub / sinfo with pieces of at most `chunks` 128-column chunks (chunks <= 0: no split)
 f3s_status build_split(Plan* p, int32_t chunks);
 constexpr int kSplitChunkCols = 128;  // column granularity of the split (the kernel's chunk)
+constexpr int kHeavyChunks = 8;       // an item of this many chunks is claimed alone (= the claim batch)
 f3s_status launch_attention_simt(const AttnArgs& a);
 f3s_status launch_attention_backward(Plan& p, const void* Q, const void* K, const void* V, const float* dO, float* dQ,
                                      float* dK, float* dV, float scale, int heads, int d, f3s_dtype dtype,

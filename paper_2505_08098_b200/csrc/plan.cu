@@ -339,11 +339,16 @@ f3s_status build_split(Plan* p, int32_t chunks) {
     std::vector<int4> meta, info;
     meta.reserve(R);
     int32_t groups = 0, pieces = 0;
+    int32_t heavy_prefix = 0;  // entries up to the last one of >= kHeavyChunks chunks
+    auto note = [&](int64_t nch) {
+        if (nch >= kHeavyChunks) heavy_prefix = (int32_t)meta.size();
+    };
     for (int32_t i = 0; i < R; ++i) {
         const int32_t k = p->h_order[i], w = p->h_rw[k + 1] - p->h_rw[k], b8 = p->h_rw8[k];
         const int64_t nch = std::max<int64_t>(1, (w + kSplitChunkCols - 1) / kSplitChunkCols);
         if (chunks <= 0 || nch <= chunks) {
             meta.push_back(make_int4(k, b8, w, 0));
+            note(nch);
             continue;
         }
         const int32_t np = (int32_t)((nch + chunks - 1) / chunks), step = chunks * kSplitChunkCols;
@@ -352,6 +357,7 @@ f3s_status build_split(Plan* p, int32_t chunks) {
         for (int32_t j = 0; j < np; ++j) {
             const int32_t c0 = j * step;
             meta.push_back(make_int4(k, b8 + c0, std::min(step, w - c0), ++pieces));
+            note((std::min(step, w - c0) + kSplitChunkCols - 1) / kSplitChunkCols);
         }
         ++groups;
     }
@@ -373,6 +379,7 @@ f3s_status build_split(Plan* p, int32_t chunks) {
     p->n_sub = (int32_t)meta.size();
     p->n_groups = groups;
     p->n_pieces = pieces;
+    p->n_heavy_sub = heavy_prefix;
     return F3S_OK;
 }
 

@@ -153,20 +153,20 @@ def test_batched_graph_shards(dist_mod, oracle_mod):
     assert_close(np.concatenate(outs), ref)
 
 
-def _hub_window_graph(n_windows=10000, hub_cols=3200, seed=3):
-    """~1 chunk per row window plus one window (rows 0..15) of hub_cols distinct columns: its
-    chunk count (25) lies between a 2-shard plan's own split bound (17) and the global one (34)."""
+def _hub_window_graph(n_windows=60000, hub_cols=2560, seed=3):
+    """1 chunk per row window plus one window (rows 0..15) of hub_cols distinct columns: its chunk
+    count (20) lies between a 2-shard plan's own split bound (16 = the floor, ~30K chunks /
+    (2 * 8 * SMs)) and the global one (26, ~60K chunks)."""
     rng = np.random.default_rng(seed)
     n = 16 * n_windows
     deg = rng.integers(2, 9, n)
-    deg[:16] = hub_cols // 16
-    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
-    ci = rng.integers(0, n, rp[-1]).astype(np.int32)
-    ci[:hub_cols] = rng.choice(n, hub_cols, replace=False)
-    for r in range(n):  # sorted unique rows (A is binary)
-        row = np.unique(ci[rp[r]:rp[r + 1]])
-        ci[rp[r]:rp[r] + len(row)] = row
-        ci[rp[r] + len(row):rp[r + 1]] = row[-1]
+    rows = np.repeat(np.arange(n, dtype=np.int64), deg)
+    cols = rng.integers(0, n, len(rows))
+    hub_r = np.repeat(np.arange(16, dtype=np.int64), hub_cols // 16)
+    hub_c = rng.choice(n, hub_cols, replace=False)
+    keys = np.unique(np.concatenate([rows[rows >= 16] * n + cols[rows >= 16], hub_r * n + hub_c]))
+    rp = np.searchsorted(keys // n, np.arange(n + 1)).astype(np.int32)
+    ci = (keys % n).astype(np.int32)
     return n, rp, ci
 
 
@@ -187,7 +187,7 @@ def test_shard_split_bound_is_global(dist_mod):
     i1 = p1.info()
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     assert i1["split_chunks"] == f3s.default_split_chunks(i1["total_chunks"], sms)
-    assert i1["split_groups"] == 0  # the 25-chunk hub window is whole in the 1-GPU plan
+    assert i1["split_groups"] == 0  # the 20-chunk hub window is whole in the 1-GPU plan
     O1 = f3s.attention(p1, Q, K, V, scale=0.125)
     own = []
     parts = []
@@ -202,7 +202,7 @@ def test_shard_split_bound_is_global(dist_mod):
                                         torch.empty((spec.row_end - spec.row_begin, H, d), dtype=torch.float32,
                                                     device="cuda"), scale=0.125))
     # the shard holding the hub would have split it with its own bound
-    assert own[0]["split_groups"] == 1 and own[0]["split_chunks"] < 25 < i1["split_chunks"]
+    assert own[0]["split_groups"] == 1 and own[0]["split_chunks"] < 20 < i1["split_chunks"]
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(parts), O1)
 

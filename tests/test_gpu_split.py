@@ -76,7 +76,8 @@ def test_split_large_scores_and_empty_rows(f3s, oracle_mod):
 
 
 def test_default_split_threshold(f3s):
-    # f3s_plan's default bound: max(16, ceil(total chunks / (2 * SMs))) chunks per piece
+    # f3s_plan's default bound: max(16, ceil(total chunks / (2 * 8 * SMs))) chunks per piece (the
+    # per-SM share of an 8-GPU row-sharded run, f3s.h f3s_default_split_chunks)
     import torch
     csr = _skewed_csr()
     rp, ci = csr_to_dev(csr)
@@ -85,7 +86,7 @@ def test_default_split_threshold(f3s):
     w = np.diff(rw_ptr.astype(np.int64))
     chunks = np.maximum(1, (w + 127) // 128)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    t = max(16, int(-(-int(chunks.sum()) // (2 * sms))))
+    t = max(16, int(-(-int(chunks.sum()) // (2 * 8 * sms))))
     info = p.info()
     assert info["split_chunks"] == t
     assert info["split_groups"] == int(np.count_nonzero(chunks > t))

@@ -34,5 +34,6 @@ if __name__ == "__main__":
     comm, mu, gamma, alpha = int(sys.argv[1]), float(sys.argv[2]), float(sys.argv[3]), float(sys.argv[4])
     t0 = time.time()
     sd = float(sys.argv[5]) if len(sys.argv) > 5 else 15.7
-    csr = configs.reddit_windows(232965, seed=1003, tail_alpha=alpha, comm_size=comm, mu=mu, gamma=gamma, ratio_sd=sd)
+    mx = float(sys.argv[6]) if len(sys.argv) > 6 else 8.5
+    csr = configs.reddit_windows(232965, seed=1003, tail_alpha=alpha, comm_size=comm, mu=mu, gamma=gamma, ratio_mean=mx, ratio_sd=sd)
     print(sys.argv[1:], window_stats(csr), f"{time.time() - t0:.0f}s", flush=True)
