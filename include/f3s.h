@@ -220,19 +220,30 @@ f3s_status f3s_attention_merge(int32_t parts, const float* O_parts, const float*
  *   dp_ij = dO_i . v_j,  D_i = sum_j p_ij dp_ij,  ds_ij = p_ij (dp_ij - D_i),
  *   dQ_i = scale sum_j ds_ij k_j,  dK_j = scale sum_i ds_ij q_i,  dV_j = sum_i p_ij dO_i,
  * with p the exact fp32 softmax of Eq.1 (the forward's rounding of P to the input dtype is not
- * differentiated).  Two deterministic passes (rows, then columns of A through a transposed index
- * the plan builds on its first backward call); no atomics on the data.
+ * differentiated).  Tensor-core path (default): the forward in partial mode gives each row's LSE and
+ * D = dO . O; a row pass (S^T = K_c Q_w^T, dP^T = V_c dO_w^T, dS^T, dQ^T += K_c^T dS^T on tcgen05,
+ * accumulated in TMEM) and a column pass over the plan of A^T (S = Q_c K_w^T, dP = dO_c V_w^T,
+ * dV^T += dO_c^T P, dK^T += Q_c^T dS); dO and dS enter the tensor cores rounded to the input dtype.
+ * The plan builds its transposed index and the plan of A^T on its first backward call.  Both passes
+ * are deterministic (fixed order, no atomics on the data).
  *
  *  Q, K, V   as for f3s_attention (device, [N, H, d] fp16/bf16, 16-byte aligned).
  *  dO        device fp32 [n_rows, H, d];  dQ device fp32 [n_rows, H, d] (written);
  *  dK, dV    device fp32 [n_cols, H, d] (written; for a row-shard plan (f3s_plan_rows) these are
  *            the shard's partial sums, to be all-reduced by the caller).
- * Asynchronous on `stream` (stream-ordered scratch of 8 * n_rows * H bytes).
+ * Asynchronous on `stream` (stream-ordered scratch of about n_rows * H * (6 d + 16) bytes).
  * Errors: as f3s_attention; INVALID_VALUE for NULL dO/dK/dV.
  */
 f3s_status f3s_attention_backward(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* dO,
                                   float* dQ, float* dK, float* dV, float scale, int32_t heads, int32_t d,
                                   f3s_dtype dtype, cudaStream_t stream);
+/* variant 0: the tensor-core path of f3s_attention_backward; 1: the CUDA-core two-pass kernels
+ * (one warp per row / column walking its entries in fp32: online max/sum/D, then p, ds; the
+ * reference for the tensor-core path).  Errors: as f3s_attention_backward; INVALID_VALUE for
+ * another variant. */
+f3s_status f3s_attention_backward_ex(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* dO,
+                                     float* dQ, float* dK, float* dV, float scale, int32_t heads, int32_t d,
+                                     f3s_dtype dtype, int32_t variant, cudaStream_t stream);
 
 /* Kernel variants for ablations (bench.py --variant); f3s_attention uses F3S_VARIANT_DEFAULT. */
 typedef enum {

@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libf3s.so")
-SOURCES = ["f3s_api.cu", "plan.cu", "attention_simt.cu", "attention_sm100.cu", "backward.cu"]
+SOURCES = ["f3s_api.cu", "plan.cu", "attention_simt.cu", "attention_sm100.cu", "backward.cu", "backward_sm100.cu"]
 HEADERS = ["internal.h", "sm100.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -979,9 +979,8 @@ __global__ void __launch_bounds__(256) k_parts_merge(int32_t parts, const float*
     }
 }
 
-namespace {
-
 // ---- host side ------------------------------------------------------------------------------------
+// tensor-map helpers (also used by backward_sm100.cu; declared in internal.h)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1060,6 +1059,9 @@ f3s_status make_map(CUtensorMap* map, const void* base, f3s_dtype dtype, int64_t
     return make_map(map, base, dtype == F3S_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                     inner, rows, ld, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
+
+
+namespace {
 
 template <int D, typename T, int HG>
 f3s_status launch(const AttnArgs& a) {

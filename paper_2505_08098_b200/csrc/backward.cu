@@ -517,6 +517,21 @@ f3s_status launch_bwd(Plan& p, const void* Q, const void* K, const void* V, cons
 
 }  // namespace
 
+// Plan of A^T (rows = columns of A, compacted columns = rows of A) for the tensor-core column
+// pass: built once per plan from the transposed index, under the plan's transpose lock.
+f3s_status build_transpose_plan(Plan& p, cudaStream_t stream) {
+    f3s_status st = build_transpose(p, stream);
+    if (st != F3S_OK) return st;
+    std::lock_guard<std::mutex> lock(p.transpose_mu);
+    if (p.tplan) return F3S_OK;
+    Plan* tp = nullptr;
+    const int32_t* col_idx = p.col_rows;
+    st = build_plan(p.col_ptr, col_idx, p.n_cols, p.n_rows, true, stream, &tp);
+    if (st != F3S_OK) return st;
+    p.tplan = tp;
+    return F3S_OK;
+}
+
 f3s_status launch_attention_backward(Plan& p, const void* Q, const void* K, const void* V, const float* dO, float* dQ,
                                      float* dK, float* dV, float scale, int heads, int d, f3s_dtype dtype,
                                      cudaStream_t stream) {

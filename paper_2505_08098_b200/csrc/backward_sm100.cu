@@ -1,0 +1,668 @@
+// backward_sm100.cu — the backward of the fused 3S pass on tcgen05 tensor cores (
+// "the backward pass ... involves SpMM and SDDMM operations in reverse order").
+//
+// For O = softmax_row(scale * (Q K^T) (.) A) V and dO = dL/dO (f3s.h f3s_attention_backward):
+//   p_ij = 2^(s_ij - LSE_i)   (s in log2 units incl. scale; LSE_i from the forward's (m, l)),
+//   D_i  = dO_i . O_i,   dp_ij = dO_i . v_j,   ds_ij = p_ij (dp_ij - D_i),
+//   dQ_i = scale sum_j ds_ij k_j,   dK_j = scale sum_i ds_ij q_i,   dV_j = sum_i p_ij dO_i.
+// Steps (host, launch_attention_backward_tc):
+//   1. the forward in partial mode (unnormalised O, (m, l) per row) and a prep kernel: LSE, D and a
+//      copy of dO in the input dtype (the tensor cores multiply 16-bit operands);
+//   2. ROW pass over the plan of A, one item per (row window, head), chunks of <= 128 compacted
+//      columns (the forward's pipeline with the roles kept): gathered K_c, V_c; per item Q_w, dO_w;
+//        MMA1   S^T  = K_c Q_w^T,  dP^T = V_c dO_w^T          (SDDMM twice)
+//        elementwise  dS^T = P^T (.) (dP^T - D)               (masked by the bitmap)
+//        MMA2   dQ^T += K_c^T dS^T                            (SpMM, accumulated in TMEM)
+//   3. COLUMN pass over the plan of A^T (row windows of 16 key columns, compacted query rows):
+//      gathered Q_c, dO_c (+ their LSE, D); per item K_w, V_w;
+//        MMA1   S = Q_c K_w^T,  dP = dO_c V_w^T;   elementwise P, dS = P (.) (dP - D)
+//        MMA2   dV^T += dO_c^T P,   dK^T += Q_c^T dS          (accumulated in TMEM)
+// Both passes are deterministic (fixed chunk order per item, no atomics on the data).
+//
+// One CTA per SM, warps with fixed roles (the forward's structure, attention_sm100.cu):
+//   0 index (work queue in LPT order, chunk slots, per-item tiles), 1 MMA1, 2 MMA2, loaders
+//   (16-byte cp.async gathers into 128B-swizzled tile slots), two elementwise warpgroups on
+//   alternate chunks, one epilogue warpgroup (TMEM accumulators -> shared tile -> TMA store).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <type_traits>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace f3s {
+namespace {
+
+using namespace sm100;
+
+template <int D, int PASS>  // PASS 0: rows (dQ), 1: columns (dK, dV)
+struct BCfg {
+    static constexpr int RB = D * 2;                 // bytes of one gathered row of one head
+    static constexpr int P = RB / 128;               // 128-byte panels per row
+    static constexpr int kRowPitch = 128 * P;
+    static constexpr int kGroupBytes = 1024 * P;     // 8 rows (one swizzle atom per panel)
+    static constexpr int kMaxRows = 128;
+    static constexpr int kTile = (kMaxRows / 8) * kGroupBytes;
+    // S/dP TMEM buffers and P/dS shared tiles, chunk slots, per-item tile slots (X and Y: 16 x D
+    // each): fewer at d = 128 so that two 32 KB tile slots per gathered operand still fit
+    static constexpr int kSB = D == 128 ? 2 : 4;
+    static constexpr int kNS = D == 128 ? 12 : 16;
+    static constexpr int kNQ = D == 128 ? 2 : 4;
+    static constexpr int kXBytes = 16 * kRowPitch;
+    static constexpr int kQBytes = 2 * kXBytes;
+    static constexpr int kNT = PASS == 0 ? 1 : 2;    // 16-bit tiles written per chunk: dS (rows); P, dS (cols)
+    static constexpr int kPBytes = 16 * kMaxRows * 2;
+    static constexpr int kNG = PASS == 0 ? 1 : 2;    // gradient accumulators: dQ; dV, dK
+    static constexpr int kOBytes = 16 * D * 4;       // one [16 x D] fp32 staging tile
+    static constexpr int kScal = PASS == 0 ? 16 : 128;  // LSE / D values per chunk slot
+    static constexpr int kSlotBytes = 32 + kMaxRows * 4 + kMaxRows * 2 + 2 * kScal * 4;
+    static constexpr int kNumBars = 5 * kNS + 2 * kNQ + 4 * kSB + 4 + 2 * 16;
+    static constexpr int kFixed = kNQ * kQBytes + kSB * kNT * kPBytes + kNG * kOBytes + kNS * kSlotBytes +
+                                  kNumBars * 8 + 64 + 16;
+    static constexpr int kN1 = (227 * 1024 - kFixed) / kTile / 2;  // A1 / A2 tile slots
+    static constexpr int kN2 = kN1;
+    static_assert(kN1 >= 2, "two tile slots per operand at least");
+    static constexpr int oT1 = 0, oT2 = kN1 * kTile;
+    static constexpr int oQ = (kN1 + kN2) * kTile;
+    static constexpr int oP = oQ + kNQ * kQBytes;
+    static constexpr int oOst = oP + kSB * kNT * kPBytes;
+    static constexpr int oSlot = oOst + kNG * kOBytes;
+    static constexpr int oRec = oSlot + kNS * kSlotBytes;  // int4 [2] accumulator records
+    static constexpr int oBar = oRec + 64;
+    static constexpr int oTmem = oBar + kNumBars * 8;
+    static constexpr int kSmemBytes = oTmem + 16;
+    static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
+    // TMEM: S (kSB x 16), dP (kSB x 16), gradient accumulators (2 item buffers x kNG x 16)
+    static constexpr int kTmS = 0, kTmP = 16 * kSB, kTmG = 32 * kSB;
+    static constexpr int kTmemCols = 256;
+    static_assert(kTmG + 2 * kNG * 16 <= kTmemCols, "TMEM columns");
+    static constexpr int kLoaderWarps = 6;
+    static constexpr int kLoader0 = 3, kEw0 = kLoader0 + kLoaderWarps, kEpi0 = kEw0 + 8;
+    static constexpr int kThreads = 32 * (kEpi0 + 4);
+    static constexpr int kBatch = 8;
+};
+
+template <int D, int PASS> struct BBars {
+    using C = BCfg<D, PASS>;
+    __host__ __device__ static constexpr int idxfull(int s) { return s; }
+    __host__ __device__ static constexpr int a1full(int s) { return C::kNS + s; }
+    __host__ __device__ static constexpr int a2full(int s) { return 2 * C::kNS + s; }
+    __host__ __device__ static constexpr int empty(int s) { return 3 * C::kNS + s; }
+    __host__ __device__ static constexpr int xyfull(int q) { return 5 * C::kNS + q; }
+    __host__ __device__ static constexpr int xyempty(int q) { return 5 * C::kNS + C::kNQ + q; }
+    static constexpr int kB0 = 5 * C::kNS + 2 * C::kNQ;
+    __host__ __device__ static constexpr int sfull(int b) { return kB0 + b; }
+    __host__ __device__ static constexpr int sfree(int b) { return kB0 + C::kSB + b; }
+    __host__ __device__ static constexpr int pfull(int b) { return kB0 + 2 * C::kSB + b; }
+    __host__ __device__ static constexpr int pempty(int b) { return kB0 + 3 * C::kSB + b; }
+    __host__ __device__ static constexpr int gfull(int a) { return kB0 + 4 * C::kSB + a; }
+    __host__ __device__ static constexpr int gempty(int a) { return kB0 + 4 * C::kSB + 2 + a; }
+    __host__ __device__ static constexpr int t1free(int t) { return kB0 + 4 * C::kSB + 4 + t; }
+    __host__ __device__ static constexpr int t2free(int t) { return kB0 + 4 * C::kSB + 4 + 16 + t; }
+};
+
+template <int kScal> struct __align__(16) BSlot {
+    int32_t rw, head, rows, qslot, flags, pad0, pad1, pad2;
+    int32_t cols[128];
+    uint16_t masks[128];
+    float lse[kScal];  // log2-domain LSE of the chunk's query rows (rows: the window's 16; cols: per entry)
+    float dd[kScal];   // D = dO . O of the same rows
+};
+
+template <typename T> __device__ __forceinline__ uint32_t bpack2(float lo, float hi);
+template <> __device__ __forceinline__ uint32_t bpack2<__half>(float lo, float hi) { return pack_f16x2(lo, hi); }
+template <> __device__ __forceinline__ uint32_t bpack2<__nv_bfloat16>(float lo, float hi) { return pack_bf16x2(lo, hi); }
+
+// store 16 values of chunk entry p as row p of an MN-major SW32 [128 x 16] B-operand tile (the
+// forward's P^T layout): one 32-byte row per entry, 8 rows per 256-byte atom, halves swapped when
+// bit 2 of p is set
+template <typename T>
+__device__ __forceinline__ void store_tile_row(uint8_t* tile, int p, const float (&v)[16]) {
+    uint4* prow = reinterpret_cast<uint4*>(tile + (p >> 3) * 256 + (p & 7) * 32);
+    const int sw = (p >> 2) & 1;
+    prow[sw] = make_uint4(bpack2<T>(v[0], v[1]), bpack2<T>(v[2], v[3]), bpack2<T>(v[4], v[5]), bpack2<T>(v[6], v[7]));
+    prow[sw ^ 1] = make_uint4(bpack2<T>(v[8], v[9]), bpack2<T>(v[10], v[11]), bpack2<T>(v[12], v[13]),
+                              bpack2<T>(v[14], v[15]));
+}
+
+template <int D, typename T, int PASS>
+__global__ void __launch_bounds__(BCfg<D, PASS>::kThreads, 1)
+k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
+            const __grid_constant__ CUtensorMap tmG1, const __grid_constant__ CUtensorMap tmG2,
+            const int4* __restrict__ meta, const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
+            int32_t* __restrict__ counter, int32_t n_items, int32_t heavy_items, int32_t H,
+            const uint8_t* __restrict__ A1g, const uint8_t* __restrict__ A2g, int64_t ld_bytes,
+            const float* __restrict__ lse_t, const float* __restrict__ dd_t, int64_t nq16, float scale_log2,
+            float g2scale, float g1scale) {
+    using C = BCfg<D, PASS>;
+    using B = BBars<D, PASS>;
+    using Slot = BSlot<C::kScal>;
+    static_assert(sizeof(Slot) == C::kSlotBytes, "slot layout");
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t sb = smem_u32(smem);
+    if (sb & 1023) __trap();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto bar = [&](int i) -> uint32_t { return sb + C::oBar + 8u * i; };
+    Slot* slots = reinterpret_cast<Slot*>(smem + C::oSlot);
+    int4* rec = reinterpret_cast<int4*>(smem + C::oRec);
+
+    for (int i = threadIdx.x; i < (C::kN1 + C::kN2) * C::kTile / 16; i += blockDim.x)
+        reinterpret_cast<int4*>(smem)[i] = make_int4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < C::kNS * C::kSlotBytes / 16; i += blockDim.x)
+        reinterpret_cast<int4*>(smem + C::oSlot)[i] = make_int4(0, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::kNS; ++s) {
+            mbar_init(bar(B::idxfull(s)), 1);
+            mbar_init(bar(B::a1full(s)), 32 * C::kLoaderWarps);
+            mbar_init(bar(B::a2full(s)), 32 * C::kLoaderWarps);
+            mbar_init(bar(B::empty(s)), 1);
+        }
+        for (int q = 0; q < C::kNQ; ++q) {
+            mbar_init(bar(B::xyfull(q)), 1);
+            mbar_init(bar(B::xyempty(q)), 1);
+        }
+        for (int b = 0; b < C::kSB; ++b) {
+            mbar_init(bar(B::sfull(b)), 1);
+            mbar_init(bar(B::sfree(b)), 4);
+            mbar_init(bar(B::pfull(b)), 128);
+            mbar_init(bar(B::pempty(b)), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(bar(B::gfull(a)), 2);  // MMA completion + the MMA2 warp's record
+            mbar_init(bar(B::gempty(a)), 128);
+        }
+        for (int t = 0; t < C::kN1; ++t) mbar_init(bar(B::t1free(t)), 1);
+        for (int t = 0; t < C::kN2; ++t) mbar_init(bar(B::t2free(t)), 1);
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmX);
+        tma_prefetch_desc(&tmY);
+        tma_prefetch_desc(&tmG1);
+        if (PASS == 1) tma_prefetch_desc(&tmG2);
+    }
+    if (warp == 1) {
+        tmem_alloc<C::kTmemCols>(sb + C::oTmem);
+        tmem_relinquish();
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + C::oTmem);
+    constexpr int chunk_rows = C::kMaxRows;
+
+    if (warp == 0) {
+        // ===== index warp: items in LPT order (heavy prefix one per claim) -> chunk slots =====
+        int32_t seq = 0, qseq = 0, last = 0;
+        bool done = false;
+        while (!done) {
+            const int nclaim = last < heavy_items ? 1 : C::kBatch;
+            int32_t it = 0x7FFFFFFF;
+            int4 mt = make_int4(0, 0, 0, 0);
+            if (lane < nclaim) {
+                it = atomicAdd(counter, 1);
+                if (it < n_items) mt = __ldg(meta + it / H);
+            }
+            __syncwarp();
+            last = __shfl_sync(0xffffffffu, it, nclaim - 1);
+            for (int b = 0; b < nclaim; ++b) {
+                const int32_t itb = __shfl_sync(0xffffffffu, it, b);
+                const int32_t k = __shfl_sync(0xffffffffu, mt.x, b);
+                const int32_t cb8 = __shfl_sync(0xffffffffu, mt.y, b);
+                const int32_t w = __shfl_sync(0xffffffffu, mt.z, b);
+                if (itb >= n_items) { done = true; continue; }
+                const int32_t h = itb - (itb / H) * H;
+                const int nch = w > 0 ? (w + chunk_rows - 1) / chunk_rows : 1;
+                const int qs = qseq % C::kNQ;
+                const int qph = (qseq / C::kNQ) & 1;
+                if (lane == 0) {  // the item's 16-row tiles X and Y (rows: Q_w, dO_w; cols: K_w, V_w)
+                    mbar_wait_lazy(bar(B::xyempty(qs)), qph ^ 1);
+                    mbar_arrive_expect_tx(bar(B::xyfull(qs)), C::kQBytes);
+                    const uint32_t xd = sb + C::oQ + qs * C::kQBytes;
+#pragma unroll
+                    for (int pp = 0; pp < C::P; ++pp) {
+                        tma_load_2d(xd + pp * 2048, &tmX, bar(B::xyfull(qs)), h * D + 64 * pp, 16 * k);
+                        tma_load_2d(xd + C::kXBytes + pp * 2048, &tmY, bar(B::xyfull(qs)), h * D + 64 * pp, 16 * k);
+                    }
+                }
+                for (int j = 0; j < nch; ++j) {
+                    const int rows = w > 0 ? min(chunk_rows, w - chunk_rows * j) : 0;
+                    const int s = seq % C::kNS;
+                    if (lane == 0) {
+                        mbar_wait_lazy(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+                        Slot& sl = slots[s];
+                        sl.rw = k;
+                        sl.head = h;
+                        sl.rows = rows;
+                        sl.qslot = qs;
+                        sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2);
+                        const uint32_t fb = bar(B::idxfull(s));
+                        const uint32_t r8 = (uint32_t)((rows + 7) & ~7);
+                        const uint32_t scal = PASS == 0 ? 2u * 64u : 0u;  // rows: the window's 16 LSE and D
+                        mbar_arrive_expect_tx(fb, (rows > 0 ? r8 * 6u : 0u) + scal);
+                        if (rows > 0) {
+                            bulk_g2s(smem_u32(sl.cols), kcols + cb8 + chunk_rows * j, r8 * 4u, fb);
+                            bulk_g2s(smem_u32(sl.masks), kmasks + cb8 + chunk_rows * j, r8 * 2u, fb);
+                        }
+                        if (PASS == 0) {
+                            bulk_g2s(smem_u32(sl.lse), lse_t + h * nq16 + 16 * (int64_t)k, 64u, fb);
+                            bulk_g2s(smem_u32(sl.dd), dd_t + h * nq16 + 16 * (int64_t)k, 64u, fb);
+                        }
+                    }
+                    ++seq;
+                }
+                ++qseq;
+            }
+        }
+        if (lane == 0) {
+            for (int w = 0; w < 2; ++w, ++seq) {  // one stop marker per elementwise warpgroup
+                const int s = seq % C::kNS;
+                mbar_wait_lazy(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+                slots[s].rows = -1 - w;
+                mbar_arrive(bar(B::idxfull(s)));
+            }
+        }
+        __syncwarp();
+    } else if (warp >= C::kLoader0 && warp < C::kLoader0 + C::kLoaderWarps) {
+        // ===== loaders: the chunk's A1 and A2 rows (+ cols: their LSE and D) =====================
+        constexpr int kPieces = C::RB / 16;
+        constexpr int kRowsPerOp = 32 / kPieces;
+        constexpr int kIters = (C::kMaxRows / kRowsPerOp + C::kLoaderWarps - 1) / C::kLoaderWarps;
+        const int lw = warp - C::kLoader0;
+        const int piece = lane % kPieces, rsub = lane / kPieces;
+        const int pnl = piece >> 3, cc = piece & 7;
+        for (int32_t seq = 0;; ++seq) {
+            const int s = seq % C::kNS;
+            mbar_wait(bar(B::idxfull(s)), (seq / C::kNS) & 1);
+            Slot& sl = slots[s];
+            const int rows = sl.rows;
+            const uint32_t f1 = bar(B::a1full(s)), f2 = bar(B::a2full(s));
+            if (rows < 0) {
+                mbar_arrive(f1);
+                mbar_arrive(f2);
+                break;
+            }
+            const int h = sl.head;
+            const int t1 = seq % C::kN1, t2 = seq % C::kN2;
+            const uint32_t d1 = sb + C::oT1 + t1 * C::kTile + pnl * 1024;
+            const uint32_t d2 = sb + C::oT2 + t2 * C::kTile + pnl * 1024;
+            const uint8_t* b1 = A1g + (int64_t)h * C::RB + piece * 16;
+            const uint8_t* b2 = A2g + (int64_t)h * C::RB + piece * 16;
+            const int ops = (rows + kRowsPerOp - 1) / kRowsPerOp;
+            mbar_wait(bar(B::t1free(t1)), ((seq / C::kN1) & 1) ^ 1);
+            mbar_wait(bar(B::t2free(t2)), ((seq / C::kN2) & 1) ^ 1);
+            int64_t jj[kIters];
+            uint32_t dst[kIters];
+            int rr[kIters];
+            bool ok[kIters];
+#pragma unroll
+            for (int i = 0; i < kIters; ++i) {
+                const int t = lw + i * C::kLoaderWarps;
+                const int r = t * kRowsPerOp + rsub;
+                ok[i] = t < ops && r < rows;
+                rr[i] = r;
+                jj[i] = ok[i] ? sl.cols[r] : 0;
+                dst[i] = (uint32_t)(r >> 3) * C::kGroupBytes + (uint32_t)(r & 7) * 128 + (uint32_t)((cc ^ (r & 7)) << 4);
+            }
+#pragma unroll
+            for (int i = 0; i < kIters; ++i)
+                if (ok[i]) cp_async_16(d1 + dst[i], b1 + jj[i] * ld_bytes);
+            if (PASS == 1) {  // the gathered query rows' LSE and D (one lane per row)
+#pragma unroll
+                for (int i = 0; i < kIters; ++i)
+                    if (ok[i] && piece == 0) {
+                        cp_async_4(smem_u32(&sl.lse[rr[i]]), lse_t + h * nq16 + jj[i]);
+                        cp_async_4(smem_u32(&sl.dd[rr[i]]), dd_t + h * nq16 + jj[i]);
+                    }
+            }
+            cp_async_mbar_arrive(f1);
+#pragma unroll
+            for (int i = 0; i < kIters; ++i)
+                if (ok[i]) cp_async_16(d2 + dst[i], b2 + jj[i] * ld_bytes);
+            cp_async_mbar_arrive(f2);
+        }
+    } else if (warp == 1) {
+        // ===== MMA1: S^T = A1_c . X^T and dP^T = A2_c . Y^T (swap-AB, M = 128, N = 16) =========
+        constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+        constexpr uint32_t idesc1 = idesc_f16(fmt, 0, 0, 128, 16);
+        const uint64_t dA = smem_desc_sw128(0, 16, C::kGroupBytes);
+        const uint64_t dX = smem_desc_sw128(0, 16, 1024);
+        for (int32_t n1 = 0;; ++n1) {
+            const int s = n1 % C::kNS, b = n1 % C::kSB;
+            mbar_wait(bar(B::a1full(s)), (n1 / C::kNS) & 1);
+            mbar_wait(bar(B::a2full(s)), (n1 / C::kNS) & 1);
+            const Slot& sl = slots[s];
+            const int rows = sl.rows, flags = sl.flags, qslot = sl.qslot;
+            if (rows < 0) break;
+            mbar_wait(bar(B::sfree(b)), ((n1 / C::kSB) & 1) ^ 1);
+            if (flags & 1) mbar_wait(bar(B::xyfull(qslot)), (flags >> 2) & 1);
+            tc_fence_after();
+            if (rows > 0) {
+                const uint64_t a1 = dA + ((sb + C::oT1 + (n1 % C::kN1) * C::kTile) >> 4);
+                const uint64_t a2 = dA + ((sb + C::oT2 + (n1 % C::kN2) * C::kTile) >> 4);
+                const uint64_t bx = dX + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
+                const uint64_t by = dX + ((sb + C::oQ + qslot * C::kQBytes + C::kXBytes) >> 4);
+#pragma unroll
+                for (int kk = 0; kk < C::RB / 32; ++kk) {
+                    const uint32_t ao = ((kk >> 2) * 1024 + (kk & 3) * 32) >> 4;
+                    const uint32_t bo = ((kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
+                    mma_f16_ss_warp(tmem + C::kTmS + b * 16, a1 + ao, bx + bo, idesc1, kk > 0 ? 1u : 0u);
+                    mma_f16_ss_warp(tmem + C::kTmP + b * 16, a2 + ao, by + bo, idesc1, kk > 0 ? 1u : 0u);
+                }
+            }
+            mma_commit_warp(bar(B::sfull(b)));
+            if (flags & 2) mma_commit_warp(bar(B::xyempty(qslot)));
+        }
+        __syncwarp();
+    } else if (warp == 2) {
+        // ===== MMA2: gradients accumulated in TMEM over the item's chunks ==========================
+        //   rows: dQ^T += K_c^T dS^T;   cols: dV^T += dO_c^T P,  dK^T += Q_c^T dS
+        constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+        constexpr uint32_t idesc2 = idesc_f16(fmt, 1, 1, D, 16);
+        const uint64_t dA = smem_desc_sw128(0, 1024, C::kGroupBytes);
+        const uint64_t dPt = smem_desc_sw32(0, 4096, 256);
+        int32_t item = 0;
+        bool any = false;
+        for (int32_t n2 = 0;; ++n2) {
+            const int s = n2 % C::kNS, b = n2 % C::kSB, a = item & 1;
+            mbar_wait(bar(B::a1full(s)), (n2 / C::kNS) & 1);
+            mbar_wait(bar(B::a2full(s)), (n2 / C::kNS) & 1);
+            const Slot& sl = slots[s];
+            const int rows = sl.rows, flags = sl.flags, rw = sl.rw, hd = sl.head;
+            if (rows < 0) {  // tell the epilogue to stop (its next record)
+                mbar_wait(bar(B::gempty(a)), ((item >> 1) & 1) ^ 1);
+                if (lane == 0) {
+                    rec[a] = make_int4(-1, 0, 0, 0);
+                    mbar_arrive(bar(B::gfull(a)));
+                    mbar_arrive(bar(B::gfull(a)));
+                }
+                break;
+            }
+            mbar_wait(bar(B::pfull(b)), (n2 / C::kSB) & 1);
+            if (flags & 1) {
+                mbar_wait(bar(B::gempty(a)), ((item >> 1) & 1) ^ 1);
+                any = false;
+            }
+            tc_fence_after();
+            if (rows > 0) {
+                const uint64_t a1 = dA + ((sb + C::oT1 + (n2 % C::kN1) * C::kTile) >> 4);
+                const uint64_t a2 = dA + ((sb + C::oT2 + (n2 % C::kN2) * C::kTile) >> 4);
+                const uint64_t p0 = dPt + ((sb + C::oP + b * C::kNT * C::kPBytes) >> 4);
+                const int nsteps = (rows + 15) / 16;
+                for (int st = 0; st < nsteps; ++st) {
+                    const uint32_t acc = (any || st > 0) ? 1u : 0u;
+                    const uint32_t ao = (st * 2 * C::kGroupBytes) >> 4, po = (st * 512) >> 4;
+                    if (PASS == 0) {
+                        mma_f16_ss_warp(tmem + C::kTmG + a * 16, a1 + ao, p0 + po, idesc2, acc);
+                    } else {
+                        mma_f16_ss_warp(tmem + C::kTmG + a * 32, a2 + ao, p0 + po, idesc2, acc);           // dV
+                        mma_f16_ss_warp(tmem + C::kTmG + a * 32 + 16, a1 + ao, p0 + (C::kPBytes >> 4) + po,  // dK
+                                        idesc2, acc);
+                    }
+                }
+                any = true;
+            }
+            mma_commit_warp(bar(B::pempty(b)));
+            mma_commit_warp(bar(B::t1free(n2 % C::kN1)));
+            mma_commit_warp(bar(B::t2free(n2 % C::kN2)));
+            mma_commit_warp(bar(B::empty(s)));
+            if (flags & 2) {
+                if (lane == 0) rec[a] = make_int4(rw, hd, any ? 1 : 0, 0);
+                mma_commit_warp(bar(B::gfull(a)));
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar(B::gfull(a)));
+                ++item;
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+    } else if (warp < C::kEpi0) {
+        // ===== elementwise warpgroups (alternate chunks) ==========================================
+        // TMEM lane p = chunk entry p (rows: compacted column j; cols: compacted query row i), the 16
+        // TMEM columns = the window's 16 query rows (rows) or key columns (cols)
+        const int q = warp & 3;
+        const int p = 32 * q + lane;
+        const int wg = (warp - C::kEw0) >> 2;
+        const uint32_t tl = (uint32_t)(32 * q) << 16;
+        for (int32_t seq = wg;; seq += 2) {
+            const int s = seq % C::kNS, b = seq % C::kSB;
+            const uint32_t bph = (seq / C::kSB) & 1;
+            mbar_wait(bar(B::idxfull(s)), (seq / C::kNS) & 1);
+            const Slot& sl = slots[s];
+            const int rows = sl.rows;
+            if (rows < 0) break;
+            if (PASS == 1) mbar_wait(bar(B::a1full(s)), (seq / C::kNS) & 1);  // the gathered LSE and D
+            const uint32_t mask = p < rows ? (uint32_t)sl.masks[p] : 0u;
+            float lse_p = 0.f, dd_p = 0.f;
+            if (PASS == 1) {
+                lse_p = sl.lse[p];
+                dd_p = sl.dd[p];
+            }
+            mbar_wait(bar(B::sfull(b)), bph);
+            tc_fence_after();
+            float x[16], y[16];
+            tmem_ld_32x32b_x16(tmem + tl + C::kTmS + b * 16, x);
+            tmem_ld_32x32b_x16(tmem + tl + C::kTmP + b * 16, y);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(B::sfree(b)));
+            float pr[16], ds[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float l = PASS == 0 ? sl.lse[i] : lse_p;
+                const float dd = PASS == 0 ? sl.dd[i] : dd_p;
+                const float pv = ((mask >> i) & 1u) ? ex2(fmaf(x[i], scale_log2, -l)) : 0.f;
+                pr[i] = pv;
+                ds[i] = pv * (y[i] - dd);
+            }
+            mbar_wait(bar(B::pempty(b)), bph ^ 1);
+            uint8_t* tile = smem + C::oP + b * C::kNT * C::kPBytes;
+            if (PASS == 0) {
+                store_tile_row<T>(tile, p, ds);
+            } else {
+                store_tile_row<T>(tile, p, pr);
+                store_tile_row<T>(tile + C::kPBytes, p, ds);
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(bar(B::pfull(b)));
+        }
+    } else {
+        // ===== epilogue: accumulators -> [16 x D] fp32 tiles -> TMA stores =========================
+        const int q = warp & 3;
+        const uint32_t tl = (uint32_t)(32 * q) << 16;
+        const bool has = D == 128 || lane < 16;
+        const int f = D == 128 ? 32 * q + lane : 16 * q + lane;  // accumulator lane -> feature
+        const bool lead = threadIdx.x == 32 * C::kEpi0;
+        for (int32_t item = 0;; ++item) {
+            const int a = item & 1;
+            mbar_wait(bar(B::gfull(a)), (item >> 1) & 1);
+            const int4 r = rec[a];
+            if (r.x < 0) break;
+            tc_fence_after();
+            float g1[16], g2[16];
+            tmem_ld_32x32b_x16(tmem + tl + C::kTmG + a * 16 * C::kNG, g1);
+            if (PASS == 1) tmem_ld_32x32b_x16(tmem + tl + C::kTmG + a * 32 + 16, g2);
+            tc_fence_before();
+            mbar_arrive(bar(B::gempty(a)));
+            const bool nz = r.z != 0;  // an item with no entries has an untouched accumulator: zeros
+            if (lead) bulk_wait_group_read<0>();
+            named_bar_sync(3, 128);
+            float* o1 = reinterpret_cast<float*>(smem + C::oOst);
+            float* o2 = o1 + 16 * D;
+            if (has) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    o1[i * D + f] = nz ? g1[i] * g1scale : 0.f;
+                    if (PASS == 1) o2[i * D + f] = nz ? g2[i] * g2scale : 0.f;
+                }
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(3, 128);
+            if (lead) {
+                tma_store_2d(&tmG1, sb + C::oOst, r.y * D, 16 * r.x);
+                if (PASS == 1) tma_store_2d(&tmG2, sb + C::oOst + C::kOBytes, r.y * D, 16 * r.x);
+                bulk_commit_group();
+            }
+        }
+        if (lead) bulk_wait_group<0>();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<C::kTmemCols>(tmem);
+    }
+}
+
+// LSE (log2 units incl. scale), D = dO . O and dO in the input dtype, from the forward's partial
+// outputs (unnormalised O, (m, l)); one warp per (row, head).  Head-major LSE / D ([H][nq16]).
+template <int D, typename T>
+__global__ void __launch_bounds__(256) k_bwd_prep(const float* __restrict__ Op, const float2* __restrict__ ml,
+                                                  const float* __restrict__ dO, int64_t n_rows, int32_t H,
+                                                  int64_t nq16, float* __restrict__ lse_t, float* __restrict__ dd_t,
+                                                  T* __restrict__ dO16) {
+    constexpr int E = D / 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t rh = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; rh < n_rows * H; rh += nw) {
+        const int64_t i = rh / H;
+        const int h = (int)(rh - i * H);
+        const float2 v = ml[rh];
+        const float inv = v.y > 0.f ? 1.f / v.y : 0.f;
+        float acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int64_t o = rh * D + lane * E + e;
+            const float g = dO[o];
+            acc = fmaf(g, Op[o] * inv, acc);
+            if constexpr (std::is_same<T, __half>::value) dO16[o] = __float2half_rn(g);
+            else dO16[o] = __float2bfloat16_rn(g);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            lse_t[h * nq16 + i] = v.y > 0.f ? v.x + __log2f(v.y) : INFINITY;  // empty row: p = 0
+            dd_t[h * nq16 + i] = acc;
+        }
+    }
+}
+
+template <int D, typename T, int PASS>
+f3s_status launch_pass(const Plan& p, const void* X, const void* Y, const void* A1, const void* A2, float* G1,
+                       float* G2, const float* lse_t, const float* dd_t, int64_t nq16, int H, float scale,
+                       int sms, cudaStream_t stream) {
+    using C = BCfg<D, PASS>;
+    if (p.num_rw == 0) return F3S_OK;
+    const f3s_dtype dt = std::is_same<T, __half>::value ? F3S_FP16 : F3S_BF16;
+    const int64_t ld = (int64_t)H * D;
+    CUtensorMap mx, my, mg1, mg2;
+    f3s_status st;
+    if ((st = make_map(&mx, X, dt, ld, p.n_rows, ld, 16)) != F3S_OK) return st;
+    if ((st = make_map(&my, Y, dt, ld, p.n_rows, ld, 16)) != F3S_OK) return st;
+    if ((st = make_map(&mg1, G1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ld, p.n_rows, ld, D, 16,
+                       CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK)
+        return st;
+    mg2 = mg1;
+    if (PASS == 1 &&
+        (st = make_map(&mg2, G2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ld, p.n_rows, ld, D, 16, CU_TENSOR_MAP_SWIZZLE_NONE)) !=
+            F3S_OK)
+        return st;
+    static std::atomic<uint64_t> attr_set{0};
+    static std::mutex mu;
+    if (!(attr_set.load() >> p.device & 1)) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!(attr_set.load() >> p.device & 1)) {
+            F3S_CUDA_TRY(cudaFuncSetAttribute(k_bwd_sm100<D, T, PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              C::kSmemBytes));
+            attr_set.fetch_or(uint64_t(1) << p.device);
+        }
+    }
+    const int64_t n_items64 = (int64_t)p.num_rw * H;
+    if (n_items64 > 0x7FFFFFFF) { set_error("too many work items"); return F3S_ERR_UNSUPPORTED; }
+    char* scratch = nullptr;
+    F3S_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&scratch), 256, stream));
+    cudaError_t err = cudaMemsetAsync(scratch, 0, sizeof(int32_t), stream);
+    if (err == cudaSuccess) {
+        const int grid = (int)std::min<int64_t>(n_items64, sms);
+        k_bwd_sm100<D, T, PASS><<<grid, C::kThreads, C::kSmemBytes, stream>>>(
+            mx, my, mg1, mg2, p.meta_lpt, p.kcols, p.kmasks, reinterpret_cast<int32_t*>(scratch), (int32_t)n_items64,
+            (int32_t)std::min<int64_t>((int64_t)p.n_heavy_lpt * H, 0x7FFFFFFF), H,
+            static_cast<const uint8_t*>(A1), static_cast<const uint8_t*>(A2), ld * 2, lse_t, dd_t, nq16,
+            scale * 1.4426950408889634f, scale, PASS == 0 ? scale : 1.f);
+        count_launch();
+        err = cudaGetLastError();
+    }
+    const cudaError_t ferr = scratch_free(scratch, stream);
+    F3S_CUDA_TRY(err);
+    F3S_CUDA_TRY(ferr);
+    return F3S_OK;
+}
+
+struct Scratch2 {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    ~Scratch2() { if (p) scratch_free(p, s); }
+};
+
+template <int D, typename T>
+f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, const float* dO, float* dQ, float* dK,
+                         float* dV, float scale, int H, cudaStream_t stream) {
+    f3s_status st = build_transpose_plan(p, stream);
+    if (st != F3S_OK) return st;
+    Plan& tp = *p.tplan;
+    int sms = 148;
+    F3S_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
+    const int64_t n = p.n_rows, nd = n * H * D;
+    const int64_t nq16 = (n + 15) / 16 * 16 + 16;
+    Scratch2 sc;
+    sc.s = stream;
+    const int64_t nh2 = (n * H + 1) / 2 * 2;  // keeps the arrays after (m, l) 16-byte aligned
+    const size_t bytes = sizeof(float) * (size_t)nd + sizeof(float2) * (size_t)nh2 +
+                         2 * sizeof(float) * (size_t)(H * nq16) + sizeof(T) * (size_t)nd + 256;
+    F3S_CUDA_TRY(scratch_alloc(&sc.p, bytes, stream));
+    char* base = static_cast<char*>(sc.p);
+    float* Op = reinterpret_cast<float*>(base);
+    float* ml = Op + nd;
+    float* lse_t = ml + 2 * nh2;
+    float* dd_t = lse_t + H * nq16;
+    T* dO16 = reinterpret_cast<T*>(dd_t + H * nq16);
+    // 1. the forward's (m, l) and unnormalised O
+    AttnArgs a{&p, Q, K, V, Op, scale, H, D, std::is_same<T, __half>::value ? F3S_FP16 : F3S_BF16, true, stream};
+    a.ml_out = ml;
+    if ((st = launch_attention_sm100(a)) != F3S_OK) return st;
+    k_bwd_prep<D, T><<<(int)std::min<int64_t>((n * H + 7) / 8, (int64_t)sms * 16), 256, 0, stream>>>(
+        Op, reinterpret_cast<const float2*>(ml), dO, n, H, nq16, lse_t, dd_t, dO16);
+    count_launch();
+    F3S_CUDA_TRY(cudaGetLastError());
+    // 2. rows: dQ
+    if ((st = launch_pass<D, T, 0>(p, Q, dO16, K, V, dQ, nullptr, lse_t, dd_t, nq16, H, scale, sms, stream)) != F3S_OK)
+        return st;
+    // 3. columns: dV (G1), dK (G2) over A^T
+    if (tp.n_rows > 0 && tp.nnz == 0) {
+        F3S_CUDA_TRY(cudaMemsetAsync(dK, 0, sizeof(float) * (size_t)tp.n_rows * H * D, stream));
+        F3S_CUDA_TRY(cudaMemsetAsync(dV, 0, sizeof(float) * (size_t)tp.n_rows * H * D, stream));
+        return F3S_OK;
+    }
+    return launch_pass<D, T, 1>(tp, K, V, Q, dO16, dV, dK, lse_t, dd_t, nq16, H, scale, sms, stream);
+}
+
+}  // namespace
+
+f3s_status launch_attention_backward_tc(Plan& p, const void* Q, const void* K, const void* V, const float* dO,
+                                        float* dQ, float* dK, float* dV, float scale, int heads, int d,
+                                        f3s_dtype dtype, cudaStream_t stream) {
+    if (dtype == F3S_FP16)
+        return d == 64 ? launch_bwd_tc<64, __half>(p, Q, K, V, dO, dQ, dK, dV, scale, heads, stream)
+                       : launch_bwd_tc<128, __half>(p, Q, K, V, dO, dQ, dK, dV, scale, heads, stream);
+    return d == 64 ? launch_bwd_tc<64, __nv_bfloat16>(p, Q, K, V, dO, dQ, dK, dV, scale, heads, stream)
+                   : launch_bwd_tc<128, __nv_bfloat16>(p, Q, K, V, dO, dQ, dK, dV, scale, heads, stream);
+}
+
+}  // namespace f3s

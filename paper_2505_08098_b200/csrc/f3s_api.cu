@@ -162,6 +162,7 @@ f3s_status f3s_plan_rows(const int32_t* row_ptr, const int32_t* col_idx, int32_t
 f3s_status f3s_plan_destroy(f3s_plan_t plan) {
     if (!plan) return F3S_OK;
     Plan* p = reinterpret_cast<Plan*>(plan);
+    if (p->tplan) f3s_plan_destroy(reinterpret_cast<f3s_plan_t>(p->tplan));
     cudaFree(p->rw_ptr);
     cudaFree(p->cols);
     cudaFree(p->masks);
@@ -244,6 +245,12 @@ f3s_status f3s_attention(f3s_plan_t plan, const void* Q, const void* K, const vo
 f3s_status f3s_attention_backward(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* dO,
                                   float* dQ, float* dK, float* dV, float scale, int32_t heads, int32_t d,
                                   f3s_dtype dtype, cudaStream_t stream) {
+    return f3s_attention_backward_ex(plan, Q, K, V, dO, dQ, dK, dV, scale, heads, d, dtype, 0, stream);
+}
+
+f3s_status f3s_attention_backward_ex(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* dO,
+                                     float* dQ, float* dK, float* dV, float scale, int32_t heads, int32_t d,
+                                     f3s_dtype dtype, int32_t variant, cudaStream_t stream) {
     try {
         f3s_status st = check_attention_args(plan, Q, K, V, dQ, scale, heads, d, dtype, true);
         if (st != F3S_OK) return st;
@@ -251,10 +258,13 @@ f3s_status f3s_attention_backward(f3s_plan_t plan, const void* Q, const void* K,
         Plan& p = *reinterpret_cast<Plan*>(plan);
         if (p.n_rows > 0 && !dO) { set_error("dO is NULL"); return F3S_ERR_INVALID_VALUE; }
         if (p.n_cols > 0 && (!dK || !dV)) { set_error("dK/dV is NULL"); return F3S_ERR_INVALID_VALUE; }
+        if (variant != 0 && variant != 1) { set_error("backward variant must be 0 or 1"); return F3S_ERR_INVALID_VALUE; }
         auto mis = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) != 0; };
         if (mis(dO) || mis(dK) || mis(dV)) { set_error("dO/dK/dV must be 16-byte aligned"); return F3S_ERR_UNSUPPORTED; }
         DeviceScope scope;
         F3S_CUDA_TRY(scope.enter(p.device));
+        if (variant == 0 && p.nnz > 0 && p.n_rows > 0)
+            return launch_attention_backward_tc(p, Q, K, V, dO, dQ, dK, dV, scale, heads, d, dtype, stream);
         return launch_attention_backward(p, Q, K, V, dO, dQ, dK, dV, scale, heads, d, dtype, stream);
     } catch (...) {
         set_error("internal error");

@@ -1,6 +1,7 @@
 // internal.h — shared declarations of libf3s (not part of the C ABI).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
@@ -66,6 +67,8 @@ struct Plan {
     std::mutex staging_mu;
     std::vector<Staging> staging;
     std::mutex transpose_mu;  // the backward's transposed index is built once, under this lock
+    Plan* tplan = nullptr;    // plan of A^T for the tensor-core backward's column pass (built on first use)
+    int32_t n_heavy_lpt = 0;  // heavy prefix of the unsplit LPT list (meta_lpt), as n_heavy_sub
 };
 
 // Switch the calling thread to `dev` for the scope of a call and restore its device after.
@@ -130,6 +133,12 @@ struct AttnArgs {
 };
 
 f3s_status launch_attention_sm100(const AttnArgs& a);
+// 2-D tensor maps over a row-major [rows, inner] matrix (ld elements between rows); 16-bit / 8-bit
+// inputs get 128-byte boxes with the 128-byte swizzle of the UMMA tiles, fp32 an unswizzled box
+f3s_status make_map(CUtensorMap* map, const void* base, CUtensorMapDataType type, int64_t inner, int64_t rows,
+                    int64_t ld, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz);
+f3s_status make_map(CUtensorMap* map, const void* base, f3s_dtype dtype, int64_t inner, int64_t rows, int64_t ld,
+                    uint32_t box_rows);
 f3s_status launch_fill_ml(float* ml, int64_t rows_heads, cudaStream_t stream);
 f3s_status launch_parts_merge(int32_t parts, const float* O_parts, const float* ml_parts, int64_t rows_heads, int32_t d,
                               float* O, cudaStream_t stream);
@@ -138,6 +147,10 @@ f3s_status build_split(Plan* p, int32_t chunks);
 constexpr int kSplitChunkCols = 128;  // column granularity of the split (the kernel's chunk)
 constexpr int kHeavyChunks = 8;       // an item of this many chunks is claimed alone (= the claim batch)
 f3s_status launch_attention_simt(const AttnArgs& a);
+f3s_status build_transpose_plan(Plan& p, cudaStream_t stream);
+f3s_status launch_attention_backward_tc(Plan& p, const void* Q, const void* K, const void* V, const float* dO,
+                                        float* dQ, float* dK, float* dV, float scale, int heads, int d,
+                                        f3s_dtype dtype, cudaStream_t stream);
 f3s_status launch_attention_backward(Plan& p, const void* Q, const void* K, const void* V, const float* dO, float* dQ,
                                      float* dK, float* dV, float scale, int heads, int d, f3s_dtype dtype,
                                      cudaStream_t stream);

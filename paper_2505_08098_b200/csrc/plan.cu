@@ -340,12 +340,14 @@ f3s_status build_split(Plan* p, int32_t chunks) {
     meta.reserve(R);
     int32_t groups = 0, pieces = 0;
     int32_t heavy_prefix = 0;  // entries up to the last one of >= kHeavyChunks chunks
+    int32_t heavy_lpt = 0;     // the same over the unsplit list
     auto note = [&](int64_t nch) {
         if (nch >= kHeavyChunks) heavy_prefix = (int32_t)meta.size();
     };
     for (int32_t i = 0; i < R; ++i) {
         const int32_t k = p->h_order[i], w = p->h_rw[k + 1] - p->h_rw[k], b8 = p->h_rw8[k];
         const int64_t nch = std::max<int64_t>(1, (w + kSplitChunkCols - 1) / kSplitChunkCols);
+        if (nch >= kHeavyChunks) heavy_lpt = i + 1;
         if (chunks <= 0 || nch <= chunks) {
             meta.push_back(make_int4(k, b8, w, 0));
             note(nch);
@@ -380,6 +382,7 @@ f3s_status build_split(Plan* p, int32_t chunks) {
     p->n_groups = groups;
     p->n_pieces = pieces;
     p->n_heavy_sub = heavy_prefix;
+    p->n_heavy_lpt = heavy_lpt;
     return F3S_OK;
 }
 

@@ -54,6 +54,7 @@ _lib.f3s_attention_merge.argtypes = [_i32, _vp, _vp, _i64, _i32, _i32, _vp, _vp]
 _lib.f3s_attention_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_trace.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]
 _lib.f3s_attention_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_backward_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_host_async.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_partition_rows.argtypes = [_vp, _i32, _i32, _vp]
@@ -67,14 +68,14 @@ _lib.f3s_launch_count.restype = _i64
 for _name in ("f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
               "f3s_attention", "f3s_attention_kv", "f3s_attention_strided", "f3s_attention_partial",
               "f3s_attention_merge", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host", "f3s_partition_rows",
-              "f3s_partition_at", "f3s_attention_backward", "f3s_attention_host_async"):
+              "f3s_partition_at", "f3s_attention_backward", "f3s_attention_backward_ex", "f3s_attention_host_async"):
     getattr(_lib, _name).restype = _i32
 
 EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info", "f3s_plan_export", "f3s_plan_set_split",
             "f3s_attention", "f3s_attention_kv", "f3s_attention_strided", "f3s_attention_partial",
             "f3s_attention_merge", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host",
             "f3s_partition_rows", "f3s_partition_at",
-            "f3s_attention_backward", "f3s_attention_host_async", "f3s_default_split_chunks",
+            "f3s_attention_backward", "f3s_attention_backward_ex", "f3s_attention_host_async", "f3s_default_split_chunks",
             "f3s_status_string", "f3s_last_error", "f3s_launch_count"]
 
 
@@ -292,17 +293,22 @@ def attention_raw(p: Plan, q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, scale
            "f3s_attention")
 
 
-def attention_backward(p: Plan, Q, K, V, dO, *, scale: float, stream=None):
-    """f3s_attention_backward: (dQ, dK, dV) fp32 device tensors for dO = dL/dO (fp32 [N, H, d])."""
+BACKWARD_VARIANTS = {"tc": 0, "simt": 1}
+
+
+def attention_backward(p: Plan, Q, K, V, dO, *, scale: float, stream=None, variant: str = "tc"):
+    """f3s_attention_backward(_ex): (dQ, dK, dV) fp32 device tensors for dO = dL/dO (fp32 [N, H, d]);
+    variant "tc" (tensor cores, the default) or "simt" (the CUDA-core kernels)."""
     import torch
     _check_tensors(p, Q, K, V, dO, what="f3s_attention_backward")
     H, d = Q.shape[1], Q.shape[2]
     dQ = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
     dK = torch.empty(K.shape, dtype=torch.float32, device=K.device)
     dV = torch.empty(V.shape, dtype=torch.float32, device=V.device)
-    _check(_lib.f3s_attention_backward(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), dO.data_ptr(),
-                                       dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(), float(scale), H, d,
-                                       _dtype_code(Q), _stream(stream)), "f3s_attention_backward")
+    _check(_lib.f3s_attention_backward_ex(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), dO.data_ptr(),
+                                          dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(), float(scale), H, d,
+                                          _dtype_code(Q), BACKWARD_VARIANTS[variant], _stream(stream)),
+           "f3s_attention_backward")
     return dQ, dK, dV
 
 

@@ -1,6 +1,6 @@
 """Time f3s_attention_backward on a bench workload and print one JSON line.
 
-  python tools/bench_backward.py [--config arxiv] [--steps 20 --warmup 5]
+  python tools/bench_backward.py [--config arxiv] [--steps 20 --warmup 5] [--variant tc|simt]
 
 useful FLOPs per call: 8 * nnz * d * H (dP = dO V^T, dQ, dK, dV; the recomputed scores are not
 counted).  Algorithmic bytes per call (HBM bound, no reuse across rows or columns):
@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", default="arxiv")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--variant", default="tc", choices=["tc", "simt"])
     a = ap.parse_args()
     import torch
     from f3s_inputs import configs
@@ -39,12 +40,12 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(1)
     dO = torch.randn(Q.shape, generator=g, device="cuda", dtype=torch.float32)
     for _ in range(a.warmup):
-        f3s.attention_backward(p, Q, K, V, dO, scale=w.scale)
+        f3s.attention_backward(p, Q, K, V, dO, scale=w.scale, variant=a.variant)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(a.steps):
-        f3s.attention_backward(p, Q, K, V, dO, scale=w.scale)
+        f3s.attention_backward(p, Q, K, V, dO, scale=w.scale, variant=a.variant)
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / a.steps
@@ -61,7 +62,9 @@ def main():
                       "config": {"workload": a.config, "n": N, "nnz": nnz, "heads": H, "d": d, "dtype": w.dtype},
                       "roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                    "frac": round(gbs / peaks["hbm_gbs"], 4), "alg_bytes_per_call": int(alg)},
-                      "kernels": "k_bwd_rows + k_bwd_cols (CUDA cores)"}))
+                      "variant": a.variant,
+                      "kernels": ("forward (partial) + k_bwd_prep + k_bwd_sm100 rows + k_bwd_sm100 columns (tcgen05)"
+                                  if a.variant == "tc" else "k_bwd_rows + k_bwd_cols (CUDA cores)")}))
 
 
 if __name__ == "__main__":
