@@ -102,7 +102,7 @@ struct Cfg {
     static constexpr int kTmemCols = kTmemUsed <= 128 ? 128 : kTmemUsed <= 256 ? 256 : 512;
     static_assert(kTmemUsed <= 512, "TMEM columns");
     static constexpr int kSlotBytes = 32 + 128 * 4 + 128 * 2;  // sizeof(Slot)
-    static constexpr int kCorrBytes = 352;                  // sizeof(CorrSlot)
+    static constexpr int kCorrBytes = HG == 4 ? 608 : 352;  // sizeof(CorrSlotT<HG>)
     static constexpr int kNumBars = 4 * kNS + 2 * kNQ + 5 * kSB + 2 * 16;
     // everything but the gathered tiles
     static constexpr int kFixedBytes = kNQ * kQBytes + kSB * kPBytes + kNO * kOBytes + kNS * kSlotBytes +
@@ -184,12 +184,17 @@ struct __align__(16) Slot {
 // softmax -> correction hand-off for one chunk (one per S/P/O buffer)
 struct __align__(16) CorrSlot {
     float m[16];         // the chunk's row max m_c (log2 units, floored; Alg.1 l.16)
-    float lpart[4][16];  // per-warp partial row sums of the chunk's unrounded E = 2^(S - m_c) (l.17)
+    float lpart[4][16];  // per-warp partial row sums of the chunk's E = 2^(S - m_c) (l.17; reading c7)
     int32_t rows, flags, rw, head;
     uint64_t t_s, t_p;   // F3S_TRACE stamps of the softmax group (written out by the correction group)
 };
+struct __align__(16) CorrSlotHG : CorrSlot {
+    float mh[4][16];     // head groups: head g's row maxima (warp g), for partial-mode outputs
+};
+template <int HG> using CorrSlotT = typename std::conditional<HG == 4, CorrSlotHG, CorrSlot>::type;
 
-static_assert(sizeof(CorrSlot) == Cfg<64>::kCorrBytes && sizeof(Slot) == Cfg<64>::kSlotBytes, "layout");
+static_assert(sizeof(CorrSlot) == Cfg<64>::kCorrBytes && sizeof(CorrSlotHG) == Cfg<64, 4>::kCorrBytes &&
+              sizeof(Slot) == Cfg<64>::kSlotBytes, "layout");
 
 // Transposing butterfly: 16 per-row values in each of 32 lanes -> lane l holds the
 // reduction over the warp for row (l >> 1) & 15.  16 shuffles.
@@ -233,7 +238,8 @@ template <> __device__ __forceinline__ float round_to<__nv_fp8_e4m3>(float v) { 
 // and a row with no entry in a chunk keeps m_c = floor and an all-zero E (reading c5).
 constexpr float kMFloor = -8.5e37f;
 
-template <int D, typename T, bool kDiag, int HG>
+// kPart: head-group kernel in partial mode (unnormalised O and per-head (m, l); f3s_attention_partial)
+template <int D, typename T, bool kDiag, int HG, bool kPart = false>
 __global__ void __launch_bounds__(Cfg<D, HG, (int)sizeof(T)>::kThreads, Cfg<D, HG, (int)sizeof(T)>::kCtasPerSm)
 k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, const int4* __restrict__ meta,
             const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
@@ -252,7 +258,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto bar = [&](int i) -> uint32_t { return sb + C::oBar + 8u * i; };
     Slot* slots = reinterpret_cast<Slot*>(smem + C::oSlot);
-    CorrSlot* corr = reinterpret_cast<CorrSlot*>(smem + C::oCorr);
+    CorrSlotT<HG>* corr = reinterpret_cast<CorrSlotT<HG>*>(smem + C::oCorr);
     // Sensitivity experiments exist only in the diagnostics instantiation (f3s_attention_trace
     // with trace_chunks < 0; results are wrong): bit0 no exp work in the softmax, bit1 no MMA2,
     // bit2 no MMA1, bit3 no K/V gathers, bit5 no S load / row max, bit6 no O stores, bit7 no
@@ -615,6 +621,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             // chunk row max (Alg.1 l.16)
             float cm[16];
             float mrow = kMFloor;  // HG = 1, lanes 0..15: the chunk max of row `lane` (reading c5 floor)
+            float rm_hg = kMFloor;  // HG = 4, lane 2i: row i's max of the warp's head
             if constexpr (HG == 1 && F3S_MAX_REDUX) {
                 // the warp's 32 columns: one redux.sync.max per row (uniform datapath), then the
                 // 4-warp combine through shared memory; lane i < 16 finishes row i and broadcasts
@@ -649,9 +656,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 #pragma unroll
                 for (int i = 1; i < 16; ++i) mrow = lane == i ? cm[i] : mrow;
             } else {  // the warp holds all columns of its head: lane 2i has row i's max
-                const float rm = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
+                rm_hg = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
 #pragma unroll
-                for (int i = 0; i < 16; ++i) cm[i] = __shfl_sync(0xffffffffu, rm, 2 * i);
+                for (int i = 0; i < 16; ++i) cm[i] = __shfl_sync(0xffffffffu, rm_hg, 2 * i);
             }
             // S^T_b and red[b] are read: MMA1 may refill buffer b (its next chunk is this
             // warpgroup's own, so red[b] is rewritten only after this chunk's combine)
@@ -705,12 +712,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             if (!C::kLsumMMA && !(lane & 1)) corr[b].lpart[q][(lane >> 1) & 15] = rl;
             if (HG == 1 && q == 0 && lane < 16) corr[b].m[lane] = mrow;
+            if constexpr (HG > 1 && kPart)
+                if (!(lane & 1)) corr[b].mh[q][lane >> 1] = fmaxf(kMFloor, rm_hg);
             if (p == 0) {
-                if (HG > 1) {
-                    float4* m4 = reinterpret_cast<float4*>(corr[b].m);
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) m4[g] = make_float4(cm[4 * g], cm[4 * g + 1], cm[4 * g + 2], cm[4 * g + 3]);
-                }
                 reinterpret_cast<int4*>(&corr[b].rows)[0] = make_int4(rows, flags, rw, hd);
                 if (kDiag) {
                     corr[b].t_s = t_s;
@@ -780,7 +784,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     float ov[16];
                     tmem_ld_32x32b_x16(tmem + tl + C::kTmemO + (b * HG + g) * 16, ov);
                     const float4* l4 = reinterpret_cast<const float4*>(corr[b].lpart[g]);  // head g's row sums
-                    if (has) {
+                    if (has && !kPart) {
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const float4 lv = l4[u];
@@ -791,7 +795,16 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                                 ost[i * (HG * D) + g * D + f] = (rows > 0 && lt[v] > 0.f) ? ov[i] * rcp_approx(lt[v]) : 0.f;
                             }
                         }
+                    } else if (has) {  // partial mode: unnormalised O, the head's (m, l) below
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) ost[i * (HG * D) + g * D + f] = rows > 0 ? ov[i] : 0.f;
                     }
+                }
+                if (kPart && q == 0 && lane < 16 && 16 * rw + lane < n_rows) {
+#pragma unroll
+                    for (int g = 0; g < HG; ++g)
+                        ml_out[(int64_t)(16 * rw + lane) * H + hd + g] =
+                            rows > 0 ? make_float2(static_cast<const CorrSlotHG&>(corr[b]).mh[g][lane], corr[b].lpart[g][lane]) : make_float2(kMFloor, 0.f);
                 }
                 tc_fence_before();
                 mbar_arrive(bar(B::pempty(b)));
@@ -1099,6 +1112,9 @@ f3s_status launch(const AttnArgs& a) {
                                               C::kSmemBytes));
             F3S_CUDA_TRY(cudaFuncSetAttribute(k_f3s_sm100<D, T, true, HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               C::kSmemBytes));
+            if (HG > 1)
+                F3S_CUDA_TRY(cudaFuncSetAttribute(k_f3s_sm100<D, T, false, HG, true>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
             attr_set.fetch_or(uint64_t(1) << dev);
         }
     }
@@ -1109,7 +1125,6 @@ f3s_status launch(const AttnArgs& a) {
     const int64_t n_items64 = (int64_t)(a.lpt ? p.n_sub : p.num_rw) * (a.heads / HG);
     if (n_items64 > 0x7FFFFFFF) { set_error("too many work items"); return F3S_ERR_UNSUPPORTED; }
     const int32_t n_items = (int32_t)n_items64;
-    if (a.ml_out && HG > 1) { set_error("internal: partial mode with head groups"); return F3S_ERR_INTERNAL; }
     int64_t ctas = (int64_t)sms * C::kCtasPerSm;
     if (a.max_ctas > 0) ctas = std::min<int64_t>(ctas, a.max_ctas);  // SMs left free for a concurrent collective
     const int grid = a.grid_override > 0 ? a.grid_override : (int)std::min<int64_t>(n_items, ctas);
@@ -1122,7 +1137,8 @@ f3s_status launch(const AttnArgs& a) {
     int32_t* counter = reinterpret_cast<int32_t*>(scratch);
     cudaError_t err = cudaMemsetAsync(counter, 0, sizeof(int32_t), a.stream);
     if (err == cudaSuccess) {
-        auto kern = (a.trace || a.expt) ? k_f3s_sm100<D, T, true, HG> : k_f3s_sm100<D, T, false, HG>;
+        auto kern = (a.trace || a.expt) ? k_f3s_sm100<D, T, true, HG>
+                    : (HG > 1 && a.ml_out) ? k_f3s_sm100<D, T, false, HG, true> : k_f3s_sm100<D, T, false, HG>;
         kern<<<grid, C::kThreads, C::kSmemBytes, a.stream>>>(
             mq, mo, a.lpt ? p.meta_sub : p.meta_nat, p.kcols, p.kmasks, counter, n_items, a.heads,
             (a.kv_ld > 0 ? a.kv_ld : (int64_t)a.heads * D) * (int64_t)sizeof(T),
@@ -1157,7 +1173,7 @@ f3s_status launch_attention_sm100(const AttnArgs& a) {
     }
     // head groups of 4 when every row window fits one 32-column block (d = 64): the per-chunk
     // pipeline cost is shared by 4 heads (batched small graphs)
-    const bool hg4 = !a.one_head && !a.ml_out && a.d == 64 && a.heads % 4 == 0 && p.max_width <= 32 && p.n_groups == 0;
+    const bool hg4 = !a.one_head && a.d == 64 && a.heads % 4 == 0 && p.max_width <= 32 && p.n_groups == 0;
     if (a.dtype == F3S_FP16) {
         if (hg4) return launch<64, __half, 4>(a);
         return a.d == 64 ? launch<64, __half, 1>(a) : launch<128, __half, 1>(a);

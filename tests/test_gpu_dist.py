@@ -149,3 +149,37 @@ def test_column_block_partials_merge(oracle_mod, parts, H, d, dtype):
         O1 = f3s.attention(plans[0], Q, K, V, scale=0.125)
         l = mlp[0, :, :, 1:2]
         assert torch.allclose(torch.where(l > 0, Op[0] / l, torch.zeros_like(Op[0])), O1, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("parts,H", [(1, 4), (3, 8)])
+def test_column_block_partials_head_groups(oracle_mod, parts, H):
+    """Partial mode on head-group plans (d = 64, H % 4 == 0, every window <= 32 columns: the
+    batched-molecules shape): the head-group epilogue leaves unnormalised O and each head's (m, l);
+    merged in block order they equal the oracle, and with one block O / l is the plain call."""
+    import torch
+
+    from helpers import assert_close, to_dev
+    from paper_2505_08098_b200 import f3s
+    g = fi.molecules(400, 25, 150, seed=parts)
+    n, d = g.n_rows, 64
+    Qb, Kb, Vb = make_qkv(n, n, H, d, "fp16", seed=9)
+    Q, K, V = to_dev(Qb, "fp16"), to_dev(Kb, "fp16"), to_dev(Vb, "fp16")
+    blocks = _column_blocks(g.row_ptr, g.col_idx, n, parts)
+    Op = torch.empty((parts, n, H, d), dtype=torch.float32, device="cuda")
+    mlp = torch.empty((parts, n, H, 2), dtype=torch.float32, device="cuda")
+    plans = []
+    for b, (rp, ci) in enumerate(blocks):
+        p = f3s.plan_rows(torch.from_numpy(rp).cuda(), torch.from_numpy(ci if len(ci) else np.zeros(1, np.int32)).cuda(),
+                          n, n)
+        assert p.info()["max_width"] <= 32
+        plans.append(p)
+        f3s.attention_partial_raw(p, Q.data_ptr(), K.data_ptr(), V.data_ptr(), 0, Op[b].data_ptr(), mlp[b].data_ptr(),
+                                  0.125, H, d, f3s.FP16, 0, torch.cuda.current_stream().cuda_stream)
+    O = f3s.attention_merge(Op, mlp)
+    torch.cuda.synchronize()
+    ref = oracle_mod.attention(g.row_ptr, g.col_idx, Qb, Kb, Vb, scale=0.125, dtype="fp16")
+    assert_close(O.cpu().numpy(), ref)
+    if parts == 1:
+        O1 = f3s.attention(plans[0], Q, K, V, scale=0.125)
+        l = mlp[0, :, :, 1:2]
+        assert torch.allclose(torch.where(l > 0, Op[0] / l, torch.zeros_like(Op[0])), O1, rtol=1e-5, atol=1e-6)
