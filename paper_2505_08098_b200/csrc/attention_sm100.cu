@@ -1120,9 +1120,10 @@ f3s_status launch(const AttnArgs& a) {
     }
     const int sms = num_sms[dev].load();
     // default variant: the LPT list with heavy row windows split into pieces (Plan::meta_sub)
-    const bool split = a.lpt && p.n_groups > 0;
+    const bool split = a.lpt && p.n_groups > 0 && a.sub_begin == 0;  // pieces lead the LPT list
     if (split && HG > 1) { set_error("internal: head groups with split windows"); return F3S_ERR_INTERNAL; }
-    const int64_t n_items64 = (int64_t)(a.lpt ? p.n_sub : p.num_rw) * (a.heads / HG);
+    const int32_t sub_end = a.sub_end < 0 ? p.n_sub : a.sub_end;
+    const int64_t n_items64 = (int64_t)(a.lpt ? sub_end - a.sub_begin : p.num_rw) * (a.heads / HG);
     if (n_items64 > 0x7FFFFFFF) { set_error("too many work items"); return F3S_ERR_UNSUPPORTED; }
     const int32_t n_items = (int32_t)n_items64;
     int64_t ctas = (int64_t)sms * C::kCtasPerSm;
@@ -1140,12 +1141,14 @@ f3s_status launch(const AttnArgs& a) {
         auto kern = (a.trace || a.expt) ? k_f3s_sm100<D, T, true, HG>
                     : (HG > 1 && a.ml_out) ? k_f3s_sm100<D, T, false, HG, true> : k_f3s_sm100<D, T, false, HG>;
         kern<<<grid, C::kThreads, C::kSmemBytes, a.stream>>>(
-            mq, mo, a.lpt ? p.meta_sub : p.meta_nat, p.kcols, p.kmasks, counter, n_items, a.heads,
+            mq, mo, a.lpt ? p.meta_sub + a.sub_begin : p.meta_nat, p.kcols, p.kmasks, counter, n_items, a.heads,
             (a.kv_ld > 0 ? a.kv_ld : (int64_t)a.heads * D) * (int64_t)sizeof(T),
             static_cast<const uint8_t*>(a.K), static_cast<const uint8_t*>(a.V), a.scale * 1.4426950408889634f, a.trace,
             a.trace_chunks, a.expt, split ? reinterpret_cast<float*>(scratch + 256) : nullptr,
             reinterpret_cast<float2*>(a.ml_out), p.n_rows, a.O,
-            a.lpt ? (int32_t)std::min<int64_t>((int64_t)p.n_heavy_sub * (a.heads / HG), 0x7FFFFFFF) : 0);
+            a.lpt ? (int32_t)std::min<int64_t>((int64_t)std::max(0, p.n_heavy_sub - a.sub_begin) * (a.heads / HG),
+                                               0x7FFFFFFF)
+                  : 0);
         count_launch();
         err = cudaGetLastError();
     }
@@ -1171,9 +1174,23 @@ f3s_status launch_attention_sm100(const AttnArgs& a) {
         // last head by the tensor map); MMA1 reads only the first 64 bytes of each row
         return a.d == 128 ? launch<128, __nv_fp8_e4m3, 1>(a) : launch<64, __nv_fp8_e4m3, 1>(a);
     }
-    // head groups of 4 when every row window fits one 32-column block (d = 64): the per-chunk
-    // pipeline cost is shared by 4 heads (batched small graphs)
-    const bool hg4 = !a.one_head && a.d == 64 && a.heads % 4 == 0 && p.max_width <= 32 && p.n_groups == 0;
+    // head groups of 4 for row windows of at most 32 columns (d = 64): the per-chunk pipeline cost
+    // is shared by 4 heads (batched small graphs).  In LPT order those windows form the tail of the
+    // work list, so a plan with both kinds runs the wide head (and every split piece) one head per
+    // chunk, then the narrow tail with head groups: two launches, the same per-head arithmetic
+    // (reading c22)
+    const bool hg_ok = !a.one_head && a.d == 64 && a.heads % 4 == 0 && p.nnz > 0 && p.n_cols > 0;
+    if (hg_ok && a.lpt && a.sub_end < 0 && p.n_wide_sub > 0 && p.n_wide_sub < p.n_sub) {
+        AttnArgs wide = a, narrow = a;
+        wide.sub_begin = 0;
+        wide.sub_end = p.n_wide_sub;
+        narrow.sub_begin = p.n_wide_sub;
+        narrow.sub_end = p.n_sub;
+        f3s_status st = a.dtype == F3S_FP16 ? launch<64, __half, 1>(wide) : launch<64, __nv_bfloat16, 1>(wide);
+        if (st != F3S_OK) return st;
+        return a.dtype == F3S_FP16 ? launch<64, __half, 4>(narrow) : launch<64, __nv_bfloat16, 4>(narrow);
+    }
+    const bool hg4 = hg_ok && p.max_width <= 32 && p.n_groups == 0;
     if (a.dtype == F3S_FP16) {
         if (hg4) return launch<64, __half, 4>(a);
         return a.d == 64 ? launch<64, __half, 1>(a) : launch<128, __half, 1>(a);

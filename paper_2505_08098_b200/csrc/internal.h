@@ -44,6 +44,9 @@ struct Plan {
     // work queue hands these out one item per claim (lighter items in batches of 8), so that a
     // run of the heaviest windows is not claimed by one CTA
     int32_t n_heavy_sub = 0;
+    // meta_sub entries of windows wider than 32 columns (and every split piece) come first in LPT
+    // order; the rest (<= 32 columns) can run 4 heads per chunk (head groups, d = 64)
+    int32_t n_wide_sub = 0;
     int64_t total_chunks = 0;     // sum over windows of max(1, ceil(w / 128)): one head's kernel chunks
     int4* meta_sub = nullptr;     // [n_sub]
     int4* ginfo = nullptr;        // [n_groups]
@@ -130,6 +133,7 @@ struct AttnArgs {
     int64_t q_ld = 0;           // elements between consecutive Q rows; 0 = heads * d
     float* ml_out = nullptr;    // partial mode: [n_rows, heads] (m, l) pairs; O left unnormalised
     int32_t max_ctas = 0;       // > 0: at most this many CTAs (SMs left for a concurrent collective)
+    int32_t sub_begin = 0, sub_end = -1;  // LPT order: this launch's range of meta_sub entries (-1: to the end)
 };
 
 f3s_status launch_attention_sm100(const AttnArgs& a);

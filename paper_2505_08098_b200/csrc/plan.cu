@@ -382,6 +382,9 @@ f3s_status build_split(Plan* p, int32_t chunks) {
     p->n_groups = groups;
     p->n_pieces = pieces;
     p->n_heavy_sub = heavy_prefix;
+    int32_t wide = 0;
+    while (wide < (int32_t)meta.size() && meta[wide].z > 32) ++wide;
+    p->n_wide_sub = wide;
     p->n_heavy_lpt = heavy_lpt;
     return F3S_OK;
 }

@@ -55,3 +55,25 @@ def test_head_groups_empty_rows_and_ragged(f3s, oracle_mod):
     empty = np.diff(csr.row_ptr) == 0
     assert empty.any() and np.all(O[empty] == 0)
     assert np.array_equal(O, _run(f3s, p, Qb, Kb, Vb, "fp16", 0.125, "one_head"))
+
+
+@pytest.mark.parametrize("H", [4, 8])
+def test_head_groups_per_window(f3s, oracle_mod, H):
+    """A plan with both wide windows (> 32 columns, one head per chunk) and narrow ones (head
+    groups): the default call runs them in two launches and is bitwise equal to the one-head
+    kernel over the whole plan (reading c22), and within the tolerances of the oracle."""
+    import torch
+    mol = fi.molecules(300, 25, 150, seed=H)
+    n_mol = mol.n_rows
+    wide = fi.random_csr(64, n_mol, 40, 120, seed=H)  # 4 windows of many distinct columns
+    rp = np.concatenate([mol.row_ptr, mol.row_ptr[-1] + wide.row_ptr[1:]]).astype(np.int32)
+    ci = np.concatenate([mol.col_idx, wide.col_idx]).astype(np.int32)
+    n = n_mol + 64
+    csr = fi.CSR(n, n, rp, ci)
+    Qb, Kb, Vb = make_qkv(n, n, H, 64, "fp16", seed=3)
+    p = f3s.plan(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(), n)
+    assert p.info()["max_width"] > 32
+    O = _run(f3s, p, Qb, Kb, Vb, "fp16", 0.125, "default")
+    ref = oracle_mod.attention(rp, ci, Qb, Kb, Vb, scale=0.125)
+    assert_close(O, ref)
+    assert np.array_equal(O, _run(f3s, p, Qb, Kb, Vb, "fp16", 0.125, "one_head"))
