@@ -67,38 +67,24 @@ struct Cfg {
     // warpgroups stay busy on long items; the correction group merges the chunk partials
     static constexpr int kSoftmaxWGs = 2;
     // S/P/O buffers in flight (TMEM and SMEM); buffer b belongs to warpgroup b % kSoftmaxWGs
-#ifndef F3S_KSB
-#define F3S_KSB 4
-#endif
-    static constexpr int kSB = HG == 4 ? 4 : F3S_KSB;
+    static constexpr int kSB = 4;
     static_assert(kSB % kSoftmaxWGs == 0, "S/P/O buffers are owned by one warpgroup each");
     static constexpr int kMaxRowsBytes = (kMaxRows / 8) * kGroupBytes;  // one gathered tile (K or V) of a chunk
     // chunk slots (ids, masks, header, barriers): the index warp fills them ahead of the loaders
     static constexpr int kNS = kMaxRowsBytes >= 32 * 1024 ? 18 : 16;
     // Q tile slots (items in flight per CTA); fp8 tiles are half as large and carry half the bytes
     // per chunk, so more items are kept in flight
-#ifndef F3S_NQ
-#define F3S_NQ 0
-#endif
-    static constexpr int kNQ = HG == 4 ? 6 : EB == 1 ? 8 : F3S_NQ > 0 ? F3S_NQ : 4;
+    static constexpr int kNQ = HG == 4 ? 6 : EB == 1 ? 8 : 4;
     static constexpr int kQBytes = 16 * kRowPitch * HG;  // HG head tiles of 16 x D
     static constexpr int kPBytes = 16 * kMaxRows * EB;
     // O staging tiles (16 x HG*D fp32) for the TMA store (head groups: one per correction group)
     static constexpr int kNO = 2;
     static constexpr int kOBytes = 16 * D * 4 * HG;
-    // Row sums l_c of the chunk's P (Alg.1 l.17) from the tensor core: MMA2 also multiplies a tile of
-    // ones by P^T, so l_c sums exactly the rounded P that multiplies V (16-bit inputs, one head per
-    // chunk); the softmax then needs no row-sum reduction.  fp8 and head groups sum in registers.
-#ifndef F3S_LSUM_MMA
-#define F3S_LSUM_MMA 0
-#endif
-#ifndef F3S_MAX_REDUX
-#define F3S_MAX_REDUX 1
-#endif
-    static constexpr bool kLsumMMA = F3S_LSUM_MMA && EB == 2 && HG == 1;
-    // TMEM: S^T, O^T (kSB x HG buffers of 16 columns each), then the l_c buffers (kSB x 16)
-    static constexpr int kTmemO = 16 * kSB * HG, kTmemL = 2 * 16 * kSB * HG;
-    static constexpr int kTmemUsed = kTmemL + (kLsumMMA ? 16 * kSB : 0);
+    // (Row sums l_c from the tensor core -- a ones tile times P^T in MMA2 -- were measured slower,
+    // MMA2 being on the critical path; round 2, profiles/r02_ab_softmax_modes.txt.)
+    // TMEM: S^T, then O^T (kSB x HG buffers of 16 columns each)
+    static constexpr int kTmemO = 16 * kSB * HG;
+    static constexpr int kTmemUsed = 2 * 16 * kSB * HG;
     static constexpr int kTmemCols = kTmemUsed <= 128 ? 128 : kTmemUsed <= 256 ? 256 : 512;
     static_assert(kTmemUsed <= 512, "TMEM columns");
     static constexpr int kSlotBytes = 32 + 128 * 4 + 128 * 2;  // sizeof(Slot)
@@ -106,7 +92,7 @@ struct Cfg {
     static constexpr int kNumBars = 4 * kNS + 2 * kNQ + 5 * kSB + 2 * 16;
     // everything but the gathered tiles
     static constexpr int kFixedBytes = kNQ * kQBytes + kSB * kPBytes + kNO * kOBytes + kNS * kSlotBytes +
-                                       kSB * 4 * 16 * 4 + kSB * kCorrBytes + kNumBars * 8 + 16 + (kLsumMMA ? 2048 : 0);
+                                       kSB * 4 * 16 * 4 + kSB * kCorrBytes + kNumBars * 8 + 16;
     // Gathered tiles: fixed-size slots of one full chunk (128 rows) each, chunk n in K tile n % kNK
     // (free again once MMA1 completed) and V tile n % kNV (free once MMA2 completed).  V tiles wait
     // for the softmax and MMA2, so they take all the shared memory that is left.
@@ -125,17 +111,13 @@ struct Cfg {
     static constexpr int oCorr = oRed + kSB * 4 * 16 * 4;  // CorrSlot [kSB]
     static constexpr int oBar = oCorr + kSB * kCorrBytes;
     static constexpr int oTmem = oBar + kNumBars * 8;
-    static constexpr int oOnes = (oTmem + 16 + 1023) / 1024 * 1024;  // one 128B-swizzle atom of ones (A of the l_c MMA)
-    static constexpr int kSmemBytes = kLsumMMA ? oOnes + 1024 : oTmem + 16;
+    static constexpr int kSmemBytes = oTmem + 16;
     static constexpr int kCtasPerSm = 1;
     // warp roles: 0 index (work queue, chunk slots, Q tiles), 1 MMA1, 2 MMA2 (each sleeping on its
     // own barriers: try_wait wakes ~60 cycles after the arrive), kLoaderWarps cp.async gather warps,
     // two softmax warpgroups, the correction warpgroup
-#ifndef F3S_NLOAD
-#define F3S_NLOAD 0
-#endif
     // gather warps: the cp.async issue rate bounds the pipeline (measured: 5-8 warps, profiles/r02_ab_*)
-    static constexpr int kLoaderWarps = F3S_NLOAD > 0 ? F3S_NLOAD : RB >= 256 ? 8 : 7;
+    static constexpr int kLoaderWarps = RB >= 256 ? 8 : 7;
     static constexpr int kMma2Warp = 2;
     static constexpr int kLoader0 = 3, kSoftmax0 = kLoader0 + kLoaderWarps, kCorr0 = kSoftmax0 + 4 * kSoftmaxWGs;
     // correction warpgroups: head-group items are single chunks with no running state, so two
@@ -293,11 +275,6 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     // only ever holds gathered input rows.
     for (int i = threadIdx.x; i < C::kTileBytes / 16; i += blockDim.x)
         reinterpret_cast<int4*>(smem + C::oK)[i] = make_int4(0, 0, 0, 0);
-    if constexpr (C::kLsumMMA) {  // 1.0 in the input format, 1024 bytes
-        const uint32_t one2 = std::is_same<T, __nv_bfloat16>::value ? 0x3F803F80u : 0x3C003C00u;
-        for (int i = threadIdx.x; i < 64; i += blockDim.x)
-            reinterpret_cast<uint4*>(smem + C::oOnes)[i] = make_uint4(one2, one2, one2, one2);
-    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::kNS; ++s) {
             mbar_init(bar(B::idxfull(s)), 1);
@@ -366,7 +343,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const int qs = qseq % C::kNQ;
                 const int qph = (qseq / C::kNQ) & 1;
                 if (lane == 0) {  // Alg.1 l.5: Q_i of the item (the slot's previous item has left MMA1)
-                    mbar_wait_lazy(bar(B::qempty(qs)), qph ^ 1);
+                    mbar_wait(bar(B::qempty(qs)), qph ^ 1);
                     mbar_arrive_expect_tx(bar(B::qfull(qs)), C::kQBytes);
 #pragma unroll
                     for (int g = 0; g < HG; ++g)
@@ -379,7 +356,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     const int rows = w > 0 ? min(chunk_rows, w - chunk_rows * j) : 0;
                     const int s = seq % C::kNS;
                     if (lane == 0) {
-                        mbar_wait_lazy(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+                        mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
                         lap(0);
                         Slot& sl = slots[s];
                         sl.rw = k;
@@ -409,7 +386,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             // producer, loaders and MMA warps stop at the first.  rows = -1 - w.
             for (int w = 0; w < C::kSoftmaxWGs; ++w, ++seq) {
                 const int s = seq % C::kNS;
-                mbar_wait_lazy(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+                mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
                 slots[s].rows = -1 - w;
                 mbar_arrive(bar(B::idxfull(s)));
             }
@@ -523,10 +500,6 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             // 16-bit P, K-major [16 x 128 bytes] with the 128-byte swizzle for fp8 P (8-bit
             // MN-major B would need 16-byte rows)
             constexpr uint32_t idesc2 = idesc_f16(fmt, 1, EB == 2 ? 1 : 0, D, 16);
-            // l_c = ones[64 x C] . P^T: every row of the M = 64 result is the row sum of P (each TMEM
-            // lane quadrant holds a copy); the ones operand is one atom read again for every K group
-            constexpr uint32_t idescL = idesc_f16(fmt, 1, 1, 64, 16);
-            const uint64_t dOnes = smem_desc_sw128(sb + C::oOnes, 1024, 0);
             const uint64_t dV = smem_desc_sw128(0, 1024, C::kGroupBytes);
             const uint64_t dP = EB == 2 ? smem_desc_sw32(0, 4096, 256) : smem_desc_sw128(0, 16, 1024);
             for (int32_t n2 = 0;; ++n2) {
@@ -554,10 +527,6 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                                 mma_f16_ss_warp(tmem + C::kTmemO + (b * HG + g) * 16,
                                                 a0 + ((g * 4 * C::kGroupBytes + st * 2 * C::kGroupBytes) >> 4),
                                                 b0 + ((g * 1024 + st * 512) >> 4), idesc2, st > 0 ? 1u : 0u);
-                        if constexpr (C::kLsumMMA)
-                            for (int st = 0; st < nsteps; ++st)
-                                mma_f16_ss_warp(tmem + C::kTmemL + b * 16, dOnes, b0 + ((st * 512) >> 4), idescL,
-                                                st > 0 ? 1u : 0u);
                     }
                 }
                 mma_commit_warp(bar(B::ofull(b)));
@@ -622,7 +591,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             float cm[16];
             float mrow = kMFloor;  // HG = 1, lanes 0..15: the chunk max of row `lane` (reading c5 floor)
             float rm_hg = kMFloor;  // HG = 4, lane 2i: row i's max of the warp's head
-            if constexpr (HG == 1 && F3S_MAX_REDUX) {
+            if constexpr (HG == 1) {
                 // the warp's 32 columns: one redux.sync.max per row (uniform datapath), then the
                 // 4-warp combine through shared memory; lane i < 16 finishes row i and broadcasts
                 float mine = -INFINITY;
@@ -640,21 +609,6 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) cm[i] = __shfl_sync(0xffffffffu, mrow, i);
-            } else if constexpr (HG == 1) {
-                // warp butterfly (lane 2i ends with row i's max over the warp), 4-warp combine
-                const float rm = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
-                if (!(lane & 1)) red[(((lane >> 1) & 15) + b * 16) * 4 + q] = rm;
-                if (p == 0) lap(2);
-                named_bar_sync(1 + wg, 128);
-                const float4* r4 = reinterpret_cast<const float4*>(red) + b * 16;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float4 r = r4[i];
-                    cm[i] = fmaxf(fmaxf(fmaxf(r.x, r.y), fmaxf(r.z, r.w)), kMFloor);
-                }
-                if (lane < 16) mrow = cm[0];
-#pragma unroll
-                for (int i = 1; i < 16; ++i) mrow = lane == i ? cm[i] : mrow;
             } else {  // the warp holds all columns of its head: lane 2i has row i's max
                 rm_hg = (expt & 32) ? 0.f : rowreduce16(x, lane, OpMax());
 #pragma unroll
@@ -676,15 +630,11 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 pv[i] = (expt & 1) ? x[i] : pexp(x[i] - cm[i]);   // E = e^{S - m_c} (l.17); 0 where masked
             }
             // this warp's part of the row sums (l.18) of the P that MMA2 multiplies: the rounded
-            // 16-bit P (reading c7), or fp8's unrounded E (reading c24); one-head 16-bit chunks get
-            // l_c from the tensor core instead (kLsumMMA)
-            float rl = 0.f;
-            if constexpr (!C::kLsumMMA) {
-                float pr[16];
+            // 16-bit P (reading c7), or fp8's unrounded E (reading c24)
+            float pr[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) pr[i] = EB == 1 ? pv[i] : round_to<T>(pv[i]);
-                rl = rowreduce16(pr, lane, OpAdd());
-            }
+            for (int i = 0; i < 16; ++i) pr[i] = EB == 1 ? pv[i] : round_to<T>(pv[i]);
+            const float rl = rowreduce16(pr, lane, OpAdd());
             if (p == 0) lap(6);
             // P_b / corr_b are free once the correction group consumed chunk seq - kSB
             mbar_wait(bar(B::pempty(b)), bph ^ 1);
@@ -710,7 +660,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 prow[sw] = lo;
                 prow[sw ^ 1] = hi;
             }
-            if (!C::kLsumMMA && !(lane & 1)) corr[b].lpart[q][(lane >> 1) & 15] = rl;
+            if (!(lane & 1)) corr[b].lpart[q][(lane >> 1) & 15] = rl;
             if (HG == 1 && q == 0 && lane < 16) corr[b].m[lane] = mrow;
             if constexpr (HG > 1 && kPart)
                 if (!(lane & 1)) corr[b].mh[q][lane >> 1] = fmaxf(kMFloor, rm_hg);
@@ -820,22 +770,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             // merge factors of row ri: O = fa * O + fb * O_c
             const float mc = corr[b].m[ri];
-            float lc;
-            if constexpr (C::kLsumMMA) {
-                // l_c from the ones MMA: lanes 0..15 of the warp's quadrant hold l_c[0..15] in the
-                // buffer's 16 columns; lane ri takes column ri (lanes 16..31 copy lanes 0..15)
-                lc = 0.f;
-                if (rows > 0) {
-                    float lv[16];
-                    tmem_ld_32x32b_x16(tmem + tl + C::kTmemL + b * 16, lv);
-                    lc = lv[0];
-#pragma unroll
-                    for (int i = 1; i < 16; ++i) lc = ri == i ? lv[i] : lc;
-                    lc = __shfl_sync(0xffffffffu, lc, ri);
-                }
-            } else {
-                lc = (corr[b].lpart[0][ri] + corr[b].lpart[1][ri]) + (corr[b].lpart[2][ri] + corr[b].lpart[3][ri]);
-            }
+            const float lc = (corr[b].lpart[0][ri] + corr[b].lpart[1][ri]) + (corr[b].lpart[2][ri] + corr[b].lpart[3][ri]);
             float fa, fb;
             if (flags & 1) {  // the item's first chunk: (m, l) = (m_c, l_c)
                 m_run = mc;

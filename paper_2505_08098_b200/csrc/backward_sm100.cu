@@ -81,7 +81,7 @@ struct BCfg {
     static constexpr int kTmS = 0, kTmP = 16 * kSB, kTmG = 32 * kSB;
     static constexpr int kTmemCols = 256;
     static_assert(kTmG + 2 * kNG * 16 <= kTmemCols, "TMEM columns");
-    static constexpr int kLoaderWarps = 6;
+    static constexpr int kLoaderWarps = D == 128 ? 8 : 6;
     static constexpr int kLoader0 = 3, kEw0 = kLoader0 + kLoaderWarps, kEpi0 = kEw0 + 8;
     static constexpr int kThreads = 32 * (kEpi0 + 4);
     static constexpr int kBatch = 8;
@@ -222,7 +222,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                 const int qs = qseq % C::kNQ;
                 const int qph = (qseq / C::kNQ) & 1;
                 if (lane == 0) {  // the item's 16-row tiles X and Y (rows: Q_w, dO_w; cols: K_w, V_w)
-                    mbar_wait_lazy(bar(B::xyempty(qs)), qph ^ 1);
+                    mbar_wait(bar(B::xyempty(qs)), qph ^ 1);
                     mbar_arrive_expect_tx(bar(B::xyfull(qs)), C::kQBytes);
                     const uint32_t xd = sb + C::oQ + qs * C::kQBytes;
 #pragma unroll
@@ -235,7 +235,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                     const int rows = w > 0 ? min(chunk_rows, w - chunk_rows * j) : 0;
                     const int s = seq % C::kNS;
                     if (lane == 0) {
-                        mbar_wait_lazy(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+                        mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
                         Slot& sl = slots[s];
                         sl.rw = k;
                         sl.head = h;
@@ -263,7 +263,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         if (lane == 0) {
             for (int w = 0; w < 2; ++w, ++seq) {  // one stop marker per elementwise warpgroup
                 const int s = seq % C::kNS;
-                mbar_wait_lazy(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
+                mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
                 slots[s].rows = -1 - w;
                 mbar_arrive(bar(B::idxfull(s)));
             }
@@ -357,6 +357,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                 }
             }
             mma_commit_warp(bar(B::sfull(b)));
+            if (PASS == 0) mma_commit_warp(bar(B::t2free(n1 % C::kN2)));  // rows: V_c is MMA1's alone
             if (flags & 2) mma_commit_warp(bar(B::xyempty(qslot)));
         }
         __syncwarp();
@@ -372,7 +373,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         for (int32_t n2 = 0;; ++n2) {
             const int s = n2 % C::kNS, b = n2 % C::kSB, a = item & 1;
             mbar_wait(bar(B::a1full(s)), (n2 / C::kNS) & 1);
-            mbar_wait(bar(B::a2full(s)), (n2 / C::kNS) & 1);
+            if (PASS == 1) mbar_wait(bar(B::a2full(s)), (n2 / C::kNS) & 1);
             const Slot& sl = slots[s];
             const int rows = sl.rows, flags = sl.flags, rw = sl.rw, hd = sl.head;
             if (rows < 0) {  // tell the epilogue to stop (its next record)
@@ -410,7 +411,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             }
             mma_commit_warp(bar(B::pempty(b)));
             mma_commit_warp(bar(B::t1free(n2 % C::kN1)));
-            mma_commit_warp(bar(B::t2free(n2 % C::kN2)));
+            if (PASS == 1) mma_commit_warp(bar(B::t2free(n2 % C::kN2)));
             mma_commit_warp(bar(B::empty(s)));
             if (flags & 2) {
                 if (lane == 0) rec[a] = make_int4(rw, hd, any ? 1 : 0, 0);

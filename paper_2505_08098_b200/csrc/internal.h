@@ -44,8 +44,9 @@ struct Plan {
     // work queue hands these out one item per claim (lighter items in batches of 8), so that a
     // run of the heaviest windows is not claimed by one CTA
     int32_t n_heavy_sub = 0;
-    // meta_sub entries of windows wider than 32 columns (and every split piece) come first in LPT
-    // order; the rest (<= 32 columns) can run 4 heads per chunk (head groups, d = 64)
+    // meta_sub entries up to the last window wider than 32 columns or split piece; the entries
+    // after it (unsplit windows of <= 32 columns, the LPT tail) can run 4 heads per chunk (head
+    // groups, d = 64)
     int32_t n_wide_sub = 0;
     int64_t total_chunks = 0;     // sum over windows of max(1, ceil(w / 128)): one head's kernel chunks
     int4* meta_sub = nullptr;     // [n_sub]

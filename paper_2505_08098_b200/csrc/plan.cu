@@ -382,8 +382,11 @@ f3s_status build_split(Plan* p, int32_t chunks) {
     p->n_groups = groups;
     p->n_pieces = pieces;
     p->n_heavy_sub = heavy_prefix;
+    // entries up to the last wide window or split piece (a split window's last piece can be narrow):
+    // everything after it is an unsplit window of <= 32 columns
     int32_t wide = 0;
-    while (wide < (int32_t)meta.size() && meta[wide].z > 32) ++wide;
+    for (int32_t i = 0; i < (int32_t)meta.size(); ++i)
+        if (meta[i].z > 32 || meta[i].w != 0) wide = i + 1;
     p->n_wide_sub = wide;
     p->n_heavy_lpt = heavy_lpt;
     return F3S_OK;

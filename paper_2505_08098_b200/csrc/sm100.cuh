@@ -42,56 +42,14 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 // Blocking wait with a watchdog: a pipeline bug traps (launch failure) instead of hanging the GPU.
 // try_wait suspends the thread in hardware for a short system time limit; the global-timer read
-// between retries doubles as a back-off.  (Measured: both a tighter spin and a long suspend hint
-// were slower — issue-slot pressure / wake-up latency on the pipeline's critical path.)
-// try_wait with a suspend-time hint (ns): the thread sleeps until the phase completes or the hint
-// expires, instead of returning at once (no issue slots burnt while waiting)
-__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity), "r"(ns)
-        : "memory");
-    return ok != 0;
-}
-#ifndef F3S_WAIT_MODE
-#define F3S_WAIT_MODE 0
-#endif
-#ifndef F3S_NAP_NS
-#define F3S_NAP_NS 200
-#endif
-#ifndef F3S_WAIT_HINT
-#define F3S_WAIT_HINT 0x989680
-#endif
+// between retries doubles as a back-off.  (Measured in round 2, profiles/r02_ab_wait_modes.txt:
+// suspend-time hints and nanosleep back-off of the off-path waiters were all within +-2 %.)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-#if F3S_WAIT_MODE & 1
-    if (mbar_try_wait_hint(bar, parity, F3S_WAIT_HINT)) return;
-    const uint64_t t0 = globaltimer_ns();
-    while (!mbar_try_wait_hint(bar, parity, F3S_WAIT_HINT)) {
-        if (globaltimer_ns() - t0 > 20000000000ull) __trap();
-    }
-#else
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = globaltimer_ns();
     while (!mbar_try_wait(bar, parity)) {
         if (globaltimer_ns() - t0 > 20000000000ull) __trap();
     }
-#endif
-}
-// wait of a role that runs ahead of the pipeline (off the critical path): back off with nanosleep
-// between polls so that its spinning does not take issue slots from the working warps
-__device__ __forceinline__ void mbar_wait_lazy(uint32_t bar, uint32_t parity) {
-#if F3S_WAIT_MODE & 2
-    if (mbar_try_wait(bar, parity)) return;
-    const uint64_t t0 = globaltimer_ns();
-    while (!mbar_try_wait(bar, parity)) {
-        __nanosleep(F3S_NAP_NS);
-        if (globaltimer_ns() - t0 > 20000000000ull) __trap();
-    }
-#else
-    mbar_wait(bar, parity);
-#endif
 }
 
 // ---- named barriers ----------------------------------------------------------------------------

@@ -77,3 +77,24 @@ def test_head_groups_per_window(f3s, oracle_mod, H):
     ref = oracle_mod.attention(rp, ci, Qb, Kb, Vb, scale=0.125)
     assert_close(O, ref)
     assert np.array_equal(O, _run(f3s, p, Qb, Kb, Vb, "fp16", 0.125, "one_head"))
+
+
+def test_head_groups_per_window_with_split(f3s, oracle_mod):
+    """Per-window head groups on a plan with split windows whose last pieces are narrow: the
+    narrow-tail launch must start after the last piece (every output row written, oracle parity,
+    bitwise equal to the one-head kernel)."""
+    import torch
+    mol = fi.molecules(200, 25, 150, seed=2)
+    n_mol = mol.n_rows
+    wide = fi.random_csr(64, n_mol, 300, 600, seed=2)  # windows of ~4-6 chunks
+    rp = np.concatenate([mol.row_ptr, mol.row_ptr[-1] + wide.row_ptr[1:]]).astype(np.int32)
+    ci = np.concatenate([mol.col_idx, wide.col_idx]).astype(np.int32)
+    n = n_mol + 64
+    Qb, Kb, Vb = make_qkv(n, n, 4, 64, "fp16", seed=4)
+    p = f3s.plan(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(), n)
+    p.set_split(1)  # every wide window in 128-column pieces; the last piece of most is < 32 columns
+    assert p.info()["split_groups"] > 0
+    O = _run(f3s, p, Qb, Kb, Vb, "fp16", 0.125, "default")
+    assert np.all(np.isfinite(O))
+    assert_close(O, oracle_mod.attention(rp, ci, Qb, Kb, Vb, scale=0.125))
+    assert np.array_equal(O, _run(f3s, p, Qb, Kb, Vb, "fp16", 0.125, "one_head"))
