@@ -64,9 +64,12 @@ struct BCfg {
     static constexpr int kNumBars = 5 * kNS + 2 * kNQ + 4 * kSB + 4 + 2 * 16;
     static constexpr int kFixed = kNQ * kQBytes + kSB * kNT * kPBytes + kNG * kOBytes + kNS * kSlotBytes +
                                   kNumBars * 8 + 64 + 16;
-    static constexpr int kN1 = (227 * 1024 - kFixed) / kTile / 2;  // A1 / A2 tile slots
-    static constexpr int kN2 = kN1;
-    static_assert(kN1 >= 2, "two tile slots per operand at least");
+    // gathered tile slots: both operands live until MMA2 in the column pass; in the row pass V_c is
+    // free after MMA1, so K_c (read by MMA1 and MMA2) gets the remaining slots
+    static constexpr int kSlotsAll = (227 * 1024 - kFixed) / kTile;
+    static constexpr int kN2 = PASS == 0 ? 2 : kSlotsAll / 2;
+    static constexpr int kN1 = PASS == 0 ? (kSlotsAll - 2 < 16 ? kSlotsAll - 2 : 16) : kSlotsAll / 2;
+    static_assert(kN1 >= 2 && kN2 >= 2 && kN1 <= 16 && kN2 <= 16, "tile slots per operand");
     static constexpr int oT1 = 0, oT2 = kN1 * kTile;
     static constexpr int oQ = (kN1 + kN2) * kTile;
     static constexpr int oP = oQ + kNQ * kQBytes;
