@@ -23,3 +23,23 @@ for (n, H, d, seed) in [(150, 2, 128, 4), (120, 3, 64, 5)]:
     O = f3s.attention(p, Q, K, V, scale=0.125)
     torch.cuda.synchronize()
     print("ok e4m3", n, H, d, float(O.abs().sum()))
+# round 2: split pieces, per-window head groups (wide head + narrow tail), partial mode with head
+# groups, tensor-core and CUDA-core backward, bf16
+mol = fi.molecules(8, 25, 60, seed=7)
+wide = fi.random_csr(32, mol.n_rows, 60, 200, seed=7)
+rp_h = np.concatenate([mol.row_ptr, mol.row_ptr[-1] + wide.row_ptr[1:]]).astype(np.int32)
+ci_h = np.concatenate([mol.col_idx, wide.col_idx]).astype(np.int32)
+n = mol.n_rows + 32
+p = f3s.plan(torch.from_numpy(rp_h).cuda(), torch.from_numpy(ci_h).cuda(), n)
+p.set_split(1)
+for dt in (torch.float16, torch.bfloat16):
+    Q = torch.randn(n, 4, 64, device="cuda").to(dt); K = torch.randn_like(Q); V = torch.randn_like(Q)
+    O = f3s.attention(p, Q, K, V, scale=0.125)
+    Op = torch.empty(Q.shape, device="cuda"); ml = torch.empty((n, 4, 2), device="cuda")
+    f3s.attention_partial_raw(p, Q.data_ptr(), K.data_ptr(), V.data_ptr(), 0, Op.data_ptr(), ml.data_ptr(), 0.125, 4, 64,
+                              f3s.FP16 if dt == torch.float16 else f3s.BF16, 0, torch.cuda.current_stream().cuda_stream)
+    dO = torch.randn(Q.shape, device="cuda")
+    f3s.attention_backward(p, Q, K, V, dO, scale=0.125, variant="tc")
+    f3s.attention_backward(p, Q, K, V, dO, scale=0.125, variant="simt")
+    torch.cuda.synchronize()
+    print("ok mixed/split/partial/backward", dt, float(O.abs().sum()))
