@@ -97,6 +97,60 @@ k_bench(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensor
     }
     // loaders: warp w handles row ops w, w + NL, ... (4 rows per op: 8 lanes x 16 B per row)
     const int piece = lane & 7, rsub = lane >> 3;
+    if (MODE == 7) {
+        // LDG + STS, software-pipelined 3 chunks deep: the loads of chunk i + 3 are issued as soon
+        // as chunk i's registers are stored
+        constexpr int kOps = (kRows / 4 + NL - 1) / NL;
+        uint4 kA[kOps], vA[kOps], kB[kOps], vB[kOps], kC[kOps], vC[kOps];
+        auto issue = [&](int64_t j, uint4 (&kk)[kOps], uint4 (&vv)[kOps]) {
+            if (j >= mine) return;
+            const int s = (int)(j % kIdx);
+            mbar_wait(idxf(s), (j / kIdx) & 1);
+            const int h = (int)(chunk_of(j) % H);
+#pragma unroll
+            for (int q = 0; q < kOps; ++q) {
+                const int op = warp + q * NL;
+                if (op < kRows / 4) {
+                    const int64_t jj = ids[s][op * 4 + rsub];
+                    kk[q] = __ldg(reinterpret_cast<const uint4*>(K + jj * ldb + h * 128 + piece * 16));
+                    vv[q] = __ldg(reinterpret_cast<const uint4*>(V + jj * ldb + h * 128 + piece * 16));
+                }
+            }
+        };
+        auto store = [&](int64_t j, uint4 (&kk)[kOps], uint4 (&vv)[kOps]) {
+            if (j >= mine) return;
+            const int t = (int)(j % ntiles);
+            if (j >= ntiles) mbar_wait(empty(t), ((j / ntiles) & 1) ^ 1);
+            const uint32_t kt = (uint32_t)__cvta_generic_to_shared(smem + (size_t)t * kTile);
+            const uint32_t vt = kt + kRows * 128;
+#pragma unroll
+            for (int q = 0; q < kOps; ++q) {
+                const int op = warp + q * NL;
+                if (op < kRows / 4) {
+                    const int r = op * 4 + rsub;
+                    const uint32_t o = (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128 + (uint32_t)((piece ^ (r & 7)) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(kt + o), "r"(kk[q].x), "r"(kk[q].y),
+                                 "r"(kk[q].z), "r"(kk[q].w) : "memory");
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(vt + o), "r"(vv[q].x), "r"(vv[q].y),
+                                 "r"(vv[q].z), "r"(vv[q].w) : "memory");
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(full(t));
+        };
+        issue(0, kA, vA);
+        issue(1, kB, vB);
+        issue(2, kC, vC);
+        for (int64_t i = 0; i < mine; i += 3) {
+            store(i, kA, vA);
+            issue(i + 3, kA, vA);
+            store(i + 1, kB, vB);
+            issue(i + 4, kB, vB);
+            store(i + 2, kC, vC);
+            issue(i + 5, kC, vC);
+        }
+        return;
+    }
     uint32_t acc = 0;
     for (int64_t i = 0; i < mine; ++i) {
         const int t = (int)(i % ntiles);
@@ -130,6 +184,48 @@ k_bench(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensor
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(vt + o), "l"(V + j * ldb + h * 128 + piece * 16) : "memory");
                 }
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(t)) : "memory");
+            }
+        } else if (MODE >= 5) {
+            // hybrid: warps [0, NC) cp.async rows [0, RS), warps [NC, NL) LDG + STS rows [RS, 128)
+            constexpr int NC = MODE == 5 ? NL * 3 / 4 : NL / 2;
+            constexpr int RS = (kRows * NC / NL) / 4 * 4;
+            if (warp < NC) {
+                for (int op = warp; op < RS / 4; op += NC) {
+                    const int r = op * 4 + rsub;
+                    const int64_t j = ids[s][r];
+                    const uint32_t o = (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128 + (uint32_t)((piece ^ (r & 7)) << 4);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(kt + o), "l"(K + j * ldb + h * 128 + piece * 16) : "memory");
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(vt + o), "l"(V + j * ldb + h * 128 + piece * 16) : "memory");
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(t)) : "memory");
+            } else {
+                constexpr int NLD = NL - NC;
+                constexpr int kOps = ((kRows - RS) / 4 + NLD - 1) / NLD;
+                uint4 kv[kOps], vv[kOps];
+                uint32_t off[kOps];
+                bool okk[kOps];
+#pragma unroll
+                for (int q = 0; q < kOps; ++q) {
+                    const int op = RS / 4 + (warp - NC) + q * NLD;
+                    okk[q] = op < kRows / 4;
+                    const int r = okk[q] ? op * 4 + rsub : 0;
+                    const int64_t j = ids[s][r];
+                    off[q] = (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128 + (uint32_t)((piece ^ (r & 7)) << 4);
+                    if (okk[q]) {
+                        kv[q] = __ldg(reinterpret_cast<const uint4*>(K + j * ldb + h * 128 + piece * 16));
+                        vv[q] = __ldg(reinterpret_cast<const uint4*>(V + j * ldb + h * 128 + piece * 16));
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < kOps; ++q)
+                    if (okk[q]) {
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(kt + off[q]), "r"(kv[q].x), "r"(kv[q].y),
+                                     "r"(kv[q].z), "r"(kv[q].w) : "memory");
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(vt + off[q]), "r"(vv[q].x), "r"(vv[q].y),
+                                     "r"(vv[q].z), "r"(vv[q].w) : "memory");
+                    }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(full(t));
             }
         } else if (MODE == 4) {
             for (int op = warp; op < kRows / 4; op += NL) {
@@ -223,6 +319,13 @@ static float run(const int32_t* cols, int64_t n_chunks, int H, const void* K, co
 extern "C" float gather_bench2(int mode, int nl, const int32_t* cols, int64_t n_chunks, int H, const void* K,
                                const void* V, int ntiles, int pf, int reps, int64_t n_rows) {
     g_nrows = n_rows;
+    if (mode == 7 && nl == 16) return run<7, 16>(cols, n_chunks, H, K, V, ntiles, pf, reps);
+    if (mode == 7 && nl == 24) return run<7, 24>(cols, n_chunks, H, K, V, ntiles, pf, reps);
+    if (mode == 7 && nl == 8) return run<7, 8>(cols, n_chunks, H, K, V, ntiles, pf, reps);
+    if (mode == 5 && nl == 8) return run<5, 8>(cols, n_chunks, H, K, V, ntiles, pf, reps);
+    if (mode == 5 && nl == 12) return run<5, 12>(cols, n_chunks, H, K, V, ntiles, pf, reps);
+    if (mode == 6 && nl == 8) return run<6, 8>(cols, n_chunks, H, K, V, ntiles, pf, reps);
+    if (mode == 6 && nl == 12) return run<6, 12>(cols, n_chunks, H, K, V, ntiles, pf, reps);
     if (mode == 4 && nl == 4) return run<4, 4>(cols, n_chunks, H, K, V, ntiles, pf, reps);
     if (mode == 4 && nl == 8) return run<4, 8>(cols, n_chunks, H, K, V, ntiles, pf, reps);
     if (mode == 0 && nl == 12) return run<0, 12>(cols, n_chunks, H, K, V, ntiles, pf, reps);

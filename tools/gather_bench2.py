@@ -28,9 +28,9 @@ def main():
         n_chunks = W // 128 * H
         gb = n_chunks * 128 * 256 / 1e9
         print(f"{name}: {n_chunks} chunks of 128 rows x (K+V) 128 B, H={H}: {gb:.2f} GB", flush=True)
-        for mode, nl, ntiles, pf in [(0, 4, 6, 0), (0, 8, 6, 0), (0, 12, 6, 0), (0, 16, 6, 0), (4, 4, 6, 0), (4, 8, 6, 0)]:
+        for mode, nl, ntiles, pf in [(0, 8, 6, 0), (7, 8, 6, 0), (7, 16, 6, 0), (7, 24, 6, 0), (7, 24, 4, 0)]:
             ms = lib.gather_bench2(mode, nl, dcols.data_ptr(), n_chunks, H, K.data_ptr(), V.data_ptr(), ntiles, pf, 4, csr.n_cols)
-            print(f"  {['cp.async','ldg+sts','tma.g4','K:tma,V:cpa','cp.async.ca'][mode]:9s} loaders {nl:2d} tiles {ntiles} prefetch {pf:2d}: "
+            print(f"  {['cp.async','ldg+sts','tma.g4','K:tma,V:cpa','cp.async.ca','hyb 3/4','hyb 1/2','ldg pipe3'][mode]:9s} loaders {nl:2d} tiles {ntiles} prefetch {pf:2d}: "
                   f"{ms:8.3f} ms  {gb / ms * 1e3:6.0f} GB/s", flush=True)
 
 
