@@ -40,8 +40,12 @@ namespace {
 
 using namespace sm100;
 
-template <int D, int PASS>  // PASS 0: rows (dQ), 1: columns (dK, dV)
+// PASS 0: rows (dQ), 1: columns (dK, dV).  HG = 4 (head groups, d = 64, every window <= 32
+// columns, as in the forward): a chunk holds the window's columns for 4 heads (tile rows 32g.. =
+// head g), elementwise warp q works on head q, one epilogue tile covers the 4 heads.
+template <int D, int PASS, int HG = 1>
 struct BCfg {
+    static_assert(HG == 1 || (HG == 4 && D == 64), "head groups: d = 64 only");
     static constexpr int RB = D * 2;                 // bytes of one gathered row of one head
     static constexpr int P = RB / 128;               // 128-byte panels per row
     static constexpr int kRowPitch = 128 * P;
@@ -50,16 +54,16 @@ struct BCfg {
     static constexpr int kTile = (kMaxRows / 8) * kGroupBytes;
     // S/dP TMEM buffers and P/dS shared tiles, chunk slots, per-item tile slots (X and Y: 16 x D
     // each): fewer at d = 128 so that two 32 KB tile slots per gathered operand still fit
-    static constexpr int kSB = D == 128 ? 2 : 4;
+    static constexpr int kSB = (D == 128 || HG == 4) ? 2 : 4;
     static constexpr int kNS = D == 128 ? 12 : 16;
-    static constexpr int kNQ = D == 128 ? 2 : 4;
-    static constexpr int kXBytes = 16 * kRowPitch;
+    static constexpr int kNQ = (D == 128 || HG == 4) ? 2 : 4;
+    static constexpr int kXBytes = 16 * kRowPitch * HG;  // HG head tiles of 16 x D
     static constexpr int kQBytes = 2 * kXBytes;
     static constexpr int kNT = PASS == 0 ? 1 : 2;    // 16-bit tiles written per chunk: dS (rows); P, dS (cols)
     static constexpr int kPBytes = 16 * kMaxRows * 2;
     static constexpr int kNG = PASS == 0 ? 1 : 2;    // gradient accumulators: dQ; dV, dK
-    static constexpr int kOBytes = 16 * D * 4;       // one [16 x D] fp32 staging tile
-    static constexpr int kScal = PASS == 0 ? 16 : 128;  // LSE / D values per chunk slot
+    static constexpr int kOBytes = 16 * D * 4 * HG;  // one [16 x HG*D] fp32 staging tile
+    static constexpr int kScal = PASS == 0 ? 16 * HG : 128;  // LSE / D values per chunk slot
     static constexpr int kSlotBytes = 32 + kMaxRows * 4 + kMaxRows * 2 + 2 * kScal * 4;
     static constexpr int kNumBars = 5 * kNS + 2 * kNQ + 4 * kSB + 4 + 2 * 16;
     static constexpr int kFixed = kNQ * kQBytes + kSB * kNT * kPBytes + kNG * kOBytes + kNS * kSlotBytes +
@@ -80,18 +84,19 @@ struct BCfg {
     static constexpr int oTmem = oBar + kNumBars * 8;
     static constexpr int kSmemBytes = oTmem + 16;
     static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
-    // TMEM: S (kSB x 16), dP (kSB x 16), gradient accumulators (2 item buffers x kNG x 16)
-    static constexpr int kTmS = 0, kTmP = 16 * kSB, kTmG = 32 * kSB;
-    static constexpr int kTmemCols = 256;
-    static_assert(kTmG + 2 * kNG * 16 <= kTmemCols, "TMEM columns");
+    // TMEM: S (kSB x HG x 16), dP (kSB x HG x 16), gradient accumulators (2 item buffers x HG x kNG x 16)
+    static constexpr int kTmS = 0, kTmP = 16 * kSB * HG, kTmG = 32 * kSB * HG;
+    static constexpr int kTmUsed = kTmG + 2 * HG * kNG * 16;
+    static constexpr int kTmemCols = kTmUsed <= 256 ? 256 : 512;
+    static_assert(kTmUsed <= 512, "TMEM columns");
     static constexpr int kLoaderWarps = D == 128 ? 8 : 6;
     static constexpr int kLoader0 = 3, kEw0 = kLoader0 + kLoaderWarps, kEpi0 = kEw0 + 8;
     static constexpr int kThreads = 32 * (kEpi0 + 4);
     static constexpr int kBatch = 8;
 };
 
-template <int D, int PASS> struct BBars {
-    using C = BCfg<D, PASS>;
+template <int D, int PASS, int HG> struct BBars {
+    using C = BCfg<D, PASS, HG>;
     __host__ __device__ static constexpr int idxfull(int s) { return s; }
     __host__ __device__ static constexpr int a1full(int s) { return C::kNS + s; }
     __host__ __device__ static constexpr int a2full(int s) { return 2 * C::kNS + s; }
@@ -133,8 +138,8 @@ __device__ __forceinline__ void store_tile_row(uint8_t* tile, int p, const float
                               bpack2<T>(v[14], v[15]));
 }
 
-template <int D, typename T, int PASS>
-__global__ void __launch_bounds__(BCfg<D, PASS>::kThreads, 1)
+template <int D, typename T, int PASS, int HG>
+__global__ void __launch_bounds__(BCfg<D, PASS, HG>::kThreads, 1)
 k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
             const __grid_constant__ CUtensorMap tmG1, const __grid_constant__ CUtensorMap tmG2,
             const int4* __restrict__ meta, const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
@@ -142,8 +147,8 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             const uint8_t* __restrict__ A1g, const uint8_t* __restrict__ A2g, int64_t ld_bytes,
             const float* __restrict__ lse_t, const float* __restrict__ dd_t, int64_t nq16, float scale_log2,
             float g2scale, float g1scale) {
-    using C = BCfg<D, PASS>;
-    using B = BBars<D, PASS>;
+    using C = BCfg<D, PASS, HG>;
+    using B = BBars<D, PASS, HG>;
     using Slot = BSlot<C::kScal>;
     static_assert(sizeof(Slot) == C::kSlotBytes, "slot layout");
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -210,7 +215,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             int4 mt = make_int4(0, 0, 0, 0);
             if (lane < nclaim) {
                 it = atomicAdd(counter, 1);
-                if (it < n_items) mt = __ldg(meta + it / H);
+                if (it < n_items) mt = __ldg(meta + it / (H / HG));
             }
             __syncwarp();
             last = __shfl_sync(0xffffffffu, it, nclaim - 1);
@@ -220,7 +225,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                 const int32_t cb8 = __shfl_sync(0xffffffffu, mt.y, b);
                 const int32_t w = __shfl_sync(0xffffffffu, mt.z, b);
                 if (itb >= n_items) { done = true; continue; }
-                const int32_t h = itb - (itb / H) * H;
+                const int32_t h = (itb - (itb / (H / HG)) * (H / HG)) * HG;  // (first) head
                 const int nch = w > 0 ? (w + chunk_rows - 1) / chunk_rows : 1;
                 const int qs = qseq % C::kNQ;
                 const int qph = (qseq / C::kNQ) & 1;
@@ -229,10 +234,13 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                     mbar_arrive_expect_tx(bar(B::xyfull(qs)), C::kQBytes);
                     const uint32_t xd = sb + C::oQ + qs * C::kQBytes;
 #pragma unroll
-                    for (int pp = 0; pp < C::P; ++pp) {
-                        tma_load_2d(xd + pp * 2048, &tmX, bar(B::xyfull(qs)), h * D + 64 * pp, 16 * k);
-                        tma_load_2d(xd + C::kXBytes + pp * 2048, &tmY, bar(B::xyfull(qs)), h * D + 64 * pp, 16 * k);
-                    }
+                    for (int g = 0; g < HG; ++g)
+#pragma unroll
+                        for (int pp = 0; pp < C::P; ++pp) {
+                            const uint32_t o = g * 16 * C::kRowPitch + pp * 2048;
+                            tma_load_2d(xd + o, &tmX, bar(B::xyfull(qs)), (h + g) * D + 64 * pp, 16 * k);
+                            tma_load_2d(xd + C::kXBytes + o, &tmY, bar(B::xyfull(qs)), (h + g) * D + 64 * pp, 16 * k);
+                        }
                 }
                 for (int j = 0; j < nch; ++j) {
                     const int rows = w > 0 ? min(chunk_rows, w - chunk_rows * j) : 0;
@@ -247,15 +255,18 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                         sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2);
                         const uint32_t fb = bar(B::idxfull(s));
                         const uint32_t r8 = (uint32_t)((rows + 7) & ~7);
-                        const uint32_t scal = PASS == 0 ? 2u * 64u : 0u;  // rows: the window's 16 LSE and D
+                        const uint32_t scal = PASS == 0 ? 2u * 64u * HG : 0u;  // rows: the window's 16 LSE and D per head
                         mbar_arrive_expect_tx(fb, (rows > 0 ? r8 * 6u : 0u) + scal);
                         if (rows > 0) {
                             bulk_g2s(smem_u32(sl.cols), kcols + cb8 + chunk_rows * j, r8 * 4u, fb);
                             bulk_g2s(smem_u32(sl.masks), kmasks + cb8 + chunk_rows * j, r8 * 2u, fb);
                         }
                         if (PASS == 0) {
-                            bulk_g2s(smem_u32(sl.lse), lse_t + h * nq16 + 16 * (int64_t)k, 64u, fb);
-                            bulk_g2s(smem_u32(sl.dd), dd_t + h * nq16 + 16 * (int64_t)k, 64u, fb);
+#pragma unroll
+                            for (int g = 0; g < HG; ++g) {
+                                bulk_g2s(smem_u32(sl.lse + 16 * g), lse_t + (h + g) * nq16 + 16 * (int64_t)k, 64u, fb);
+                                bulk_g2s(smem_u32(sl.dd + 16 * g), dd_t + (h + g) * nq16 + 16 * (int64_t)k, 64u, fb);
+                            }
                         }
                     }
                     ++seq;
@@ -297,7 +308,8 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             const uint32_t d2 = sb + C::oT2 + t2 * C::kTile + pnl * 1024;
             const uint8_t* b1 = A1g + (int64_t)h * C::RB + piece * 16;
             const uint8_t* b2 = A2g + (int64_t)h * C::RB + piece * 16;
-            const int ops = (rows + kRowsPerOp - 1) / kRowsPerOp;
+            // HG = 1: tile row r = compacted column r.  HG = 4: tile row 32g + r = column r of head h + g
+            const int ops = HG == 1 ? (rows + kRowsPerOp - 1) / kRowsPerOp : C::kMaxRows / kRowsPerOp;
             mbar_wait(bar(B::t1free(t1)), ((seq / C::kN1) & 1) ^ 1);
             mbar_wait(bar(B::t2free(t2)), ((seq / C::kN2) & 1) ^ 1);
             int64_t jj[kIters];
@@ -307,27 +319,29 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 #pragma unroll
             for (int i = 0; i < kIters; ++i) {
                 const int t = lw + i * C::kLoaderWarps;
-                const int r = t * kRowsPerOp + rsub;
+                const int tr = t * kRowsPerOp + rsub;  // tile row
+                const int r = HG == 1 ? tr : (tr & 31);
                 ok[i] = t < ops && r < rows;
-                rr[i] = r;
+                rr[i] = tr;
                 jj[i] = ok[i] ? sl.cols[r] : 0;
-                dst[i] = (uint32_t)(r >> 3) * C::kGroupBytes + (uint32_t)(r & 7) * 128 + (uint32_t)((cc ^ (r & 7)) << 4);
+                dst[i] = (uint32_t)(tr >> 3) * C::kGroupBytes + (uint32_t)(tr & 7) * 128 + (uint32_t)((cc ^ (tr & 7)) << 4);
             }
 #pragma unroll
             for (int i = 0; i < kIters; ++i)
-                if (ok[i]) cp_async_16(d1 + dst[i], b1 + jj[i] * ld_bytes);
-            if (PASS == 1) {  // the gathered query rows' LSE and D (one lane per row)
+                if (ok[i]) cp_async_16(d1 + dst[i], b1 + jj[i] * ld_bytes + (HG == 1 ? 0 : (int64_t)(rr[i] >> 5) * C::RB));
+            if (PASS == 1) {  // the gathered query rows' LSE and D (one lane per tile row)
 #pragma unroll
                 for (int i = 0; i < kIters; ++i)
                     if (ok[i] && piece == 0) {
-                        cp_async_4(smem_u32(&sl.lse[rr[i]]), lse_t + h * nq16 + jj[i]);
-                        cp_async_4(smem_u32(&sl.dd[rr[i]]), dd_t + h * nq16 + jj[i]);
+                        const int64_t hh = h + (HG == 1 ? 0 : (rr[i] >> 5));
+                        cp_async_4(smem_u32(&sl.lse[rr[i]]), lse_t + hh * nq16 + jj[i]);
+                        cp_async_4(smem_u32(&sl.dd[rr[i]]), dd_t + hh * nq16 + jj[i]);
                     }
             }
             cp_async_mbar_arrive(f1);
 #pragma unroll
             for (int i = 0; i < kIters; ++i)
-                if (ok[i]) cp_async_16(d2 + dst[i], b2 + jj[i] * ld_bytes);
+                if (ok[i]) cp_async_16(d2 + dst[i], b2 + jj[i] * ld_bytes + (HG == 1 ? 0 : (int64_t)(rr[i] >> 5) * C::RB));
             cp_async_mbar_arrive(f2);
         }
     } else if (warp == 1) {
@@ -352,12 +366,14 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                 const uint64_t bx = dX + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
                 const uint64_t by = dX + ((sb + C::oQ + qslot * C::kQBytes + C::kXBytes) >> 4);
 #pragma unroll
-                for (int kk = 0; kk < C::RB / 32; ++kk) {
-                    const uint32_t ao = ((kk >> 2) * 1024 + (kk & 3) * 32) >> 4;
-                    const uint32_t bo = ((kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
-                    mma_f16_ss_warp(tmem + C::kTmS + b * 16, a1 + ao, bx + bo, idesc1, kk > 0 ? 1u : 0u);
-                    mma_f16_ss_warp(tmem + C::kTmP + b * 16, a2 + ao, by + bo, idesc1, kk > 0 ? 1u : 0u);
-                }
+                for (int g = 0; g < HG; ++g)  // HG > 1: head g against its own X/Y tile; lanes 32g.. are read
+#pragma unroll
+                    for (int kk = 0; kk < C::RB / 32; ++kk) {
+                        const uint32_t ao = ((kk >> 2) * 1024 + (kk & 3) * 32) >> 4;
+                        const uint32_t bo = (g * 16 * C::kRowPitch + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
+                        mma_f16_ss_warp(tmem + C::kTmS + (b * HG + g) * 16, a1 + ao, bx + bo, idesc1, kk > 0 ? 1u : 0u);
+                        mma_f16_ss_warp(tmem + C::kTmP + (b * HG + g) * 16, a2 + ao, by + bo, idesc1, kk > 0 ? 1u : 0u);
+                    }
             }
             mma_commit_warp(bar(B::sfull(b)));
             if (PASS == 0) mma_commit_warp(bar(B::t2free(n1 % C::kN2)));  // rows: V_c is MMA1's alone
@@ -398,16 +414,20 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                 const uint64_t a1 = dA + ((sb + C::oT1 + (n2 % C::kN1) * C::kTile) >> 4);
                 const uint64_t a2 = dA + ((sb + C::oT2 + (n2 % C::kN2) * C::kTile) >> 4);
                 const uint64_t p0 = dPt + ((sb + C::oP + b * C::kNT * C::kPBytes) >> 4);
-                const int nsteps = (rows + 15) / 16;
-                for (int st = 0; st < nsteps; ++st) {
-                    const uint32_t acc = (any || st > 0) ? 1u : 0u;
-                    const uint32_t ao = (st * 2 * C::kGroupBytes) >> 4, po = (st * 512) >> 4;
-                    if (PASS == 0) {
-                        mma_f16_ss_warp(tmem + C::kTmG + a * 16, a1 + ao, p0 + po, idesc2, acc);
-                    } else {
-                        mma_f16_ss_warp(tmem + C::kTmG + a * 32, a2 + ao, p0 + po, idesc2, acc);           // dV
-                        mma_f16_ss_warp(tmem + C::kTmG + a * 32 + 16, a1 + ao, p0 + (C::kPBytes >> 4) + po,  // dK
-                                        idesc2, acc);
+                const int nsteps = HG == 1 ? (rows + 15) / 16 : 2;  // head groups: 32 tile rows per head
+#pragma unroll
+                for (int g = 0; g < HG; ++g) {
+                    const uint32_t gacc = C::kTmG + (a * HG + g) * 16 * C::kNG;  // this item buffer's head g
+                    for (int st = 0; st < nsteps; ++st) {
+                        const uint32_t acc = (any || st > 0) ? 1u : 0u;
+                        const uint32_t ao = (g * 4 * C::kGroupBytes + st * 2 * C::kGroupBytes) >> 4;
+                        const uint32_t po = (g * 1024 + st * 512) >> 4;
+                        if (PASS == 0) {
+                            mma_f16_ss_warp(tmem + gacc, a1 + ao, p0 + po, idesc2, acc);
+                        } else {
+                            mma_f16_ss_warp(tmem + gacc, a2 + ao, p0 + po, idesc2, acc);                         // dV
+                            mma_f16_ss_warp(tmem + gacc + 16, a1 + ao, p0 + (C::kPBytes >> 4) + po, idesc2, acc);  // dK
+                        }
                     }
                 }
                 any = true;
@@ -431,9 +451,11 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         // TMEM lane p = chunk entry p (rows: compacted column j; cols: compacted query row i), the 16
         // TMEM columns = the window's 16 query rows (rows) or key columns (cols)
         const int q = warp & 3;
-        const int p = 32 * q + lane;
+        const int p = 32 * q + lane;  // tile row = TMEM lane
+        const int col = HG == 1 ? p : lane;  // compacted column / row of the chunk (HG = 4: of head q)
         const int wg = (warp - C::kEw0) >> 2;
         const uint32_t tl = (uint32_t)(32 * q) << 16;
+        const int hb = HG == 1 ? 0 : q;  // the warp's head within the group
         for (int32_t seq = wg;; seq += 2) {
             const int s = seq % C::kNS, b = seq % C::kSB;
             const uint32_t bph = (seq / C::kSB) & 1;
@@ -442,7 +464,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             const int rows = sl.rows;
             if (rows < 0) break;
             if (PASS == 1) mbar_wait(bar(B::a1full(s)), (seq / C::kNS) & 1);  // the gathered LSE and D
-            const uint32_t mask = p < rows ? (uint32_t)sl.masks[p] : 0u;
+            const uint32_t mask = col < rows ? (uint32_t)sl.masks[col] : 0u;
             float lse_p = 0.f, dd_p = 0.f;
             if (PASS == 1) {
                 lse_p = sl.lse[p];
@@ -451,16 +473,16 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             mbar_wait(bar(B::sfull(b)), bph);
             tc_fence_after();
             float x[16], y[16];
-            tmem_ld_32x32b_x16(tmem + tl + C::kTmS + b * 16, x);
-            tmem_ld_32x32b_x16(tmem + tl + C::kTmP + b * 16, y);
+            tmem_ld_32x32b_x16(tmem + tl + C::kTmS + (b * HG + hb) * 16, x);
+            tmem_ld_32x32b_x16(tmem + tl + C::kTmP + (b * HG + hb) * 16, y);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(B::sfree(b)));
             float pr[16], ds[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                const float l = PASS == 0 ? sl.lse[i] : lse_p;
-                const float dd = PASS == 0 ? sl.dd[i] : dd_p;
+                const float l = PASS == 0 ? sl.lse[16 * hb + i] : lse_p;
+                const float dd = PASS == 0 ? sl.dd[16 * hb + i] : dd_p;
                 const float pv = ((mask >> i) & 1u) ? ex2(fmaf(x[i], scale_log2, -l)) : 0.f;
                 pr[i] = pv;
                 ds[i] = pv * (y[i] - dd);
@@ -490,23 +512,27 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             const int4 r = rec[a];
             if (r.x < 0) break;
             tc_fence_after();
-            float g1[16], g2[16];
-            tmem_ld_32x32b_x16(tmem + tl + C::kTmG + a * 16 * C::kNG, g1);
-            if (PASS == 1) tmem_ld_32x32b_x16(tmem + tl + C::kTmG + a * 32 + 16, g2);
-            tc_fence_before();
-            mbar_arrive(bar(B::gempty(a)));
             const bool nz = r.z != 0;  // an item with no entries has an untouched accumulator: zeros
             if (lead) bulk_wait_group_read<0>();
             named_bar_sync(3, 128);
             float* o1 = reinterpret_cast<float*>(smem + C::oOst);
-            float* o2 = o1 + 16 * D;
-            if (has) {
+            float* o2 = o1 + 16 * D * HG;
+#pragma unroll 1
+            for (int g = 0; g < HG; ++g) {  // [16 x HG*D] tiles: head g in columns g*D ..
+                float g1[16], g2[16];
+                const uint32_t gacc = C::kTmG + (a * HG + g) * 16 * C::kNG;
+                tmem_ld_32x32b_x16(tmem + tl + gacc, g1);
+                if (PASS == 1) tmem_ld_32x32b_x16(tmem + tl + gacc + 16, g2);
+                if (has) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    o1[i * D + f] = nz ? g1[i] * g1scale : 0.f;
-                    if (PASS == 1) o2[i * D + f] = nz ? g2[i] * g2scale : 0.f;
+                    for (int i = 0; i < 16; ++i) {
+                        o1[i * (HG * D) + g * D + f] = nz ? g1[i] * g1scale : 0.f;
+                        if (PASS == 1) o2[i * (HG * D) + g * D + f] = nz ? g2[i] * g2scale : 0.f;
+                    }
                 }
             }
+            tc_fence_before();
+            mbar_arrive(bar(B::gempty(a)));
             fence_proxy_async_smem();
             named_bar_sync(3, 128);
             if (lead) {
@@ -558,11 +584,11 @@ __global__ void __launch_bounds__(256) k_bwd_prep(const float* __restrict__ Op, 
     }
 }
 
-template <int D, typename T, int PASS>
-f3s_status launch_pass(const Plan& p, const void* X, const void* Y, const void* A1, const void* A2, float* G1,
-                       float* G2, const float* lse_t, const float* dd_t, int64_t nq16, int H, float scale,
-                       int sms, cudaStream_t stream) {
-    using C = BCfg<D, PASS>;
+template <int D, typename T, int PASS, int HG>
+f3s_status launch_pass_hg(const Plan& p, const void* X, const void* Y, const void* A1, const void* A2, float* G1,
+                          float* G2, const float* lse_t, const float* dd_t, int64_t nq16, int H, float scale,
+                          int sms, cudaStream_t stream) {
+    using C = BCfg<D, PASS, HG>;
     if (p.num_rw == 0) return F3S_OK;
     const f3s_dtype dt = std::is_same<T, __half>::value ? F3S_FP16 : F3S_BF16;
     const int64_t ld = (int64_t)H * D;
@@ -570,34 +596,33 @@ f3s_status launch_pass(const Plan& p, const void* X, const void* Y, const void* 
     f3s_status st;
     if ((st = make_map(&mx, X, dt, ld, p.n_rows, ld, 16)) != F3S_OK) return st;
     if ((st = make_map(&my, Y, dt, ld, p.n_rows, ld, 16)) != F3S_OK) return st;
-    if ((st = make_map(&mg1, G1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ld, p.n_rows, ld, D, 16,
+    if ((st = make_map(&mg1, G1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ld, p.n_rows, ld, D * HG, 16,
                        CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK)
         return st;
     mg2 = mg1;
-    if (PASS == 1 &&
-        (st = make_map(&mg2, G2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ld, p.n_rows, ld, D, 16, CU_TENSOR_MAP_SWIZZLE_NONE)) !=
-            F3S_OK)
+    if (PASS == 1 && (st = make_map(&mg2, G2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ld, p.n_rows, ld, D * HG, 16,
+                                    CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK)
         return st;
     static std::atomic<uint64_t> attr_set{0};
     static std::mutex mu;
     if (!(attr_set.load() >> p.device & 1)) {
         std::lock_guard<std::mutex> lock(mu);
         if (!(attr_set.load() >> p.device & 1)) {
-            F3S_CUDA_TRY(cudaFuncSetAttribute(k_bwd_sm100<D, T, PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            F3S_CUDA_TRY(cudaFuncSetAttribute(k_bwd_sm100<D, T, PASS, HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               C::kSmemBytes));
             attr_set.fetch_or(uint64_t(1) << p.device);
         }
     }
-    const int64_t n_items64 = (int64_t)p.num_rw * H;
+    const int64_t n_items64 = (int64_t)p.num_rw * (H / HG);
     if (n_items64 > 0x7FFFFFFF) { set_error("too many work items"); return F3S_ERR_UNSUPPORTED; }
     char* scratch = nullptr;
     F3S_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&scratch), 256, stream));
     cudaError_t err = cudaMemsetAsync(scratch, 0, sizeof(int32_t), stream);
     if (err == cudaSuccess) {
         const int grid = (int)std::min<int64_t>(n_items64, sms);
-        k_bwd_sm100<D, T, PASS><<<grid, C::kThreads, C::kSmemBytes, stream>>>(
+        k_bwd_sm100<D, T, PASS, HG><<<grid, C::kThreads, C::kSmemBytes, stream>>>(
             mx, my, mg1, mg2, p.meta_lpt, p.kcols, p.kmasks, reinterpret_cast<int32_t*>(scratch), (int32_t)n_items64,
-            (int32_t)std::min<int64_t>((int64_t)p.n_heavy_lpt * H, 0x7FFFFFFF), H,
+            (int32_t)std::min<int64_t>((int64_t)p.n_heavy_lpt * (H / HG), 0x7FFFFFFF), H,
             static_cast<const uint8_t*>(A1), static_cast<const uint8_t*>(A2), ld * 2, lse_t, dd_t, nq16,
             scale * 1.4426950408889634f, scale, PASS == 0 ? scale : 1.f);
         count_launch();
@@ -607,6 +632,18 @@ f3s_status launch_pass(const Plan& p, const void* X, const void* Y, const void* 
     F3S_CUDA_TRY(err);
     F3S_CUDA_TRY(ferr);
     return F3S_OK;
+}
+
+// head groups of 4 when d = 64, H % 4 == 0 and every window of the pass's plan has <= 32 columns
+template <int D, typename T, int PASS>
+f3s_status launch_pass(const Plan& p, const void* X, const void* Y, const void* A1, const void* A2, float* G1,
+                       float* G2, const float* lse_t, const float* dd_t, int64_t nq16, int H, float scale,
+                       int sms, cudaStream_t stream) {
+    if constexpr (D == 64) {
+        if (H % 4 == 0 && p.max_width <= 32)
+            return launch_pass_hg<D, T, PASS, 4>(p, X, Y, A1, A2, G1, G2, lse_t, dd_t, nq16, H, scale, sms, stream);
+    }
+    return launch_pass_hg<D, T, PASS, 1>(p, X, Y, A1, A2, G1, G2, lse_t, dd_t, nq16, H, scale, sms, stream);
 }
 
 struct Scratch2 {

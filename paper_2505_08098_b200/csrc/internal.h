@@ -101,7 +101,7 @@ inline int32_t default_split_chunks(int64_t total_chunks, int32_t num_sms) {
 }
 
 // Stream-ordered per-call scratch from the library's own memory pool on the current device
-// (release threshold 256 MB, so steady-state calls reuse pool memory instead of mapping new
+// (freed memory stays reserved in the pool -- no release threshold -- so steady-state calls reuse it instead of mapping new
 // pages at every call; a pool of its own leaves the caller's default-pool settings alone).
 cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t stream);
 cudaError_t scratch_free(void* ptr, cudaStream_t stream);

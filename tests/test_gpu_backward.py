@@ -117,3 +117,29 @@ def test_backward_tc_vs_simt(f3s, oracle_mod, dtype, d, H):
         _close(a, r)
         _close(b, r)
         _close(a, b.astype(np.float64))
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("H", [4, 8])
+def test_backward_head_groups(f3s, oracle_mod, dtype, H):
+    """d = 64, H % 4 == 0, every window <= 32 columns (the batched-molecules shape): both backward
+    passes run 4 heads per chunk; parity with the oracle and with the CUDA-core kernels."""
+    import torch
+    csr = fi.molecules(300, 25, 150, seed=H)
+    n = csr.n_rows
+    Qb, Kb, Vb = make_qkv(n, n, H, 64, dtype, seed=12)
+    G = np.random.default_rng(H).standard_normal((n, H, 64)).astype(np.float32)
+    rp, ci = csr_to_dev(csr)
+    p = f3s.plan(rp, ci, n)
+    assert p.info()["max_width"] <= 32
+    dO = torch.from_numpy(G).cuda()
+    Q, K, V = to_dev(Qb, dtype), to_dev(Kb, dtype), to_dev(Vb, dtype)
+    tc = [x.cpu().numpy() for x in f3s.attention_backward(p, Q, K, V, dO, scale=0.125, variant="tc")]
+    again = [x.cpu().numpy() for x in f3s.attention_backward(p, Q, K, V, dO, scale=0.125, variant="tc")]
+    simt = [x.cpu().numpy() for x in f3s.attention_backward(p, Q, K, V, dO, scale=0.125, variant="simt")]
+    ref = oracle_mod.attention_backward(csr.row_ptr, csr.col_idx, decode(Qb, dtype), decode(Kb, dtype),
+                                        decode(Vb, dtype), G.astype(np.float64), scale=0.125)
+    for a, b, c, r in zip(tc, again, simt, ref):
+        assert np.array_equal(a, b)
+        _close(a, r)
+        _close(a, c.astype(np.float64))
