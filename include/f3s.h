@@ -237,6 +237,30 @@ f3s_status f3s_attention_merge(int32_t parts, const float* O_parts, const float*
 f3s_status f3s_attention_backward(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* dO,
                                   float* dQ, float* dK, float* dV, float scale, int32_t heads, int32_t d,
                                   f3s_dtype dtype, cudaStream_t stream);
+/*
+ * Training forward: O exactly as f3s_attention (bitwise: the same kernel and
+ * rounding) plus each row's softmax statistics, which f3s_attention_backward_saved consumes instead
+ * of recomputing the forward.  ml[i][h] = (m, l): m the row maximum of scale * log2(e) * q_i . k_j
+ * over the row's entries (Alg.1 l.16, in log2 units; -8.5e37 for an empty row), l = sum_j
+ * 2^(s_ij - m) (l.17; 0 for an empty row), so LSE_i = m + log2(l) in the same units.
+ *  O   device float [n_rows, heads, d];  ml device float [n_rows, heads, 2] (8-byte aligned).
+ * Errors: as f3s_attention; INVALID_VALUE for NULL ml.
+ */
+f3s_status f3s_attention_fwd(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float* ml,
+                             float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
+
+/*
+ * f3s_attention_backward with the forward's saved outputs (O, ml from f3s_attention_fwd on the same
+ * plan, Q, K, V, scale): the same two tensor-core passes without the forward recomputation (the
+ * backward of a training step: PAPER.md:752).  D_i = dO_i . O_i and LSE_i = m_i + log2(l_i).
+ *  O   device float [n_rows, heads, d] (16-byte aligned);  ml device float [n_rows, heads, 2].
+ *  Other arguments as f3s_attention_backward (stream-ordered scratch of about n_rows * H * (2 d + 8)
+ *  bytes).  Errors: as f3s_attention_backward; INVALID_VALUE for NULL O/ml.
+ */
+f3s_status f3s_attention_backward_saved(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* O,
+                                        const float* ml, const float* dO, float* dQ, float* dK, float* dV, float scale,
+                                        int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
+
 /* variant 0: the tensor-core path of f3s_attention_backward; 1: the CUDA-core two-pass kernels
  * (one warp per row / column walking its entries in fp32: online max/sum/D, then p, ds; the
  * reference for the tensor-core path).  Errors: as f3s_attention_backward; INVALID_VALUE for

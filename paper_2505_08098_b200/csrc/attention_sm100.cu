@@ -229,7 +229,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const uint8_t* __restrict__ Kg, const uint8_t* __restrict__ Vg, float scale_log2,
             uint64_t* __restrict__ trace, int32_t trace_chunks, int32_t expt_arg,
             float* __restrict__ scratch, float2* __restrict__ ml_out, int32_t n_rows, float* __restrict__ Og,
-            int32_t heavy_items) {
+            int32_t heavy_items, int32_t ml_norm) {
     constexpr int EB = (int)sizeof(T);
     using C = Cfg<D, HG, EB>;
     using B = Bars<D, HG, EB>;
@@ -734,7 +734,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                     float ov[16];
                     tmem_ld_32x32b_x16(tmem + tl + C::kTmemO + (b * HG + g) * 16, ov);
                     const float4* l4 = reinterpret_cast<const float4*>(corr[b].lpart[g]);  // head g's row sums
-                    if (has && !kPart) {
+                    if (has && (!kPart || ml_norm)) {
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const float4 lv = l4[u];
@@ -745,7 +745,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                                 ost[i * (HG * D) + g * D + f] = (rows > 0 && lt[v] > 0.f) ? ov[i] * rcp_approx(lt[v]) : 0.f;
                             }
                         }
-                    } else if (has) {  // partial mode: unnormalised O, the head's (m, l) below
+                    } else if (has) {  // partial mode: unnormalised O (unless ml_norm), the head's (m, l) below
 #pragma unroll
                         for (int i = 0; i < 16; ++i) ost[i * (HG * D) + g * D + f] = rows > 0 ? ov[i] : 0.f;
                     }
@@ -806,8 +806,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             if (flags & 2) {
                 // O_i = diag(l)^-1 O_i (l.24); empty row (l = 0) -> 0 (reading c4).  Partial mode
                 // (ml_out != nullptr, f3s_attention_partial): O stays unnormalised and the row's
-                // (m, l) go to ml_out, for f3s_attention_merge to combine column blocks
-                const float linv = ml_out ? 1.f : l_run > 0.f ? rcp_approx(l_run) : 0.f;
+                // (m, l) go to ml_out, for f3s_attention_merge to combine column blocks; with
+                // ml_norm (f3s_attention_fwd) O is normalised as in f3s_attention and (m, l) kept
+                const float linv = (ml_out && !ml_norm) ? 1.f : l_run > 0.f ? rcp_approx(l_run) : 0.f;
                 float li[16];  // 1 / l of the 16 rows, broadcast to every lane (outside the lane-divergent stores)
 #pragma unroll
                 for (int i = 0; i < 16; ++i) li[i] = __shfl_sync(0xffffffffu, linv, i);
@@ -870,7 +871,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 template <int D>
 __global__ void __launch_bounds__(256) k_split_merge(const int4* __restrict__ ginfo, const float* __restrict__ scratch,
                                                      float* __restrict__ O, int32_t H, int32_t n_rows,
-                                                     float2* __restrict__ ml_out) {
+                                                     float2* __restrict__ ml_out, int32_t ml_norm) {
     const int g = blockIdx.x / H, h = blockIdx.x - (blockIdx.x / H) * H;
     const int4 gi = ginfo[g];
     const int64_t rec_floats = 32 + 16 * D, stride = (int64_t)H * rec_floats;
@@ -888,8 +889,8 @@ __global__ void __launch_bounds__(256) k_split_merge(const int4* __restrict__ gi
         }
         const int64_t row = 16 * (int64_t)gi.z + i;
         if (row >= n_rows) continue;
-        if (ml_out) {  // partial mode: the window's unnormalised O and its (m, l)
-            O[(row * H + h) * D + f] = acc;
+        if (ml_out) {  // partial mode: the window's unnormalised O (normalised: ml_norm) and its (m, l)
+            O[(row * H + h) * D + f] = ml_norm ? (l > 0.f ? acc / l : 0.f) : acc;
             if (f == 0) ml_out[row * H + h] = make_float2(M, l);
         } else {
             O[(row * H + h) * D + f] = l > 0.f ? acc / l : 0.f;  // empty row -> 0 (reading c4)
@@ -1083,14 +1084,15 @@ f3s_status launch(const AttnArgs& a) {
             reinterpret_cast<float2*>(a.ml_out), p.n_rows, a.O,
             a.lpt ? (int32_t)std::min<int64_t>((int64_t)std::max(0, p.n_heavy_sub - a.sub_begin) * (a.heads / HG),
                                                0x7FFFFFFF)
-                  : 0);
+                  : 0,
+            a.ml_norm ? 1 : 0);
         count_launch();
         err = cudaGetLastError();
     }
     if (err == cudaSuccess && split) {
         k_split_merge<D><<<(int)((int64_t)p.n_groups * a.heads), 256, 0, a.stream>>>(
             p.ginfo, reinterpret_cast<const float*>(scratch + 256), a.O, a.heads, p.n_rows,
-            reinterpret_cast<float2*>(a.ml_out));
+            reinterpret_cast<float2*>(a.ml_out), a.ml_norm ? 1 : 0);
         count_launch();
         err = cudaGetLastError();
     }

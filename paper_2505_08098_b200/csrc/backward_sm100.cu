@@ -552,12 +552,13 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 }
 
 // LSE (log2 units incl. scale), D = dO . O and dO in the input dtype, from the forward's partial
-// outputs (unnormalised O, (m, l)); one warp per (row, head).  Head-major LSE / D ([H][nq16]).
+// outputs (unnormalised O, (m, l)) or the saved outputs of f3s_attention_fwd (normalized: O / l,
+// (m, l)); one warp per (row, head).  Head-major LSE / D ([H][nq16]).
 template <int D, typename T>
 __global__ void __launch_bounds__(256) k_bwd_prep(const float* __restrict__ Op, const float2* __restrict__ ml,
                                                   const float* __restrict__ dO, int64_t n_rows, int32_t H,
                                                   int64_t nq16, float* __restrict__ lse_t, float* __restrict__ dd_t,
-                                                  T* __restrict__ dO16) {
+                                                  T* __restrict__ dO16, int32_t normalized) {
     constexpr int E = D / 32;
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -565,7 +566,7 @@ __global__ void __launch_bounds__(256) k_bwd_prep(const float* __restrict__ Op, 
         const int64_t i = rh / H;
         const int h = (int)(rh - i * H);
         const float2 v = ml[rh];
-        const float inv = v.y > 0.f ? 1.f / v.y : 0.f;
+        const float inv = normalized ? 1.f : v.y > 0.f ? 1.f / v.y : 0.f;  // saved O is already O / l
         float acc = 0.f;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -653,8 +654,9 @@ struct Scratch2 {
 };
 
 template <int D, typename T>
-f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, const float* dO, float* dQ, float* dK,
-                         float* dV, float scale, int H, cudaStream_t stream) {
+f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, const float* O_saved,
+                         const float* ml_saved, const float* dO, float* dQ, float* dK, float* dV, float scale, int H,
+                         cudaStream_t stream) {
     f3s_status st = build_transpose_plan(p, stream);
     if (st != F3S_OK) return st;
     Plan& tp = *p.tplan;
@@ -665,21 +667,29 @@ f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, c
     Scratch2 sc;
     sc.s = stream;
     const int64_t nh2 = (n * H + 1) / 2 * 2;  // keeps the arrays after (m, l) 16-byte aligned
-    const size_t bytes = sizeof(float) * (size_t)nd + sizeof(float2) * (size_t)nh2 +
+    const bool saved = O_saved != nullptr;      // f3s_attention_backward_saved: no forward recomputation
+    const size_t bytes = (saved ? 0 : sizeof(float) * (size_t)nd + sizeof(float2) * (size_t)nh2) +
                          2 * sizeof(float) * (size_t)(H * nq16) + sizeof(T) * (size_t)nd + 256;
     F3S_CUDA_TRY(scratch_alloc(&sc.p, bytes, stream));
     char* base = static_cast<char*>(sc.p);
-    float* Op = reinterpret_cast<float*>(base);
-    float* ml = Op + nd;
-    float* lse_t = ml + 2 * nh2;
+    const float* Op = O_saved;
+    const float* ml = ml_saved;
+    float* lse_t = reinterpret_cast<float*>(base);
+    if (!saved) {
+        // 1. the forward's (m, l) and unnormalised O
+        float* op = reinterpret_cast<float*>(base);
+        float* mlp = op + nd;
+        lse_t = mlp + 2 * nh2;
+        AttnArgs a{&p, Q, K, V, op, scale, H, D, std::is_same<T, __half>::value ? F3S_FP16 : F3S_BF16, true, stream};
+        a.ml_out = mlp;
+        if ((st = launch_attention_sm100(a)) != F3S_OK) return st;
+        Op = op;
+        ml = mlp;
+    }
     float* dd_t = lse_t + H * nq16;
     T* dO16 = reinterpret_cast<T*>(dd_t + H * nq16);
-    // 1. the forward's (m, l) and unnormalised O
-    AttnArgs a{&p, Q, K, V, Op, scale, H, D, std::is_same<T, __half>::value ? F3S_FP16 : F3S_BF16, true, stream};
-    a.ml_out = ml;
-    if ((st = launch_attention_sm100(a)) != F3S_OK) return st;
     k_bwd_prep<D, T><<<(int)std::min<int64_t>((n * H + 7) / 8, (int64_t)sms * 16), 256, 0, stream>>>(
-        Op, reinterpret_cast<const float2*>(ml), dO, n, H, nq16, lse_t, dd_t, dO16);
+        Op, reinterpret_cast<const float2*>(ml), dO, n, H, nq16, lse_t, dd_t, dO16, saved ? 1 : 0);
     count_launch();
     F3S_CUDA_TRY(cudaGetLastError());
     // 2. rows: dQ
@@ -696,14 +706,14 @@ f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, c
 
 }  // namespace
 
-f3s_status launch_attention_backward_tc(Plan& p, const void* Q, const void* K, const void* V, const float* dO,
-                                        float* dQ, float* dK, float* dV, float scale, int heads, int d,
-                                        f3s_dtype dtype, cudaStream_t stream) {
+f3s_status launch_attention_backward_tc(Plan& p, const void* Q, const void* K, const void* V, const float* O,
+                                        const float* ml, const float* dO, float* dQ, float* dK, float* dV,
+                                        float scale, int heads, int d, f3s_dtype dtype, cudaStream_t stream) {
     if (dtype == F3S_FP16)
-        return d == 64 ? launch_bwd_tc<64, __half>(p, Q, K, V, dO, dQ, dK, dV, scale, heads, stream)
-                       : launch_bwd_tc<128, __half>(p, Q, K, V, dO, dQ, dK, dV, scale, heads, stream);
-    return d == 64 ? launch_bwd_tc<64, __nv_bfloat16>(p, Q, K, V, dO, dQ, dK, dV, scale, heads, stream)
-                   : launch_bwd_tc<128, __nv_bfloat16>(p, Q, K, V, dO, dQ, dK, dV, scale, heads, stream);
+        return d == 64 ? launch_bwd_tc<64, __half>(p, Q, K, V, O, ml, dO, dQ, dK, dV, scale, heads, stream)
+                       : launch_bwd_tc<128, __half>(p, Q, K, V, O, ml, dO, dQ, dK, dV, scale, heads, stream);
+    return d == 64 ? launch_bwd_tc<64, __nv_bfloat16>(p, Q, K, V, O, ml, dO, dQ, dK, dV, scale, heads, stream)
+                   : launch_bwd_tc<128, __nv_bfloat16>(p, Q, K, V, O, ml, dO, dQ, dK, dV, scale, heads, stream);
 }
 
 }  // namespace f3s

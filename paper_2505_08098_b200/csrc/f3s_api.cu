@@ -267,8 +267,58 @@ f3s_status f3s_attention_backward_ex(f3s_plan_t plan, const void* Q, const void*
         DeviceScope scope;
         F3S_CUDA_TRY(scope.enter(p.device));
         if (variant == 0 && p.nnz > 0 && p.n_rows > 0)
-            return launch_attention_backward_tc(p, Q, K, V, dO, dQ, dK, dV, scale, heads, d, dtype, stream);
+            return launch_attention_backward_tc(p, Q, K, V, nullptr, nullptr, dO, dQ, dK, dV, scale, heads, d, dtype,
+                                                stream);
         return launch_attention_backward(p, Q, K, V, dO, dQ, dK, dV, scale, heads, d, dtype, stream);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_fwd(f3s_plan_t plan, const void* Q, const void* K, const void* V, float* O, float* ml,
+                             float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
+    try {
+        f3s_status st = check_attention_args(plan, Q, K, V, O, scale, heads, d, dtype, true);
+        if (st != F3S_OK) return st;
+        const Plan& p = *reinterpret_cast<const Plan*>(plan);
+        if (p.n_rows > 0 && !ml) { set_error("ml is NULL"); return F3S_ERR_INVALID_VALUE; }
+        if (reinterpret_cast<uintptr_t>(ml) & 7) { set_error("ml must be 8-byte aligned"); return F3S_ERR_UNSUPPORTED; }
+        if (p.n_rows == 0) return F3S_OK;
+        AttnArgs a{&p, Q, K, V, O, scale, heads, d, dtype, true, stream};
+        a.ml_out = ml;
+        a.ml_norm = true;
+        DeviceScope scope;
+        F3S_CUDA_TRY(scope.enter(p.device));
+        if (p.nnz == 0 || p.n_cols == 0) {  // every row is empty: O = 0, (m, l) = (floor, 0) (reading c4)
+            F3S_CUDA_TRY(cudaMemsetAsync(O, 0, sizeof(float) * (size_t)p.n_rows * heads * d, stream));
+            return launch_fill_ml(ml, (int64_t)p.n_rows * heads, stream);
+        }
+        return launch_attention_sm100(a);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_backward_saved(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* O,
+                                        const float* ml, const float* dO, float* dQ, float* dK, float* dV, float scale,
+                                        int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
+    try {
+        f3s_status st = check_attention_args(plan, Q, K, V, dQ, scale, heads, d, dtype, true);
+        if (st != F3S_OK) return st;
+        if (dtype == F3S_E4M3) { set_error("backward: F3S_FP16 or F3S_BF16 only"); return F3S_ERR_UNSUPPORTED; }
+        Plan& p = *reinterpret_cast<Plan*>(plan);
+        if (p.n_rows > 0 && (!dO || !O || !ml)) { set_error("O/ml/dO is NULL"); return F3S_ERR_INVALID_VALUE; }
+        if (p.n_cols > 0 && (!dK || !dV)) { set_error("dK/dV is NULL"); return F3S_ERR_INVALID_VALUE; }
+        auto mis = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) != 0; };
+        if (mis(dO) || mis(dK) || mis(dV) || mis(O)) { set_error("O/dO/dK/dV must be 16-byte aligned"); return F3S_ERR_UNSUPPORTED; }
+        if (reinterpret_cast<uintptr_t>(ml) & 7) { set_error("ml must be 8-byte aligned"); return F3S_ERR_UNSUPPORTED; }
+        DeviceScope scope;
+        F3S_CUDA_TRY(scope.enter(p.device));
+        if (p.nnz > 0 && p.n_rows > 0)
+            return launch_attention_backward_tc(p, Q, K, V, O, ml, dO, dQ, dK, dV, scale, heads, d, dtype, stream);
+        return launch_attention_backward(p, Q, K, V, dO, dQ, dK, dV, scale, heads, d, dtype, stream);  // all zero
     } catch (...) {
         set_error("internal error");
         return F3S_ERR_INTERNAL;

@@ -133,6 +133,7 @@ struct AttnArgs {
     int64_t kv_ld = 0;          // elements between consecutive K (and V) rows; 0 = heads * d
     int64_t q_ld = 0;           // elements between consecutive Q rows; 0 = heads * d
     float* ml_out = nullptr;    // partial mode: [n_rows, heads] (m, l) pairs; O left unnormalised
+    bool ml_norm = false;       // with ml_out: O normalised as in f3s_attention (f3s_attention_fwd)
     int32_t max_ctas = 0;       // > 0: at most this many CTAs (SMs left for a concurrent collective)
     int32_t sub_begin = 0, sub_end = -1;  // LPT order: this launch's range of meta_sub entries (-1: to the end)
 };
@@ -153,9 +154,10 @@ constexpr int kSplitChunkCols = 128;  // column granularity of the split (the ke
 constexpr int kHeavyChunks = 8;       // an item of this many chunks is claimed alone (= the claim batch)
 f3s_status launch_attention_simt(const AttnArgs& a);
 f3s_status build_transpose_plan(Plan& p, cudaStream_t stream);
-f3s_status launch_attention_backward_tc(Plan& p, const void* Q, const void* K, const void* V, const float* dO,
-                                        float* dQ, float* dK, float* dV, float scale, int heads, int d,
-                                        f3s_dtype dtype, cudaStream_t stream);
+// O, ml: the saved outputs of f3s_attention_fwd, or NULL (the forward is recomputed in partial mode)
+f3s_status launch_attention_backward_tc(Plan& p, const void* Q, const void* K, const void* V, const float* O,
+                                        const float* ml, const float* dO, float* dQ, float* dK, float* dV,
+                                        float scale, int heads, int d, f3s_dtype dtype, cudaStream_t stream);
 f3s_status launch_attention_backward(Plan& p, const void* Q, const void* K, const void* V, const float* dO, float* dQ,
                                      float* dK, float* dV, float scale, int heads, int d, f3s_dtype dtype,
                                      cudaStream_t stream);

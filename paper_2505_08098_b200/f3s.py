@@ -54,6 +54,9 @@ _lib.f3s_attention_merge.argtypes = [_i32, _vp, _vp, _i64, _i32, _i32, _vp, _vp]
 _lib.f3s_attention_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_trace.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]
 _lib.f3s_attention_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_fwd.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
+_lib.f3s_attention_backward_saved.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32,
+                                              _i32, _vp]
 _lib.f3s_attention_backward_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_host_async.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
@@ -75,7 +78,7 @@ EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info"
             "f3s_attention", "f3s_attention_kv", "f3s_attention_strided", "f3s_attention_partial",
             "f3s_attention_merge", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host",
             "f3s_partition_rows", "f3s_partition_at",
-            "f3s_attention_backward", "f3s_attention_backward_ex", "f3s_attention_host_async", "f3s_default_split_chunks",
+            "f3s_attention_backward", "f3s_attention_backward_ex", "f3s_attention_fwd", "f3s_attention_backward_saved", "f3s_attention_host_async", "f3s_default_split_chunks",
             "f3s_status_string", "f3s_last_error", "f3s_launch_count"]
 
 
@@ -309,6 +312,43 @@ def attention_backward(p: Plan, Q, K, V, dO, *, scale: float, stream=None, varia
                                           dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(), float(scale), H, d,
                                           _dtype_code(Q), BACKWARD_VARIANTS[variant], _stream(stream)),
            "f3s_attention_backward")
+    return dQ, dK, dV
+
+
+def attention_fwd(p: Plan, Q, K, V, O=None, ml=None, *, scale: float = 1.0, stream=None):
+    """f3s_attention_fwd: O (bitwise as attention()) and the per-row softmax statistics ml
+    [N, H, 2] = (m, l) that attention_backward_saved consumes."""
+    import torch
+    _check_tensors(p, Q, K, V, O, what="f3s_attention_fwd")
+    H, d = Q.shape[1], Q.shape[2]
+    if O is None:
+        O = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
+    if ml is None:
+        ml = torch.empty((Q.shape[0], H, 2), dtype=torch.float32, device=Q.device)
+    elif ml.dtype != torch.float32 or tuple(ml.shape) != (Q.shape[0], H, 2) or not ml.is_contiguous() \
+            or ml.device != Q.device:
+        raise ValueError(f"attention_fwd: ml must be a contiguous float32 [{Q.shape[0]}, {H}, 2] tensor on Q's device")
+    _check(_lib.f3s_attention_fwd(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), O.data_ptr(), ml.data_ptr(),
+                                  float(scale), H, d, _dtype_code(Q), _stream(stream)), "f3s_attention_fwd")
+    return O, ml
+
+
+def attention_backward_saved(p: Plan, Q, K, V, O, ml, dO, *, scale: float, stream=None):
+    """f3s_attention_backward_saved: (dQ, dK, dV) from the saved outputs (O, ml) of attention_fwd."""
+    import torch
+    _check_tensors(p, Q, K, V, dO, what="f3s_attention_backward_saved")
+    _check_tensors(p, Q, K, V, O, what="f3s_attention_backward_saved")
+    H, d = Q.shape[1], Q.shape[2]
+    if ml.dtype != torch.float32 or tuple(ml.shape) != (Q.shape[0], H, 2) or not ml.is_contiguous() \
+            or ml.device != Q.device:
+        raise ValueError("attention_backward_saved: ml must be attention_fwd's float32 [N, H, 2] statistics")
+    dQ = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
+    dK = torch.empty(K.shape, dtype=torch.float32, device=K.device)
+    dV = torch.empty(V.shape, dtype=torch.float32, device=V.device)
+    _check(_lib.f3s_attention_backward_saved(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), O.data_ptr(),
+                                             ml.data_ptr(), dO.data_ptr(), dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(),
+                                             float(scale), H, d, _dtype_code(Q), _stream(stream)),
+           "f3s_attention_backward_saved")
     return dQ, dK, dV
 
 

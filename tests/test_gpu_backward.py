@@ -143,3 +143,56 @@ def test_backward_head_groups(f3s, oracle_mod, dtype, H):
         assert np.array_equal(a, b)
         _close(a, r)
         _close(a, c.astype(np.float64))
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("graph,d,H", [("power", 64, 2), ("power", 128, 1), ("molecules", 64, 4), ("ragged", 64, 3)])
+def test_training_forward_and_saved_backward(f3s, oracle_mod, dtype, graph, d, H):
+    """f3s_attention_fwd gives f3s_attention's O bit for bit plus (m, l) with LSE = m + log2(l) the
+    oracle's log-sum-exp; f3s_attention_backward_saved on those saved outputs meets the oracle
+    backward's bar (and matches the recomputing backward within it)."""
+    import torch
+    if graph == "power":
+        csr = fi.chung_lu(3000, 40000, gamma=2.1, max_deg=1500, seed=5 + d)
+    elif graph == "molecules":
+        csr = fi.molecules(300, 25, 150, seed=H)
+    else:
+        csr = fi.random_csr(1000 + 7, 1000 + 7, 0, 40, keep_dups=True, unsorted=True, seed=d + H)
+    n = csr.n_rows
+    Qb, Kb, Vb = make_qkv(n, csr.n_cols, H, d, dtype, seed=31)
+    G = np.random.default_rng(3 * d + H).standard_normal((n, H, d)).astype(np.float32)
+    scale = 1.0 / np.sqrt(d)
+    rp, ci = csr_to_dev(csr)
+    p = f3s.plan(rp, ci, n)
+    Q, K, V = to_dev(Qb, dtype), to_dev(Kb, dtype), to_dev(Vb, dtype)
+    O, ml = f3s.attention_fwd(p, Q, K, V, scale=scale)
+    O_ref = f3s.attention(p, Q, K, V, scale=scale)
+    torch.cuda.synchronize()
+    assert torch.equal(O, O_ref)
+    # statistics: LSE_i = m + log2(l) = log2 sum_j exp(scale q_i.k_j) over the row's distinct columns
+    qd, kd = decode(Qb, dtype), decode(Kb, dtype)
+    mlh = ml.cpu().numpy().astype(np.float64)
+    rows = np.random.default_rng(1).choice(n, size=min(n, 300), replace=False)
+    for i in rows:
+        cols = np.unique(csr.col_idx[csr.row_ptr[i]:csr.row_ptr[i + 1]])
+        for h in range(H):
+            if cols.size == 0:
+                assert mlh[i, h, 1] == 0.0
+                continue
+            s = scale * (kd[cols, h, :] @ qd[i, h, :])
+            lse2 = (s.max() + np.log(np.exp(s - s.max()).sum())) / np.log(2.0)
+            got = mlh[i, h, 0] + np.log2(mlh[i, h, 1])
+            # l sums the P values rounded to the input dtype (reading c7): relative error <= u, the
+            # unit roundoff (2^-11 fp16, 2^-8 bf16), so |log2 error| <= log2(1 + u) + fp32 noise
+            u = 2.0 ** -11 if dtype == "fp16" else 2.0 ** -8
+            assert abs(got - lse2) <= np.log2(1 + u) + 1e-4 * max(1.0, abs(lse2)), (i, h, got, lse2)
+    dO = torch.from_numpy(G).cuda()
+    saved = [x.cpu().numpy() for x in f3s.attention_backward_saved(p, Q, K, V, O, ml, dO, scale=scale)]
+    again = [x.cpu().numpy() for x in f3s.attention_backward_saved(p, Q, K, V, O, ml, dO, scale=scale)]
+    recomputed = [x.cpu().numpy() for x in f3s.attention_backward(p, Q, K, V, dO, scale=scale)]
+    ref = oracle_mod.attention_backward(csr.row_ptr, csr.col_idx, qd, kd, decode(Vb, dtype), G.astype(np.float64),
+                                        scale=scale)
+    for a, b, c, r in zip(saved, again, recomputed, ref):
+        assert np.array_equal(a, b)
+        _close(a, r)
+        _close(a, c.astype(np.float64))

@@ -24,7 +24,8 @@ def main():
     ap.add_argument("--config", default="arxiv")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--variant", default="tc", choices=["tc", "simt"])
+    ap.add_argument("--variant", default="tc", choices=["tc", "simt", "saved"],
+                    help="saved: f3s_attention_backward_saved on the outputs of f3s_attention_fwd (no recomputed forward)")
     a = ap.parse_args()
     import torch
     from f3s_inputs import configs
@@ -39,16 +40,32 @@ def main():
     H, d = Q.shape[1], Q.shape[2]
     g = torch.Generator(device="cuda").manual_seed(1)
     dO = torch.randn(Q.shape, generator=g, device="cuda", dtype=torch.float32)
+    if a.variant == "saved":
+        O, ml = f3s.attention_fwd(p, Q, K, V, scale=w.scale)
+        step = lambda: f3s.attention_backward_saved(p, Q, K, V, O, ml, dO, scale=w.scale)
+    else:
+        step = lambda: f3s.attention_backward(p, Q, K, V, dO, scale=w.scale, variant=a.variant)
     for _ in range(a.warmup):
-        f3s.attention_backward(p, Q, K, V, dO, scale=w.scale, variant=a.variant)
+        step()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(a.steps):
-        f3s.attention_backward(p, Q, K, V, dO, scale=w.scale, variant=a.variant)
+        step()
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / a.steps
+    fwd_ms = None
+    if a.variant == "saved":  # the training forward alone, for the fwd + bwd step time
+        O2, ml2 = torch.empty_like(O), torch.empty_like(ml)
+        for _ in range(3):
+            f3s.attention_fwd(p, Q, K, V, O2, ml2, scale=w.scale)
+        s.record()
+        for _ in range(a.steps):
+            f3s.attention_fwd(p, Q, K, V, O2, ml2, scale=w.scale)
+        e.record()
+        torch.cuda.synchronize()
+        fwd_ms = s.elapsed_time(e) / a.steps
     info = p.info()
     nnz, N, Nc = info["nnz"], csr.n_rows, csr.n_cols
     flops = 8.0 * nnz * d * H
@@ -63,8 +80,11 @@ def main():
                       "roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                    "frac": round(gbs / peaks["hbm_gbs"], 4), "alg_bytes_per_call": int(alg)},
                       "variant": a.variant,
-                      "kernels": ("forward (partial) + k_bwd_prep + k_bwd_sm100 rows + k_bwd_sm100 columns (tcgen05)"
-                                  if a.variant == "tc" else "k_bwd_rows + k_bwd_cols (CUDA cores)")}))
+                      "training_forward_ms": None if fwd_ms is None else round(fwd_ms, 4),
+                      "kernels": {"tc": "forward (partial) + k_bwd_prep + k_bwd_sm100 rows + k_bwd_sm100 columns (tcgen05)",
+                                  "saved": "k_bwd_prep + k_bwd_sm100 rows + k_bwd_sm100 columns (tcgen05); O, (m, l) saved "
+                                           "by f3s_attention_fwd",
+                                  "simt": "k_bwd_rows + k_bwd_cols (CUDA cores)"}[a.variant]}))
 
 
 if __name__ == "__main__":
