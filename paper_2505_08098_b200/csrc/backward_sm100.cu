@@ -55,7 +55,8 @@ struct BCfg {
     // S/dP TMEM buffers and P/dS shared tiles, chunk slots, per-item tile slots (X and Y: 16 x D
     // each): fewer at d = 128 so that two 32 KB tile slots per gathered operand still fit
     static constexpr int kSB = (D == 128 || HG == 4) ? 2 : 4;
-    static constexpr int kNS = D == 128 ? 12 : 16;
+    // (d = 128 columns: 10 slots leave room for a fifth gathered tile, the third Q_c slot)
+    static constexpr int kNS = D == 128 ? (PASS == 1 ? 10 : 12) : 16;
     static constexpr int kNQ = (D == 128 || HG == 4) ? 2 : 4;
     static constexpr int kXBytes = 16 * kRowPitch * HG;  // HG head tiles of 16 x D
     static constexpr int kQBytes = 2 * kXBytes;
@@ -71,8 +72,9 @@ struct BCfg {
     // gathered tile slots: both operands live until MMA2 in the column pass; in the row pass V_c is
     // free after MMA1, so K_c (read by MMA1 and MMA2) gets the remaining slots
     static constexpr int kSlotsAll = (227 * 1024 - kFixed) / kTile;
+    // (the loaders issue a chunk's A1 rows before they wait for its A2 slot, so an odd slot goes to A1)
     static constexpr int kN2 = PASS == 0 ? 2 : kSlotsAll / 2;
-    static constexpr int kN1 = PASS == 0 ? (kSlotsAll - 2 < 16 ? kSlotsAll - 2 : 16) : kSlotsAll / 2;
+    static constexpr int kN1 = PASS == 0 ? (kSlotsAll - 2 < 16 ? kSlotsAll - 2 : 16) : kSlotsAll - kSlotsAll / 2;
     static_assert(kN1 >= 2 && kN2 >= 2 && kN1 <= 16 && kN2 <= 16, "tile slots per operand");
     static constexpr int oT1 = 0, oT2 = kN1 * kTile;
     static constexpr int oQ = (kN1 + kN2) * kTile;
@@ -311,7 +313,6 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             // HG = 1: tile row r = compacted column r.  HG = 4: tile row 32g + r = column r of head h + g
             const int ops = HG == 1 ? (rows + kRowsPerOp - 1) / kRowsPerOp : C::kMaxRows / kRowsPerOp;
             mbar_wait(bar(B::t1free(t1)), ((seq / C::kN1) & 1) ^ 1);
-            mbar_wait(bar(B::t2free(t2)), ((seq / C::kN2) & 1) ^ 1);
             int64_t jj[kIters];
             uint32_t dst[kIters];
             int rr[kIters];
@@ -339,6 +340,9 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                     }
             }
             cp_async_mbar_arrive(f1);
+            // the A2 slot is awaited only now: with more A1 than A2 slots the A1 rows of the next
+            // chunk are already on their way while the A2 slot drains
+            mbar_wait(bar(B::t2free(t2)), ((seq / C::kN2) & 1) ^ 1);
 #pragma unroll
             for (int i = 0; i < kIters; ++i)
                 if (ok[i]) cp_async_16(d2 + dst[i], b2 + jj[i] * ld_bytes + (HG == 1 ? 0 : (int64_t)(rr[i] >> 5) * C::RB));
@@ -353,18 +357,18 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         for (int32_t n1 = 0;; ++n1) {
             const int s = n1 % C::kNS, b = n1 % C::kSB;
             mbar_wait(bar(B::a1full(s)), (n1 / C::kNS) & 1);
-            mbar_wait(bar(B::a2full(s)), (n1 / C::kNS) & 1);
             const Slot& sl = slots[s];
             const int rows = sl.rows, flags = sl.flags, qslot = sl.qslot;
             if (rows < 0) break;
             mbar_wait(bar(B::sfree(b)), ((n1 / C::kSB) & 1) ^ 1);
             if (flags & 1) mbar_wait(bar(B::xyfull(qslot)), (flags >> 2) & 1);
             tc_fence_after();
+            // S^T from A1 as soon as A1 has landed, then dP^T once A2 has (the loaders issue A1 first)
+            const uint64_t a1 = dA + ((sb + C::oT1 + (n1 % C::kN1) * C::kTile) >> 4);
+            const uint64_t a2 = dA + ((sb + C::oT2 + (n1 % C::kN2) * C::kTile) >> 4);
+            const uint64_t bx = dX + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
+            const uint64_t by = dX + ((sb + C::oQ + qslot * C::kQBytes + C::kXBytes) >> 4);
             if (rows > 0) {
-                const uint64_t a1 = dA + ((sb + C::oT1 + (n1 % C::kN1) * C::kTile) >> 4);
-                const uint64_t a2 = dA + ((sb + C::oT2 + (n1 % C::kN2) * C::kTile) >> 4);
-                const uint64_t bx = dX + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
-                const uint64_t by = dX + ((sb + C::oQ + qslot * C::kQBytes + C::kXBytes) >> 4);
 #pragma unroll
                 for (int g = 0; g < HG; ++g)  // HG > 1: head g against its own X/Y tile; lanes 32g.. are read
 #pragma unroll
@@ -372,6 +376,17 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                         const uint32_t ao = ((kk >> 2) * 1024 + (kk & 3) * 32) >> 4;
                         const uint32_t bo = (g * 16 * C::kRowPitch + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
                         mma_f16_ss_warp(tmem + C::kTmS + (b * HG + g) * 16, a1 + ao, bx + bo, idesc1, kk > 0 ? 1u : 0u);
+                    }
+            }
+            mbar_wait(bar(B::a2full(s)), (n1 / C::kNS) & 1);
+            tc_fence_after();
+            if (rows > 0) {
+#pragma unroll
+                for (int g = 0; g < HG; ++g)
+#pragma unroll
+                    for (int kk = 0; kk < C::RB / 32; ++kk) {
+                        const uint32_t ao = ((kk >> 2) * 1024 + (kk & 3) * 32) >> 4;
+                        const uint32_t bo = (g * 16 * C::kRowPitch + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
                         mma_f16_ss_warp(tmem + C::kTmP + (b * HG + g) * 16, a2 + ao, by + bo, idesc1, kk > 0 ? 1u : 0u);
                     }
             }
