@@ -56,7 +56,10 @@ struct BCfg {
     // each): fewer at d = 128 so that two 32 KB tile slots per gathered operand still fit
     static constexpr int kSB = (D == 128 || HG == 4) ? 2 : 4;
     // (d = 128 columns: 10 slots leave room for a fifth gathered tile, the third Q_c slot)
-    static constexpr int kNS = D == 128 ? (PASS == 1 ? 10 : 12) : 16;
+    static constexpr int kNS = D == 128 ? (PASS == 1 ? 10 : 12) : HG == 4 ? 8 : 16;
+    // epilogue warpgroups: head groups (one chunk per item, 4 heads of fp32 gradients per item) use
+    // two on alternate items (accumulator buffer e), each with its own staging tiles
+    static constexpr int kEpiWGs = HG == 4 ? 2 : 1;
     static constexpr int kNQ = (D == 128 || HG == 4) ? 2 : 4;
     static constexpr int kXBytes = 16 * kRowPitch * HG;  // HG head tiles of 16 x D
     static constexpr int kQBytes = 2 * kXBytes;
@@ -64,10 +67,12 @@ struct BCfg {
     static constexpr int kPBytes = 16 * kMaxRows * 2;
     static constexpr int kNG = PASS == 0 ? 1 : 2;    // gradient accumulators: dQ; dV, dK
     static constexpr int kOBytes = 16 * D * 4 * HG;  // one [16 x HG*D] fp32 staging tile
-    static constexpr int kScal = PASS == 0 ? 16 * HG : 128;  // LSE / D values per chunk slot
-    static constexpr int kSlotBytes = 32 + kMaxRows * 4 + kMaxRows * 2 + 2 * kScal * 4;
+    // (LSE, D) pairs per chunk slot: rows, the window's 16 per head; columns none (the elementwise
+    // warps load the gathered rows' pairs themselves, off the loaders' cp.async path)
+    static constexpr int kScal = PASS == 0 ? 16 * HG : 0;
+    static constexpr int kSlotBytes = 32 + kMaxRows * 4 + kMaxRows * 2 + kScal * 8;
     static constexpr int kNumBars = 5 * kNS + 2 * kNQ + 4 * kSB + 4 + 2 * 16;
-    static constexpr int kFixed = kNQ * kQBytes + kSB * kNT * kPBytes + kNG * kOBytes + kNS * kSlotBytes +
+    static constexpr int kFixed = kNQ * kQBytes + kSB * kNT * kPBytes + kEpiWGs * kNG * kOBytes + kNS * kSlotBytes +
                                   kNumBars * 8 + 64 + 16;
     // gathered tile slots: both operands live until MMA2 in the column pass; in the row pass V_c is
     // free after MMA1, so K_c (read by MMA1 and MMA2) gets the remaining slots
@@ -80,7 +85,7 @@ struct BCfg {
     static constexpr int oQ = (kN1 + kN2) * kTile;
     static constexpr int oP = oQ + kNQ * kQBytes;
     static constexpr int oOst = oP + kSB * kNT * kPBytes;
-    static constexpr int oSlot = oOst + kNG * kOBytes;
+    static constexpr int oSlot = oOst + kEpiWGs * kNG * kOBytes;
     static constexpr int oRec = oSlot + kNS * kSlotBytes;  // int4 [2] accumulator records
     static constexpr int oBar = oRec + 64;
     static constexpr int oTmem = oBar + kNumBars * 8;
@@ -93,7 +98,7 @@ struct BCfg {
     static_assert(kTmUsed <= 512, "TMEM columns");
     static constexpr int kLoaderWarps = D == 128 ? 8 : 6;
     static constexpr int kLoader0 = 3, kEw0 = kLoader0 + kLoaderWarps, kEpi0 = kEw0 + 8;
-    static constexpr int kThreads = 32 * (kEpi0 + 4);
+    static constexpr int kThreads = 32 * (kEpi0 + 4 * kEpiWGs);
     static constexpr int kBatch = 8;
 };
 
@@ -120,8 +125,12 @@ template <int kScal> struct __align__(16) BSlot {
     int32_t rw, head, rows, qslot, flags, pad0, pad1, pad2;
     int32_t cols[128];
     uint16_t masks[128];
-    float lse[kScal];  // log2-domain LSE of the chunk's query rows (rows: the window's 16; cols: per entry)
-    float dd[kScal];   // D = dO . O of the same rows
+    float2 ld[kScal];  // (LSE in log2 units, D = dO . O) of the window's 16 query rows per head (rows pass)
+};
+template <> struct __align__(16) BSlot<0> {
+    int32_t rw, head, rows, qslot, flags, pad0, pad1, pad2;
+    int32_t cols[128];
+    uint16_t masks[128];
 };
 
 template <typename T> __device__ __forceinline__ uint32_t bpack2(float lo, float hi);
@@ -147,7 +156,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             const int4* __restrict__ meta, const int32_t* __restrict__ kcols, const uint16_t* __restrict__ kmasks,
             int32_t* __restrict__ counter, int32_t n_items, int32_t heavy_items, int32_t H,
             const uint8_t* __restrict__ A1g, const uint8_t* __restrict__ A2g, int64_t ld_bytes,
-            const float* __restrict__ lse_t, const float* __restrict__ dd_t, int64_t nq16, float scale_log2,
+            const float2* __restrict__ ld_t, int64_t nq16, float scale_log2,
             float g2scale, float g1scale) {
     using C = BCfg<D, PASS, HG>;
     using B = BBars<D, PASS, HG>;
@@ -257,18 +266,16 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                         sl.flags = (j == 0 ? 1 : 0) | (j == nch - 1 ? 2 : 0) | (qph << 2);
                         const uint32_t fb = bar(B::idxfull(s));
                         const uint32_t r8 = (uint32_t)((rows + 7) & ~7);
-                        const uint32_t scal = PASS == 0 ? 2u * 64u * HG : 0u;  // rows: the window's 16 LSE and D per head
+                        const uint32_t scal = PASS == 0 ? 128u * HG : 0u;  // rows: the window's 16 (LSE, D) per head
                         mbar_arrive_expect_tx(fb, (rows > 0 ? r8 * 6u : 0u) + scal);
                         if (rows > 0) {
                             bulk_g2s(smem_u32(sl.cols), kcols + cb8 + chunk_rows * j, r8 * 4u, fb);
                             bulk_g2s(smem_u32(sl.masks), kmasks + cb8 + chunk_rows * j, r8 * 2u, fb);
                         }
-                        if (PASS == 0) {
+                        if constexpr (PASS == 0) {
 #pragma unroll
-                            for (int g = 0; g < HG; ++g) {
-                                bulk_g2s(smem_u32(sl.lse + 16 * g), lse_t + (h + g) * nq16 + 16 * (int64_t)k, 64u, fb);
-                                bulk_g2s(smem_u32(sl.dd + 16 * g), dd_t + (h + g) * nq16 + 16 * (int64_t)k, 64u, fb);
-                            }
+                            for (int g = 0; g < HG; ++g)
+                                bulk_g2s(smem_u32(sl.ld + 16 * g), ld_t + (h + g) * nq16 + 16 * (int64_t)k, 128u, fb);
                         }
                     }
                     ++seq;
@@ -286,7 +293,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         }
         __syncwarp();
     } else if (warp >= C::kLoader0 && warp < C::kLoader0 + C::kLoaderWarps) {
-        // ===== loaders: the chunk's A1 and A2 rows (+ cols: their LSE and D) =====================
+        // ===== loaders: the chunk's A1 and A2 rows ===============================================
         constexpr int kPieces = C::RB / 16;
         constexpr int kRowsPerOp = 32 / kPieces;
         constexpr int kIters = (C::kMaxRows / kRowsPerOp + C::kLoaderWarps - 1) / C::kLoaderWarps;
@@ -330,15 +337,6 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 #pragma unroll
             for (int i = 0; i < kIters; ++i)
                 if (ok[i]) cp_async_16(d1 + dst[i], b1 + jj[i] * ld_bytes + (HG == 1 ? 0 : (int64_t)(rr[i] >> 5) * C::RB));
-            if (PASS == 1) {  // the gathered query rows' LSE and D (one lane per tile row)
-#pragma unroll
-                for (int i = 0; i < kIters; ++i)
-                    if (ok[i] && piece == 0) {
-                        const int64_t hh = h + (HG == 1 ? 0 : (rr[i] >> 5));
-                        cp_async_4(smem_u32(&sl.lse[rr[i]]), lse_t + hh * nq16 + jj[i]);
-                        cp_async_4(smem_u32(&sl.dd[rr[i]]), dd_t + hh * nq16 + jj[i]);
-                    }
-            }
             cp_async_mbar_arrive(f1);
             // the A2 slot is awaited only now: with more A1 than A2 slots the A1 rows of the next
             // chunk are already on their way while the A2 slot drains
@@ -410,12 +408,15 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             if (PASS == 1) mbar_wait(bar(B::a2full(s)), (n2 / C::kNS) & 1);
             const Slot& sl = slots[s];
             const int rows = sl.rows, flags = sl.flags, rw = sl.rw, hd = sl.head;
-            if (rows < 0) {  // tell the epilogue to stop (its next record)
-                mbar_wait(bar(B::gempty(a)), ((item >> 1) & 1) ^ 1);
-                if (lane == 0) {
-                    rec[a] = make_int4(-1, 0, 0, 0);
-                    mbar_arrive(bar(B::gfull(a)));
-                    mbar_arrive(bar(B::gfull(a)));
+            if (rows < 0) {  // tell the epilogue warpgroup(s) to stop (their next records)
+                for (int e = 0; e < C::kEpiWGs; ++e) {
+                    const int it = item + e, ae = it & 1;
+                    mbar_wait(bar(B::gempty(ae)), ((it >> 1) & 1) ^ 1);
+                    if (lane == 0) {
+                        rec[ae] = make_int4(-1, 0, 0, 0);
+                        mbar_arrive(bar(B::gfull(ae)));
+                        mbar_arrive(bar(B::gfull(ae)));
+                    }
                 }
                 break;
             }
@@ -478,12 +479,11 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             const Slot& sl = slots[s];
             const int rows = sl.rows;
             if (rows < 0) break;
-            if (PASS == 1) mbar_wait(bar(B::a1full(s)), (seq / C::kNS) & 1);  // the gathered LSE and D
             const uint32_t mask = col < rows ? (uint32_t)sl.masks[col] : 0u;
-            float lse_p = 0.f, dd_p = 0.f;
-            if (PASS == 1) {
-                lse_p = sl.lse[p];
-                dd_p = sl.dd[p];
+            float2 ld_p = make_float2(0.f, 0.f);
+            if constexpr (PASS == 1) {  // the (LSE, D) of this lane's gathered query row (L2; its
+                                        // latency hides behind the gathers and MMA1)
+                if (col < rows) ld_p = __ldg(ld_t + (int64_t)(sl.head + hb) * nq16 + sl.cols[col]);
             }
             mbar_wait(bar(B::sfull(b)), bph);
             tc_fence_after();
@@ -496,8 +496,11 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             float pr[16], ds[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                const float l = PASS == 0 ? sl.lse[16 * hb + i] : lse_p;
-                const float dd = PASS == 0 ? sl.dd[16 * hb + i] : dd_p;
+                float l = ld_p.x, dd = ld_p.y;
+                if constexpr (PASS == 0) {
+                    l = sl.ld[16 * hb + i].x;
+                    dd = sl.ld[16 * hb + i].y;
+                }
                 const float pv = ((mask >> i) & 1u) ? ex2(fmaf(x[i], scale_log2, -l)) : 0.f;
                 pr[i] = pv;
                 ds[i] = pv * (y[i] - dd);
@@ -520,8 +523,10 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         const uint32_t tl = (uint32_t)(32 * q) << 16;
         const bool has = D == 128 || lane < 16;
         const int f = D == 128 ? 32 * q + lane : 16 * q + lane;  // accumulator lane -> feature
-        const bool lead = threadIdx.x == 32 * C::kEpi0;
-        for (int32_t item = 0;; ++item) {
+        const int e = (warp - C::kEpi0) >> 2;  // epilogue warpgroup: items e, e + kEpiWGs, ..
+        const bool lead = threadIdx.x == 32 * (C::kEpi0 + 4 * e);
+        const uint32_t ost = C::oOst + e * C::kNG * C::kOBytes;
+        for (int32_t item = e;; item += C::kEpiWGs) {
             const int a = item & 1;
             mbar_wait(bar(B::gfull(a)), (item >> 1) & 1);
             const int4 r = rec[a];
@@ -529,8 +534,8 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             tc_fence_after();
             const bool nz = r.z != 0;  // an item with no entries has an untouched accumulator: zeros
             if (lead) bulk_wait_group_read<0>();
-            named_bar_sync(3, 128);
-            float* o1 = reinterpret_cast<float*>(smem + C::oOst);
+            named_bar_sync(3 + e, 128);
+            float* o1 = reinterpret_cast<float*>(smem + ost);
             float* o2 = o1 + 16 * D * HG;
 #pragma unroll 1
             for (int g = 0; g < HG; ++g) {  // [16 x HG*D] tiles: head g in columns g*D ..
@@ -549,10 +554,10 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             tc_fence_before();
             mbar_arrive(bar(B::gempty(a)));
             fence_proxy_async_smem();
-            named_bar_sync(3, 128);
+            named_bar_sync(3 + e, 128);
             if (lead) {
-                tma_store_2d(&tmG1, sb + C::oOst, r.y * D, 16 * r.x);
-                if (PASS == 1) tma_store_2d(&tmG2, sb + C::oOst + C::kOBytes, r.y * D, 16 * r.x);
+                tma_store_2d(&tmG1, sb + ost, r.y * D, 16 * r.x);
+                if (PASS == 1) tma_store_2d(&tmG2, sb + ost + C::kOBytes, r.y * D, 16 * r.x);
                 bulk_commit_group();
             }
         }
@@ -566,43 +571,63 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     }
 }
 
-// LSE (log2 units incl. scale), D = dO . O and dO in the input dtype, from the forward's partial
-// outputs (unnormalised O, (m, l)) or the saved outputs of f3s_attention_fwd (normalized: O / l,
-// (m, l)); one warp per (row, head).  Head-major LSE / D ([H][nq16]).
+// (LSE, D) per row and head -- LSE_i = m_i + log2(l_i) in log2 units incl. scale (+inf for an empty
+// row: p = 0), D_i = dO_i . O_i -- and dO in the input dtype, from the forward's partial outputs
+// (unnormalised O, (m, l)) or the saved outputs of f3s_attention_fwd (normalized: O / l, (m, l)).
+// D / 4 lanes per (row, head), 16-byte loads, kU (row, head) pairs per group in flight; head-major
+// output ld_t[h][nq16].
 template <int D, typename T>
 __global__ void __launch_bounds__(256) k_bwd_prep(const float* __restrict__ Op, const float2* __restrict__ ml,
                                                   const float* __restrict__ dO, int64_t n_rows, int32_t H,
-                                                  int64_t nq16, float* __restrict__ lse_t, float* __restrict__ dd_t,
-                                                  T* __restrict__ dO16, int32_t normalized) {
-    constexpr int E = D / 32;
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t rh = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; rh < n_rows * H; rh += nw) {
-        const int64_t i = rh / H;
-        const int h = (int)(rh - i * H);
-        const float2 v = ml[rh];
-        const float inv = normalized ? 1.f : v.y > 0.f ? 1.f / v.y : 0.f;  // saved O is already O / l
-        float acc = 0.f;
+                                                  int64_t nq16, float2* __restrict__ ld_t, T* __restrict__ dO16,
+                                                  int32_t normalized) {
+    constexpr int L = D / 4, kU = 4;
+    const int sub = threadIdx.x % L;
+    const int64_t ng = (int64_t)gridDim.x * (blockDim.x / L);
+    const int64_t gid = (int64_t)blockIdx.x * (blockDim.x / L) + threadIdx.x / L;
+    const int64_t total = n_rows * H;
+    for (int64_t r0 = gid; r0 < total; r0 += ng * kU) {
+        float4 o[kU], g[kU];
+        float2 v[kU];
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const int64_t o = rh * D + lane * E + e;
-            const float g = dO[o];
-            acc = fmaf(g, Op[o] * inv, acc);
-            if constexpr (std::is_same<T, __half>::value) dO16[o] = __float2half_rn(g);
-            else dO16[o] = __float2bfloat16_rn(g);
+        for (int u = 0; u < kU; ++u) {
+            const int64_t rh = r0 + u * ng;
+            if (rh < total) {
+                o[u] = __ldg(reinterpret_cast<const float4*>(Op + rh * D) + sub);
+                g[u] = __ldg(reinterpret_cast<const float4*>(dO + rh * D) + sub);
+                v[u] = __ldg(ml + rh);
+            }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-            lse_t[h * nq16 + i] = v.y > 0.f ? v.x + __log2f(v.y) : INFINITY;  // empty row: p = 0
-            dd_t[h * nq16 + i] = acc;
+        for (int u = 0; u < kU; ++u) {
+            const int64_t rh = r0 + u * ng;
+            const float inv = normalized ? 1.f : v[u].y > 0.f ? 1.f / v[u].y : 0.f;  // saved O is already O / l
+            float acc = fmaf(g[u].x, o[u].x * inv, fmaf(g[u].y, o[u].y * inv, fmaf(g[u].z, o[u].z * inv, g[u].w * (o[u].w * inv))));
+#pragma unroll
+            for (int off = L / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (rh < total) {
+                uint2 pk;
+                if constexpr (std::is_same<T, __half>::value) {
+                    pk.x = pack_f16x2(g[u].x, g[u].y);
+                    pk.y = pack_f16x2(g[u].z, g[u].w);
+                } else {
+                    pk.x = pack_bf16x2(g[u].x, g[u].y);
+                    pk.y = pack_bf16x2(g[u].z, g[u].w);
+                }
+                reinterpret_cast<uint2*>(dO16 + rh * D)[sub] = pk;
+                if (sub == 0) {
+                    const int64_t i = rh / H;
+                    const int h = (int)(rh - i * H);
+                    ld_t[h * nq16 + i] = make_float2(v[u].y > 0.f ? v[u].x + __log2f(v[u].y) : INFINITY, acc);
+                }
+            }
         }
     }
 }
 
 template <int D, typename T, int PASS, int HG>
 f3s_status launch_pass_hg(const Plan& p, const void* X, const void* Y, const void* A1, const void* A2, float* G1,
-                          float* G2, const float* lse_t, const float* dd_t, int64_t nq16, int H, float scale,
+                          float* G2, const float2* ld_t, int64_t nq16, int H, float scale,
                           int sms, cudaStream_t stream) {
     using C = BCfg<D, PASS, HG>;
     if (p.num_rw == 0) return F3S_OK;
@@ -639,7 +664,7 @@ f3s_status launch_pass_hg(const Plan& p, const void* X, const void* Y, const voi
         k_bwd_sm100<D, T, PASS, HG><<<grid, C::kThreads, C::kSmemBytes, stream>>>(
             mx, my, mg1, mg2, p.meta_lpt, p.kcols, p.kmasks, reinterpret_cast<int32_t*>(scratch), (int32_t)n_items64,
             (int32_t)std::min<int64_t>((int64_t)p.n_heavy_lpt * (H / HG), 0x7FFFFFFF), H,
-            static_cast<const uint8_t*>(A1), static_cast<const uint8_t*>(A2), ld * 2, lse_t, dd_t, nq16,
+            static_cast<const uint8_t*>(A1), static_cast<const uint8_t*>(A2), ld * 2, ld_t, nq16,
             scale * 1.4426950408889634f, scale, PASS == 0 ? scale : 1.f);
         count_launch();
         err = cudaGetLastError();
@@ -653,13 +678,13 @@ f3s_status launch_pass_hg(const Plan& p, const void* X, const void* Y, const voi
 // head groups of 4 when d = 64, H % 4 == 0 and every window of the pass's plan has <= 32 columns
 template <int D, typename T, int PASS>
 f3s_status launch_pass(const Plan& p, const void* X, const void* Y, const void* A1, const void* A2, float* G1,
-                       float* G2, const float* lse_t, const float* dd_t, int64_t nq16, int H, float scale,
+                       float* G2, const float2* ld_t, int64_t nq16, int H, float scale,
                        int sms, cudaStream_t stream) {
     if constexpr (D == 64) {
         if (H % 4 == 0 && p.max_width <= 32)
-            return launch_pass_hg<D, T, PASS, 4>(p, X, Y, A1, A2, G1, G2, lse_t, dd_t, nq16, H, scale, sms, stream);
+            return launch_pass_hg<D, T, PASS, 4>(p, X, Y, A1, A2, G1, G2, ld_t, nq16, H, scale, sms, stream);
     }
-    return launch_pass_hg<D, T, PASS, 1>(p, X, Y, A1, A2, G1, G2, lse_t, dd_t, nq16, H, scale, sms, stream);
+    return launch_pass_hg<D, T, PASS, 1>(p, X, Y, A1, A2, G1, G2, ld_t, nq16, H, scale, sms, stream);
 }
 
 struct Scratch2 {
@@ -689,26 +714,26 @@ f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, c
     char* base = static_cast<char*>(sc.p);
     const float* Op = O_saved;
     const float* ml = ml_saved;
-    float* lse_t = reinterpret_cast<float*>(base);
+    float2* ld_t = reinterpret_cast<float2*>(base);
     if (!saved) {
         // 1. the forward's (m, l) and unnormalised O
         float* op = reinterpret_cast<float*>(base);
         float* mlp = op + nd;
-        lse_t = mlp + 2 * nh2;
+        ld_t = reinterpret_cast<float2*>(mlp + 2 * nh2);
         AttnArgs a{&p, Q, K, V, op, scale, H, D, std::is_same<T, __half>::value ? F3S_FP16 : F3S_BF16, true, stream};
         a.ml_out = mlp;
         if ((st = launch_attention_sm100(a)) != F3S_OK) return st;
         Op = op;
         ml = mlp;
     }
-    float* dd_t = lse_t + H * nq16;
-    T* dO16 = reinterpret_cast<T*>(dd_t + H * nq16);
-    k_bwd_prep<D, T><<<(int)std::min<int64_t>((n * H + 7) / 8, (int64_t)sms * 16), 256, 0, stream>>>(
-        Op, reinterpret_cast<const float2*>(ml), dO, n, H, nq16, lse_t, dd_t, dO16, saved ? 1 : 0);
+    T* dO16 = reinterpret_cast<T*>(ld_t + H * nq16);
+    const int64_t per_block = 4 * (256 / (D / 4));  // (row, head) pairs one block covers per pass
+    k_bwd_prep<D, T><<<(int)std::min<int64_t>((n * H + per_block - 1) / per_block, (int64_t)sms * 8), 256, 0, stream>>>(
+        Op, reinterpret_cast<const float2*>(ml), dO, n, H, nq16, ld_t, dO16, saved ? 1 : 0);
     count_launch();
     F3S_CUDA_TRY(cudaGetLastError());
     // 2. rows: dQ
-    if ((st = launch_pass<D, T, 0>(p, Q, dO16, K, V, dQ, nullptr, lse_t, dd_t, nq16, H, scale, sms, stream)) != F3S_OK)
+    if ((st = launch_pass<D, T, 0>(p, Q, dO16, K, V, dQ, nullptr, ld_t, nq16, H, scale, sms, stream)) != F3S_OK)
         return st;
     // 3. columns: dV (G1), dK (G2) over A^T
     if (tp.n_rows > 0 && tp.nnz == 0) {
@@ -716,7 +741,7 @@ f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, c
         F3S_CUDA_TRY(cudaMemsetAsync(dV, 0, sizeof(float) * (size_t)tp.n_rows * H * D, stream));
         return F3S_OK;
     }
-    return launch_pass<D, T, 1>(tp, K, V, Q, dO16, dV, dK, lse_t, dd_t, nq16, H, scale, sms, stream);
+    return launch_pass<D, T, 1>(tp, K, V, Q, dO16, dV, dK, ld_t, nq16, H, scale, sms, stream);
 }
 
 }  // namespace
