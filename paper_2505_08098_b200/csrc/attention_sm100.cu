@@ -478,17 +478,25 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const uint64_t a0 = dK + ((sb + C::oK + (n1 % C::kNK) * C::kMaxRowsBytes) >> 4);
                 const uint64_t b0 = dQ + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
                 if (rows > 0 && !(expt & 4)) {
-                    // HG > 1: one M = 128 MMA group per head g against its own Q tile into its own
-                    // S^T buffer; only lanes 32g .. 32g+31 (head g's tile rows) are read back
+                    if constexpr (HG > 1) {
+                        // head groups (d = 64): the HG Q tiles are one [16 HG x 64] K-major tile, so one
+                        // N = 16 HG MMA per K-step gives S^T of every tile row against every head's
+                        // rows; lanes 32g .. 32g+31 (head g's tile rows) are read back from columns
+                        // 16g .. 16g+15 only -- the products with the other heads' Q are never read
+                        constexpr uint32_t idesc1g = idesc_f16(fmt, 0, 0, 128, 16 * HG);
 #pragma unroll
-                    for (int g = 0; g < HG; ++g)
+                        for (int kk = 0; kk < C::RB / 32; ++kk)
+                            mma_f16_ss_warp(tmem + b * HG * 16, a0 + ((kk * 32) >> 4), b0 + ((kk * 32) >> 4), idesc1g,
+                                            kk > 0 ? 1u : 0u);
+                    } else {
 #pragma unroll
                         for (int kk = 0; kk < C::RB / 32; ++kk) {  // K-steps of 32 bytes
                             const uint64_t ad = a0 + (((kk >> 2) * 1024 + (kk & 3) * 32) >> 4);
-                            const uint64_t bd = b0 + ((g * 16 * C::kRowPitch + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4);
-                            if (EB == 1) mma_f8_ss_warp(tmem + (b * HG + g) * 16, ad, bd, idesc1, kk > 0 ? 1u : 0u);
-                            else mma_f16_ss_warp(tmem + (b * HG + g) * 16, ad, bd, idesc1, kk > 0 ? 1u : 0u);
+                            const uint64_t bd = b0 + (((kk >> 2) * 2048 + (kk & 3) * 32) >> 4);
+                            if (EB == 1) mma_f8_ss_warp(tmem + b * 16, ad, bd, idesc1, kk > 0 ? 1u : 0u);
+                            else mma_f16_ss_warp(tmem + b * 16, ad, bd, idesc1, kk > 0 ? 1u : 0u);
                         }
+                    }
                 }
                 mma_commit_warp(bar(B::sfull(b)));
                 mma_commit_warp(bar(B::ktfree(n1 % C::kNK)));

@@ -349,7 +349,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     } else if (warp == 1) {
         // ===== MMA1: S^T = A1_c . X^T and dP^T = A2_c . Y^T (swap-AB, M = 128, N = 16) =========
         constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
-        constexpr uint32_t idesc1 = idesc_f16(fmt, 0, 0, 128, 16);
+        constexpr uint32_t idesc1 = idesc_f16(fmt, 0, 0, 128, 16 * HG);
         const uint64_t dA = smem_desc_sw128(0, 16, C::kGroupBytes);
         const uint64_t dX = smem_desc_sw128(0, 16, 1024);
         for (int32_t n1 = 0;; ++n1) {
@@ -366,27 +366,25 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             const uint64_t a2 = dA + ((sb + C::oT2 + (n1 % C::kN2) * C::kTile) >> 4);
             const uint64_t bx = dX + ((sb + C::oQ + qslot * C::kQBytes) >> 4);
             const uint64_t by = dX + ((sb + C::oQ + qslot * C::kQBytes + C::kXBytes) >> 4);
+            // HG > 1: the HG head tiles of X (Y) form one [16 HG x 64] K-major tile: one N = 16 HG MMA
+            // per K-step; head g's tile rows (lanes 32g ..) are read back from columns 16g .. only
             if (rows > 0) {
 #pragma unroll
-                for (int g = 0; g < HG; ++g)  // HG > 1: head g against its own X/Y tile; lanes 32g.. are read
-#pragma unroll
-                    for (int kk = 0; kk < C::RB / 32; ++kk) {
-                        const uint32_t ao = ((kk >> 2) * 1024 + (kk & 3) * 32) >> 4;
-                        const uint32_t bo = (g * 16 * C::kRowPitch + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
-                        mma_f16_ss_warp(tmem + C::kTmS + (b * HG + g) * 16, a1 + ao, bx + bo, idesc1, kk > 0 ? 1u : 0u);
-                    }
+                for (int kk = 0; kk < C::RB / 32; ++kk) {
+                    const uint32_t ko = ((kk >> 2) * 1024 + (kk & 3) * 32) >> 4;
+                    const uint32_t bo = ((kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
+                    mma_f16_ss_warp(tmem + C::kTmS + b * HG * 16, a1 + ko, bx + bo, idesc1, kk > 0 ? 1u : 0u);
+                }
             }
             mbar_wait(bar(B::a2full(s)), (n1 / C::kNS) & 1);
             tc_fence_after();
             if (rows > 0) {
 #pragma unroll
-                for (int g = 0; g < HG; ++g)
-#pragma unroll
-                    for (int kk = 0; kk < C::RB / 32; ++kk) {
-                        const uint32_t ao = ((kk >> 2) * 1024 + (kk & 3) * 32) >> 4;
-                        const uint32_t bo = (g * 16 * C::kRowPitch + (kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
-                        mma_f16_ss_warp(tmem + C::kTmP + (b * HG + g) * 16, a2 + ao, by + bo, idesc1, kk > 0 ? 1u : 0u);
-                    }
+                for (int kk = 0; kk < C::RB / 32; ++kk) {
+                    const uint32_t ko = ((kk >> 2) * 1024 + (kk & 3) * 32) >> 4;
+                    const uint32_t bo = ((kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
+                    mma_f16_ss_warp(tmem + C::kTmP + b * HG * 16, a2 + ko, by + bo, idesc1, kk > 0 ? 1u : 0u);
+                }
             }
             mma_commit_warp(bar(B::sfull(b)));
             if (PASS == 0) mma_commit_warp(bar(B::t2free(n1 % C::kN2)));  // rows: V_c is MMA1's alone
