@@ -60,7 +60,9 @@ struct BCfg {
     // epilogue warpgroups: head groups (one chunk per item, 4 heads of fp32 gradients per item) use
     // two on alternate items (accumulator buffer e), each with its own staging tiles
     static constexpr int kEpiWGs = HG == 4 ? 2 : 1;
-    static constexpr int kNQ = (D == 128 || HG == 4) ? 2 : 4;
+    // per-item X/Y tile slots: the next items' tiles are in flight while one item runs (their TMA
+    // latency is exposed with 2 slots and one-chunk items); d = 128 columns: 3 keep five tile slots
+    static constexpr int kNQ = HG == 4 ? 2 : (D == 128 && PASS == 1) ? 3 : 4;
     static constexpr int kXBytes = 16 * kRowPitch * HG;  // HG head tiles of 16 x D
     static constexpr int kQBytes = 2 * kXBytes;
     static constexpr int kNT = PASS == 0 ? 1 : 2;    // 16-bit tiles written per chunk: dS (rows); P, dS (cols)
