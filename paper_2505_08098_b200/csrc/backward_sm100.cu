@@ -100,7 +100,8 @@ struct BCfg {
     static_assert(kTmUsed <= 512, "TMEM columns");
     static constexpr int kLoaderWarps = D == 128 ? 8 : 6;
     static constexpr int kLoader0 = 3, kEw0 = kLoader0 + kLoaderWarps, kEpi0 = kEw0 + 8;
-    static constexpr int kThreads = 32 * (kEpi0 + 4 * kEpiWGs);
+    static constexpr int kTileWarp = kEpi0 + 4 * kEpiWGs;  // per-item X/Y tiles (TMA)
+    static constexpr int kThreads = 32 * (kTileWarp + 1);
     static constexpr int kBatch = 8;
 };
 
@@ -240,21 +241,8 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                 if (itb >= n_items) { done = true; continue; }
                 const int32_t h = (itb - (itb / (H / HG)) * (H / HG)) * HG;  // (first) head
                 const int nch = w > 0 ? (w + chunk_rows - 1) / chunk_rows : 1;
-                const int qs = qseq % C::kNQ;
+                const int qs = qseq % C::kNQ;  // the item's X/Y slot (loaded by the tile warp)
                 const int qph = (qseq / C::kNQ) & 1;
-                if (lane == 0) {  // the item's 16-row tiles X and Y (rows: Q_w, dO_w; cols: K_w, V_w)
-                    mbar_wait(bar(B::xyempty(qs)), qph ^ 1);
-                    mbar_arrive_expect_tx(bar(B::xyfull(qs)), C::kQBytes);
-                    const uint32_t xd = sb + C::oQ + qs * C::kQBytes;
-#pragma unroll
-                    for (int g = 0; g < HG; ++g)
-#pragma unroll
-                        for (int pp = 0; pp < C::P; ++pp) {
-                            const uint32_t o = g * 16 * C::kRowPitch + pp * 2048;
-                            tma_load_2d(xd + o, &tmX, bar(B::xyfull(qs)), (h + g) * D + 64 * pp, 16 * k);
-                            tma_load_2d(xd + C::kXBytes + o, &tmY, bar(B::xyfull(qs)), (h + g) * D + 64 * pp, 16 * k);
-                        }
-                }
                 for (int j = 0; j < nch; ++j) {
                     const int rows = w > 0 ? min(chunk_rows, w - chunk_rows * j) : 0;
                     const int s = seq % C::kNS;
@@ -291,6 +279,33 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                 mbar_wait(bar(B::empty(s)), ((seq / C::kNS) & 1) ^ 1);
                 slots[s].rows = -1 - w;
                 mbar_arrive(bar(B::idxfull(s)));
+            }
+        }
+        __syncwarp();
+    } else if (warp == C::kTileWarp) {
+        // ===== tile warp: the item's 16-row tiles X and Y (rows: Q_w, dO_w; cols: K_w, V_w) =======
+        // walks the chunk slots in order and loads at each item's first chunk, so that waiting for
+        // a free X/Y slot never holds the index warp back from filling chunk slots ahead
+        if (lane == 0) {
+            for (int32_t seq = 0;; ++seq) {
+                const int s = seq % C::kNS;
+                mbar_wait(bar(B::idxfull(s)), (seq / C::kNS) & 1);
+                const Slot& sl = slots[s];
+                const int rows = sl.rows, flags = sl.flags;
+                if (rows < 0) break;
+                if (!(flags & 1)) continue;
+                const int qs = sl.qslot, qph = (flags >> 2) & 1, k = sl.rw, h = sl.head;
+                mbar_wait(bar(B::xyempty(qs)), qph ^ 1);
+                mbar_arrive_expect_tx(bar(B::xyfull(qs)), C::kQBytes);
+                const uint32_t xd = sb + C::oQ + qs * C::kQBytes;
+#pragma unroll
+                for (int g = 0; g < HG; ++g)
+#pragma unroll
+                    for (int pp = 0; pp < C::P; ++pp) {
+                        const uint32_t o = g * 16 * C::kRowPitch + pp * 2048;
+                        tma_load_2d(xd + o, &tmX, bar(B::xyfull(qs)), (h + g) * D + 64 * pp, 16 * k);
+                        tma_load_2d(xd + C::kXBytes + o, &tmY, bar(B::xyfull(qs)), (h + g) * D + 64 * pp, 16 * k);
+                    }
             }
         }
         __syncwarp();
