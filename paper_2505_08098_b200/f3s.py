@@ -352,6 +352,43 @@ def attention_backward_saved(p: Plan, Q, K, V, O, ml, dO, *, scale: float, strea
     return dQ, dK, dV
 
 
+class _AttentionFn:
+    """torch.autograd.Function over the C ABI (built lazily so that importing this module needs no
+    torch): forward = f3s_attention_fwd, backward = f3s_attention_backward_saved on the saved
+    (O, ml).  Gradients come back in fp32 and are cast to the inputs' dtypes."""
+    fn = None
+
+    @classmethod
+    def get(cls):
+        if cls.fn is None:
+            import torch
+
+            class Fn(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, Q, K, V, p, scale):
+                    O, ml = attention_fwd(p, Q, K, V, scale=scale)
+                    ctx.save_for_backward(Q, K, V, O, ml)
+                    ctx.plan, ctx.scale = p, scale
+                    return O
+
+                @staticmethod
+                def backward(ctx, dO):
+                    Q, K, V, O, ml = ctx.saved_tensors
+                    dO = dO.to(torch.float32).contiguous()
+                    dQ, dK, dV = attention_backward_saved(ctx.plan, Q, K, V, O, ml, dO, scale=ctx.scale)
+                    return dQ.to(Q.dtype), dK.to(K.dtype), dV.to(V.dtype), None, None
+
+            cls.fn = Fn
+        return cls.fn
+
+
+def attention_autograd(p: Plan, Q, K, V, *, scale: float = 1.0):
+    """O = f3s attention with autograd support (training): the forward saves O and the per-row
+    softmax statistics; O.backward() runs the tensor-core backward without recomputing the forward.
+    Q, K, V: contiguous fp16/bf16 CUDA tensors (gradients in the same dtypes); O: float32."""
+    return _AttentionFn.get().apply(Q, K, V, p, float(scale))
+
+
 def attention_trace(p: Plan, Q, K, V, O, *, scale: float, trace_chunks: int = 4096, grid: int = 0,
                     variant: str | int = "default", stream=None):
     """Run the default kernel with F3S_TRACE on; returns uint64 [grid, trace_chunks, 16] globaltimer stamps."""

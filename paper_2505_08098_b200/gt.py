@@ -7,8 +7,9 @@ PAPER.md:683-694: the GT model's attention layer, whose 3S kernel the paper swap
      O   = softmax_row(scale (Q K^T) ⊙ A) V     the fused 3S pass (libf3s, tcgen05)
      out = O W_o                one library GEMM on O cast to the input dtype
 
-Weights are random-initialised (no trained weights exist offline); the layer is an inference
-layer: no bias, residual or normalisation (those belong to the surrounding block).
+Weights are random-initialised (no trained weights exist offline); no bias, residual or
+normalisation (those belong to the surrounding block).  forward() is the inference layer;
+forward_train() the same layer under autograd, its 3S backward on the tensor cores (f3).
 """
 from __future__ import annotations
 
@@ -43,3 +44,15 @@ class GTAttention:
         return O.view(h.shape[0], self.H * self.d).to(self.dtype) @ self.W_o
 
     __call__ = forward
+
+    def parameters(self):
+        return [self.W_qkv, self.W_o]
+
+    def forward_train(self, plan: "f3s.Plan", h):
+        """The same layer with autograd (a training step): Q, K, V are split out of the projection
+        (the backward needs them contiguous), the 3S pass runs f3s_attention_fwd and its backward
+        f3s_attention_backward_saved (attention_autograd); set requires_grad on the weights and/or h."""
+        qkv = self.project(h)
+        Q, K, V = (qkv[:, i].contiguous() for i in range(3))
+        O = f3s.attention_autograd(plan, Q, K, V, scale=self.scale)
+        return O.view(h.shape[0], self.H * self.d).to(self.dtype) @ self.W_o
