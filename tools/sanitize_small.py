@@ -43,3 +43,15 @@ for dt in (torch.float16, torch.bfloat16):
     f3s.attention_backward(p, Q, K, V, dO, scale=0.125, variant="simt")
     torch.cuda.synchronize()
     print("ok mixed/split/partial/backward", dt, float(O.abs().sum()))
+# round 2, later: the training pair (f3s_attention_fwd + f3s_attention_backward_saved) on the
+# mixed/split plan, a head-group plan and d = 128
+for (pl, nn, H, d) in [(p, n, 4, 64), (None, 0, 8, 64), (None, 0, 2, 128)]:
+    if pl is None:
+        g = fi.molecules(10, 20, 40, seed=H + d) if H == 8 else fi.random_csr(300, 300, 0, 200, seed=d)
+        pl, nn = f3s.plan(torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda(), g.n_rows), g.n_rows
+    Q = torch.randn(nn, H, d, device="cuda").half(); K = torch.randn_like(Q); V = torch.randn_like(Q)
+    O, ml = f3s.attention_fwd(pl, Q, K, V, scale=0.125)
+    dO = torch.randn(Q.shape, device="cuda")
+    dQ, dK, dV = f3s.attention_backward_saved(pl, Q, K, V, O, ml, dO, scale=0.125)
+    torch.cuda.synchronize()
+    print("ok fwd+saved backward", nn, H, d, float(dQ.abs().sum() + dK.abs().sum() + dV.abs().sum()))
