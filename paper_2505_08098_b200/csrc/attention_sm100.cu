@@ -318,10 +318,13 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         // TMA load of Q_w (16 x d per head, Alg.1 l.5) into the item's Q slot.
         int32_t seq = 0, qseq = 0, last = 0;
         bool done = false;
+        // claim batch: kBatch items per queue round trip, fewer when the problem has under
+        // 4 kBatch items per CTA (a small graph would otherwise run on n_items / kBatch CTAs)
+        const int batch = max(1, min(C::kBatch, n_items / (4 * (int)gridDim.x)));
         while (!done) {
             // items of the LPT list's heavy prefix are claimed one per round trip, the rest
-            // kBatch at a time (the claim is per lane: consecutive indices, one CTA)
-            const int nclaim = last < heavy_items ? 1 : C::kBatch;
+            // `batch` at a time (the claim is per lane: consecutive indices, one CTA)
+            const int nclaim = last < heavy_items ? 1 : batch;
             int32_t it = 0x7FFFFFFF;
             int4 mt = make_int4(0, 0, 0, 0);
             if (lane < nclaim) {

@@ -223,8 +223,9 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         // ===== index warp: items in LPT order (heavy prefix one per claim) -> chunk slots =====
         int32_t seq = 0, qseq = 0, last = 0;
         bool done = false;
+        const int batch = max(1, min(C::kBatch, n_items / (4 * (int)gridDim.x)));  // as the forward's
         while (!done) {
-            const int nclaim = last < heavy_items ? 1 : C::kBatch;
+            const int nclaim = last < heavy_items ? 1 : batch;
             int32_t it = 0x7FFFFFFF;
             int4 mt = make_int4(0, 0, 0, 0);
             if (lane < nclaim) {
