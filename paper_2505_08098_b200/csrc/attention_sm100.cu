@@ -238,6 +238,9 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     const uint32_t sb = smem_u32(smem);
     if (sb & 1023) __trap();  // swizzled tiles need 1024-byte alignment
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // F3S_TRACE: stamps 8 (kernel entry) and 9 (setup done) of the CTA's first chunk record
+    if (kDiag && trace != nullptr && trace_chunks > 0 && threadIdx.x == 0)
+        trace[(size_t)blockIdx.x * trace_chunks * 16 + 8] = globaltimer_ns();
     auto bar = [&](int i) -> uint32_t { return sb + C::oBar + 8u * i; };
     Slot* slots = reinterpret_cast<Slot*>(smem + C::oSlot);
     CorrSlotT<HG>* corr = reinterpret_cast<CorrSlotT<HG>*>(smem + C::oCorr);
@@ -310,6 +313,8 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + C::oTmem);
+    if (kDiag && trace != nullptr && trace_chunks > 0 && threadIdx.x == 0)
+        trace[(size_t)blockIdx.x * trace_chunks * 16 + 9] = globaltimer_ns();
 
     if (warp == 0) {
         // ===== index warp: work queue (LPT order) -> chunk slots and Q tiles ==============
