@@ -77,3 +77,35 @@ def test_full_size_parity_all_outputs(oracle_mod, graphs, name, dtype):
     rel = (sq_diff / sq_ref) ** 0.5 if sq_ref > 0 else sq_diff ** 0.5
     print(f"{name} {dtype}: {n * w.H * w.d} outputs, max_abs {max_abs:.3e} (row {worst}), rel_fro {rel:.3e}")
     assert max_abs <= TOL_MAX_ABS and rel <= TOL_REL_FRO, (max_abs, worst, rel)
+
+
+@pytest.mark.parametrize("name", ["arxiv", "reddit", "batched"])
+def test_full_size_backward_all_outputs(oracle_mod, graphs, name):
+    """The training pair at full size: f3s_attention_fwd, then
+    f3s_attention_backward_saved for a seeded dO; every element of dQ, dK and dV against the fp64
+    oracle backward on the same fp16 inputs, within reading c23's bar (max-abs <= 1e-2 * max(1,
+    max|ref|), relative Frobenius <= 5e-3, per gradient)."""
+    import torch
+
+    from conftest import decode
+    from paper_2505_08098_b200 import f3s
+    w, csr = graphs(name)
+    Qb, Kb, Vb = w.qkv(csr, dtype="fp16")
+    G = np.random.default_rng(7).standard_normal((csr.n_rows, w.H, w.d)).astype(np.float32)
+    p = f3s.plan(torch.from_numpy(csr.row_ptr).cuda(), torch.from_numpy(csr.col_idx).cuda(), csr.n_rows)
+    Q, K, V = to_dev(Qb, "fp16"), to_dev(Kb, "fp16"), to_dev(Vb, "fp16")
+    O, ml = f3s.attention_fwd(p, Q, K, V, scale=w.scale)
+    got = [x.cpu().numpy() for x in f3s.attention_backward_saved(p, Q, K, V, O, ml, torch.from_numpy(G).cuda(),
+                                                                 scale=w.scale)]
+    del O, ml, Q, K, V
+    torch.cuda.synchronize()
+    ref = oracle_mod.attention_backward(csr.row_ptr, csr.col_idx, decode(Qb, "fp16"), decode(Kb, "fp16"),
+                                        decode(Vb, "fp16"), G.astype(np.float64), scale=w.scale)
+    for nm, g, r in zip(("dQ", "dK", "dV"), got, ref):
+        assert np.all(np.isfinite(g)), nm
+        diff = g.astype(np.float64) - r
+        max_abs = float(np.abs(diff).max())
+        rel = float(np.sqrt((diff * diff).sum() / max((r * r).sum(), 1e-300)))
+        scale = max(1.0, float(np.abs(r).max()))
+        print(f"{name} {nm}: {r.size} outputs, max_abs {max_abs:.3e} (scale {scale:.3e}), rel_fro {rel:.3e}")
+        assert max_abs <= 1e-2 * scale and rel <= 5e-3, (nm, max_abs, scale, rel)
