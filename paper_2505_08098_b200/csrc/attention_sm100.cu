@@ -88,7 +88,7 @@ struct Cfg {
     static constexpr int kTmemCols = kTmemUsed <= 128 ? 128 : kTmemUsed <= 256 ? 256 : 512;
     static_assert(kTmemUsed <= 512, "TMEM columns");
     static constexpr int kSlotBytes = 32 + 128 * 4 + 128 * 2;  // sizeof(Slot)
-    static constexpr int kCorrBytes = HG == 4 ? 608 : 352;  // sizeof(CorrSlotT<HG>)
+    static constexpr int kCorrBytes = 352;  // sizeof(CorrSlot)
     static constexpr int kNumBars = 4 * kNS + 2 * kNQ + 5 * kSB + 2 * 16;
     // everything but the gathered tiles
     static constexpr int kFixedBytes = kNQ * kQBytes + kSB * kPBytes + kNO * kOBytes + kNS * kSlotBytes +
@@ -170,13 +170,9 @@ struct __align__(16) CorrSlot {
     int32_t rows, flags, rw, head;
     uint64_t t_s, t_p;   // F3S_TRACE stamps of the softmax group (written out by the correction group)
 };
-struct __align__(16) CorrSlotHG : CorrSlot {
-    float mh[4][16];     // head groups: head g's row maxima (warp g), for partial-mode outputs
-};
-template <int HG> using CorrSlotT = typename std::conditional<HG == 4, CorrSlotHG, CorrSlot>::type;
+template <int HG> using CorrSlotT = CorrSlot;
 
-static_assert(sizeof(CorrSlot) == Cfg<64>::kCorrBytes && sizeof(CorrSlotHG) == Cfg<64, 4>::kCorrBytes &&
-              sizeof(Slot) == Cfg<64>::kSlotBytes, "layout");
+static_assert(sizeof(CorrSlot) == Cfg<64>::kCorrBytes && sizeof(Slot) == Cfg<64>::kSlotBytes, "layout");
 
 // Transposing butterfly: 16 per-row values in each of 32 lanes -> lane l holds the
 // reduction over the warp for row (l >> 1) & 15.  16 shuffles.
@@ -678,8 +674,12 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             }
             if (!(lane & 1)) corr[b].lpart[q][(lane >> 1) & 15] = rl;
             if (HG == 1 && q == 0 && lane < 16) corr[b].m[lane] = mrow;
-            if constexpr (HG > 1 && kPart)
-                if (!(lane & 1)) corr[b].mh[q][lane >> 1] = fmaxf(kMFloor, rm_hg);
+            if constexpr (HG > 1 && kPart) {  // partial / training outputs: head q's (m, l) of each row
+                const int r = lane >> 1;
+                if (!(lane & 1) && 16 * rw + r < n_rows)
+                    ml_out[(int64_t)(16 * rw + r) * H + hd + q] =
+                        rows > 0 ? make_float2(fmaxf(kMFloor, rm_hg), rl) : make_float2(kMFloor, 0.f);
+            }
             if (p == 0) {
                 reinterpret_cast<int4*>(&corr[b].rows)[0] = make_int4(rows, flags, rw, hd);
                 if (kDiag) {
@@ -761,16 +761,10 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                                 ost[i * (HG * D) + g * D + f] = (rows > 0 && lt[v] > 0.f) ? ov[i] * rcp_approx(lt[v]) : 0.f;
                             }
                         }
-                    } else if (has) {  // partial mode: unnormalised O (unless ml_norm), the head's (m, l) below
+                    } else if (has) {  // partial mode: unnormalised O (unless ml_norm); the softmax warps wrote each head's (m, l)
 #pragma unroll
                         for (int i = 0; i < 16; ++i) ost[i * (HG * D) + g * D + f] = rows > 0 ? ov[i] : 0.f;
                     }
-                }
-                if (kPart && q == 0 && lane < 16 && 16 * rw + lane < n_rows) {
-#pragma unroll
-                    for (int g = 0; g < HG; ++g)
-                        ml_out[(int64_t)(16 * rw + lane) * H + hd + g] =
-                            rows > 0 ? make_float2(static_cast<const CorrSlotHG&>(corr[b]).mh[g][lane], corr[b].lpart[g][lane]) : make_float2(kMFloor, 0.f);
                 }
                 tc_fence_before();
                 mbar_arrive(bar(B::pempty(b)));
