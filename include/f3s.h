@@ -261,6 +261,18 @@ f3s_status f3s_attention_backward_saved(f3s_plan_t plan, const void* Q, const vo
                                         const float* ml, const float* dO, float* dQ, float* dK, float* dV, float scale,
                                         int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
 
+/*
+ * f3s_attention_backward_saved with dO given in the input dtype (F3S_FP16 / F3S_BF16, device
+ * [n_rows, heads, d], 16-byte aligned): the tensor cores read it in place and D_i = dO_i . O_i uses
+ * its values, so a layer whose attention output is cast to the input dtype hands its gradient over
+ * without a conversion (half the dO bytes; no converted copy is written).
+ * Errors: as f3s_attention_backward_saved.
+ */
+f3s_status f3s_attention_backward_saved_lp(f3s_plan_t plan, const void* Q, const void* K, const void* V,
+                                           const float* O, const float* ml, const void* dO, float* dQ, float* dK,
+                                           float* dV, float scale, int32_t heads, int32_t d, f3s_dtype dtype,
+                                           cudaStream_t stream);
+
 /* variant 0: the tensor-core path of f3s_attention_backward; 1: the CUDA-core two-pass kernels
  * (one warp per row / column walking its entries in fp32: online max/sum/D, then p, ds; the
  * reference for the tensor-core path).  Errors: as f3s_attention_backward; INVALID_VALUE for

@@ -591,12 +591,15 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 // row: p = 0), D_i = dO_i . O_i -- and dO in the input dtype, from the forward's partial outputs
 // (unnormalised O, (m, l)) or the saved outputs of f3s_attention_fwd (normalized: O / l, (m, l)).
 // D / 4 lanes per (row, head), 16-byte loads, kU (row, head) pairs per group in flight; head-major
-// output ld_t[h][nq16].
-template <int D, typename T>
+// output ld_t[h][nq16].  kLp: dO is given in the input dtype (f3s_attention_backward_saved_lp): it is
+// read as such and used in place by the passes (no dO16 written).
+template <int D, typename T, bool kLp = false>
 __global__ void __launch_bounds__(256) k_bwd_prep(const float* __restrict__ Op, const float2* __restrict__ ml,
-                                                  const float* __restrict__ dO, int64_t n_rows, int32_t H,
+                                                  const void* __restrict__ dOv, int64_t n_rows, int32_t H,
                                                   int64_t nq16, float2* __restrict__ ld_t, T* __restrict__ dO16,
                                                   int32_t normalized) {
+    const float* __restrict__ dO = static_cast<const float*>(dOv);
+    const T* __restrict__ dOl = static_cast<const T*>(dOv);
     constexpr int L = D / 4, kU = 4;
     const int sub = threadIdx.x % L;
     const int64_t ng = (int64_t)gridDim.x * (blockDim.x / L);
@@ -610,7 +613,13 @@ __global__ void __launch_bounds__(256) k_bwd_prep(const float* __restrict__ Op, 
             const int64_t rh = r0 + u * ng;
             if (rh < total) {
                 o[u] = __ldg(reinterpret_cast<const float4*>(Op + rh * D) + sub);
-                g[u] = __ldg(reinterpret_cast<const float4*>(dO + rh * D) + sub);
+                if constexpr (kLp) {
+                    const uint2 w = __ldg(reinterpret_cast<const uint2*>(dOl + rh * D) + sub);
+                    const T* t = reinterpret_cast<const T*>(&w);
+                    g[u] = make_float4((float)t[0], (float)t[1], (float)t[2], (float)t[3]);
+                } else {
+                    g[u] = __ldg(reinterpret_cast<const float4*>(dO + rh * D) + sub);
+                }
                 v[u] = __ldg(ml + rh);
             }
         }
@@ -622,15 +631,17 @@ __global__ void __launch_bounds__(256) k_bwd_prep(const float* __restrict__ Op, 
 #pragma unroll
             for (int off = L / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
             if (rh < total) {
-                uint2 pk;
-                if constexpr (std::is_same<T, __half>::value) {
-                    pk.x = pack_f16x2(g[u].x, g[u].y);
-                    pk.y = pack_f16x2(g[u].z, g[u].w);
-                } else {
-                    pk.x = pack_bf16x2(g[u].x, g[u].y);
-                    pk.y = pack_bf16x2(g[u].z, g[u].w);
+                if constexpr (!kLp) {
+                    uint2 pk;
+                    if constexpr (std::is_same<T, __half>::value) {
+                        pk.x = pack_f16x2(g[u].x, g[u].y);
+                        pk.y = pack_f16x2(g[u].z, g[u].w);
+                    } else {
+                        pk.x = pack_bf16x2(g[u].x, g[u].y);
+                        pk.y = pack_bf16x2(g[u].z, g[u].w);
+                    }
+                    reinterpret_cast<uint2*>(dO16 + rh * D)[sub] = pk;
                 }
-                reinterpret_cast<uint2*>(dO16 + rh * D)[sub] = pk;
                 if (sub == 0) {
                     const int64_t i = rh / H;
                     const int h = (int)(rh - i * H);
@@ -711,8 +722,8 @@ struct Scratch2 {
 
 template <int D, typename T>
 f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, const float* O_saved,
-                         const float* ml_saved, const float* dO, float* dQ, float* dK, float* dV, float scale, int H,
-                         cudaStream_t stream) {
+                         const float* ml_saved, const void* dO, bool dO_lp, float* dQ, float* dK, float* dV,
+                         float scale, int H, cudaStream_t stream) {
     f3s_status st = build_transpose_plan(p, stream);
     if (st != F3S_OK) return st;
     Plan& tp = *p.tplan;
@@ -725,7 +736,7 @@ f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, c
     const int64_t nh2 = (n * H + 1) / 2 * 2;  // keeps the arrays after (m, l) 16-byte aligned
     const bool saved = O_saved != nullptr;      // f3s_attention_backward_saved: no forward recomputation
     const size_t bytes = (saved ? 0 : sizeof(float) * (size_t)nd + sizeof(float2) * (size_t)nh2) +
-                         2 * sizeof(float) * (size_t)(H * nq16) + sizeof(T) * (size_t)nd + 256;
+                         2 * sizeof(float) * (size_t)(H * nq16) + (dO_lp ? 0 : sizeof(T) * (size_t)nd) + 256;
     F3S_CUDA_TRY(scratch_alloc(&sc.p, bytes, stream));
     char* base = static_cast<char*>(sc.p);
     const float* Op = O_saved;
@@ -742,10 +753,16 @@ f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, c
         Op = op;
         ml = mlp;
     }
-    T* dO16 = reinterpret_cast<T*>(ld_t + H * nq16);
+    // dO in the input dtype for the tensor cores: the caller's (dO_lp), else a converted copy
+    T* dO16 = dO_lp ? const_cast<T*>(static_cast<const T*>(dO)) : reinterpret_cast<T*>(ld_t + H * nq16);
     const int64_t per_block = 4 * (256 / (D / 4));  // (row, head) pairs one block covers per pass
-    k_bwd_prep<D, T><<<(int)std::min<int64_t>((n * H + per_block - 1) / per_block, (int64_t)sms * 8), 256, 0, stream>>>(
-        Op, reinterpret_cast<const float2*>(ml), dO, n, H, nq16, ld_t, dO16, saved ? 1 : 0);
+    const int pgrid = (int)std::min<int64_t>((n * H + per_block - 1) / per_block, (int64_t)sms * 8);
+    if (dO_lp)
+        k_bwd_prep<D, T, true><<<pgrid, 256, 0, stream>>>(Op, reinterpret_cast<const float2*>(ml), dO, n, H, nq16,
+                                                          ld_t, nullptr, saved ? 1 : 0);
+    else
+        k_bwd_prep<D, T><<<pgrid, 256, 0, stream>>>(Op, reinterpret_cast<const float2*>(ml), dO, n, H, nq16, ld_t,
+                                                    dO16, saved ? 1 : 0);
     count_launch();
     F3S_CUDA_TRY(cudaGetLastError());
     // 2. rows: dQ
@@ -763,13 +780,13 @@ f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, c
 }  // namespace
 
 f3s_status launch_attention_backward_tc(Plan& p, const void* Q, const void* K, const void* V, const float* O,
-                                        const float* ml, const float* dO, float* dQ, float* dK, float* dV,
+                                        const float* ml, const void* dO, bool dO_lp, float* dQ, float* dK, float* dV,
                                         float scale, int heads, int d, f3s_dtype dtype, cudaStream_t stream) {
     if (dtype == F3S_FP16)
-        return d == 64 ? launch_bwd_tc<64, __half>(p, Q, K, V, O, ml, dO, dQ, dK, dV, scale, heads, stream)
-                       : launch_bwd_tc<128, __half>(p, Q, K, V, O, ml, dO, dQ, dK, dV, scale, heads, stream);
-    return d == 64 ? launch_bwd_tc<64, __nv_bfloat16>(p, Q, K, V, O, ml, dO, dQ, dK, dV, scale, heads, stream)
-                   : launch_bwd_tc<128, __nv_bfloat16>(p, Q, K, V, O, ml, dO, dQ, dK, dV, scale, heads, stream);
+        return d == 64 ? launch_bwd_tc<64, __half>(p, Q, K, V, O, ml, dO, dO_lp, dQ, dK, dV, scale, heads, stream)
+                       : launch_bwd_tc<128, __half>(p, Q, K, V, O, ml, dO, dO_lp, dQ, dK, dV, scale, heads, stream);
+    return d == 64 ? launch_bwd_tc<64, __nv_bfloat16>(p, Q, K, V, O, ml, dO, dO_lp, dQ, dK, dV, scale, heads, stream)
+                   : launch_bwd_tc<128, __nv_bfloat16>(p, Q, K, V, O, ml, dO, dO_lp, dQ, dK, dV, scale, heads, stream);
 }
 
 }  // namespace f3s

@@ -267,8 +267,8 @@ f3s_status f3s_attention_backward_ex(f3s_plan_t plan, const void* Q, const void*
         DeviceScope scope;
         F3S_CUDA_TRY(scope.enter(p.device));
         if (variant == 0 && p.nnz > 0 && p.n_rows > 0)
-            return launch_attention_backward_tc(p, Q, K, V, nullptr, nullptr, dO, dQ, dK, dV, scale, heads, d, dtype,
-                                                stream);
+            return launch_attention_backward_tc(p, Q, K, V, nullptr, nullptr, dO, false, dQ, dK, dV, scale, heads, d,
+                                                dtype, stream);
         return launch_attention_backward(p, Q, K, V, dO, dQ, dK, dV, scale, heads, d, dtype, stream);
     } catch (...) {
         set_error("internal error");
@@ -301,24 +301,48 @@ f3s_status f3s_attention_fwd(f3s_plan_t plan, const void* Q, const void* K, cons
     }
 }
 
+static f3s_status backward_saved_impl(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* O,
+                                      const float* ml, const void* dO, bool dO_lp, float* dQ, float* dK, float* dV,
+                                      float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
+    f3s_status st = check_attention_args(plan, Q, K, V, dQ, scale, heads, d, dtype, true);
+    if (st != F3S_OK) return st;
+    if (dtype == F3S_E4M3) { set_error("backward: F3S_FP16 or F3S_BF16 only"); return F3S_ERR_UNSUPPORTED; }
+    Plan& p = *reinterpret_cast<Plan*>(plan);
+    if (p.n_rows > 0 && (!dO || !O || !ml)) { set_error("O/ml/dO is NULL"); return F3S_ERR_INVALID_VALUE; }
+    if (p.n_cols > 0 && (!dK || !dV)) { set_error("dK/dV is NULL"); return F3S_ERR_INVALID_VALUE; }
+    auto mis = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) != 0; };
+    if (mis(dO) || mis(dK) || mis(dV) || mis(O)) { set_error("O/dO/dK/dV must be 16-byte aligned"); return F3S_ERR_UNSUPPORTED; }
+    if (reinterpret_cast<uintptr_t>(ml) & 7) { set_error("ml must be 8-byte aligned"); return F3S_ERR_UNSUPPORTED; }
+    DeviceScope scope;
+    F3S_CUDA_TRY(scope.enter(p.device));
+    if (p.nnz > 0 && p.n_rows > 0)
+        return launch_attention_backward_tc(p, Q, K, V, O, ml, dO, dO_lp, dQ, dK, dV, scale, heads, d, dtype, stream);
+    // every row empty: all gradients are zero
+    if (p.n_rows > 0) F3S_CUDA_TRY(cudaMemsetAsync(dQ, 0, sizeof(float) * (size_t)p.n_rows * heads * d, stream));
+    if (p.n_cols > 0) {
+        F3S_CUDA_TRY(cudaMemsetAsync(dK, 0, sizeof(float) * (size_t)p.n_cols * heads * d, stream));
+        F3S_CUDA_TRY(cudaMemsetAsync(dV, 0, sizeof(float) * (size_t)p.n_cols * heads * d, stream));
+    }
+    return F3S_OK;
+}
+
 f3s_status f3s_attention_backward_saved(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* O,
                                         const float* ml, const float* dO, float* dQ, float* dK, float* dV, float scale,
                                         int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
     try {
-        f3s_status st = check_attention_args(plan, Q, K, V, dQ, scale, heads, d, dtype, true);
-        if (st != F3S_OK) return st;
-        if (dtype == F3S_E4M3) { set_error("backward: F3S_FP16 or F3S_BF16 only"); return F3S_ERR_UNSUPPORTED; }
-        Plan& p = *reinterpret_cast<Plan*>(plan);
-        if (p.n_rows > 0 && (!dO || !O || !ml)) { set_error("O/ml/dO is NULL"); return F3S_ERR_INVALID_VALUE; }
-        if (p.n_cols > 0 && (!dK || !dV)) { set_error("dK/dV is NULL"); return F3S_ERR_INVALID_VALUE; }
-        auto mis = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) != 0; };
-        if (mis(dO) || mis(dK) || mis(dV) || mis(O)) { set_error("O/dO/dK/dV must be 16-byte aligned"); return F3S_ERR_UNSUPPORTED; }
-        if (reinterpret_cast<uintptr_t>(ml) & 7) { set_error("ml must be 8-byte aligned"); return F3S_ERR_UNSUPPORTED; }
-        DeviceScope scope;
-        F3S_CUDA_TRY(scope.enter(p.device));
-        if (p.nnz > 0 && p.n_rows > 0)
-            return launch_attention_backward_tc(p, Q, K, V, O, ml, dO, dQ, dK, dV, scale, heads, d, dtype, stream);
-        return launch_attention_backward(p, Q, K, V, dO, dQ, dK, dV, scale, heads, d, dtype, stream);  // all zero
+        return backward_saved_impl(plan, Q, K, V, O, ml, dO, false, dQ, dK, dV, scale, heads, d, dtype, stream);
+    } catch (...) {
+        set_error("internal error");
+        return F3S_ERR_INTERNAL;
+    }
+}
+
+f3s_status f3s_attention_backward_saved_lp(f3s_plan_t plan, const void* Q, const void* K, const void* V,
+                                           const float* O, const float* ml, const void* dO, float* dQ, float* dK,
+                                           float* dV, float scale, int32_t heads, int32_t d, f3s_dtype dtype,
+                                           cudaStream_t stream) {
+    try {
+        return backward_saved_impl(plan, Q, K, V, O, ml, dO, true, dQ, dK, dV, scale, heads, d, dtype, stream);
     } catch (...) {
         set_error("internal error");
         return F3S_ERR_INTERNAL;

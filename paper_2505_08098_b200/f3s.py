@@ -57,6 +57,7 @@ _lib.f3s_attention_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, 
 _lib.f3s_attention_fwd.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_backward_saved.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32,
                                               _i32, _vp]
+_lib.f3s_attention_backward_saved_lp.argtypes = _lib.f3s_attention_backward_saved.argtypes
 _lib.f3s_attention_backward_ex.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
 _lib.f3s_attention_host_async.argtypes = [_vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]
@@ -78,7 +79,8 @@ EXPORTED = ["f3s_plan", "f3s_plan_rows", "f3s_plan_destroy", "f3s_plan_get_info"
             "f3s_attention", "f3s_attention_kv", "f3s_attention_strided", "f3s_attention_partial",
             "f3s_attention_merge", "f3s_attention_ex", "f3s_attention_trace", "f3s_attention_host",
             "f3s_partition_rows", "f3s_partition_at",
-            "f3s_attention_backward", "f3s_attention_backward_ex", "f3s_attention_fwd", "f3s_attention_backward_saved", "f3s_attention_host_async", "f3s_default_split_chunks",
+            "f3s_attention_backward", "f3s_attention_backward_ex", "f3s_attention_fwd", "f3s_attention_backward_saved",
+            "f3s_attention_backward_saved_lp", "f3s_attention_host_async", "f3s_default_split_chunks",
             "f3s_status_string", "f3s_last_error", "f3s_launch_count"]
 
 
@@ -334,9 +336,11 @@ def attention_fwd(p: Plan, Q, K, V, O=None, ml=None, *, scale: float = 1.0, stre
 
 
 def attention_backward_saved(p: Plan, Q, K, V, O, ml, dO, *, scale: float, stream=None):
-    """f3s_attention_backward_saved: (dQ, dK, dV) from the saved outputs (O, ml) of attention_fwd."""
+    """f3s_attention_backward_saved(_lp): (dQ, dK, dV) from the saved outputs (O, ml) of
+    attention_fwd; dO float32, or in Q's dtype (the _lp entry point: read in place)."""
     import torch
-    _check_tensors(p, Q, K, V, dO, what="f3s_attention_backward_saved")
+    lp = dO.dtype == Q.dtype
+    _check_tensors(p, Q, K, V, dO, out_dtype=Q.dtype if lp else None, what="f3s_attention_backward_saved")
     _check_tensors(p, Q, K, V, O, what="f3s_attention_backward_saved")
     H, d = Q.shape[1], Q.shape[2]
     if ml.dtype != torch.float32 or tuple(ml.shape) != (Q.shape[0], H, 2) or not ml.is_contiguous() \
@@ -345,10 +349,10 @@ def attention_backward_saved(p: Plan, Q, K, V, O, ml, dO, *, scale: float, strea
     dQ = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
     dK = torch.empty(K.shape, dtype=torch.float32, device=K.device)
     dV = torch.empty(V.shape, dtype=torch.float32, device=V.device)
-    _check(_lib.f3s_attention_backward_saved(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), O.data_ptr(),
-                                             ml.data_ptr(), dO.data_ptr(), dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(),
-                                             float(scale), H, d, _dtype_code(Q), _stream(stream)),
-           "f3s_attention_backward_saved")
+    fn = _lib.f3s_attention_backward_saved_lp if lp else _lib.f3s_attention_backward_saved
+    _check(fn(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), O.data_ptr(), ml.data_ptr(), dO.data_ptr(),
+              dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(), float(scale), H, d, _dtype_code(Q), _stream(stream)),
+           "f3s_attention_backward_saved" + ("_lp" if lp else ""))
     return dQ, dK, dV
 
 
@@ -365,28 +369,30 @@ class _AttentionFn:
 
             class Fn(torch.autograd.Function):
                 @staticmethod
-                def forward(ctx, Q, K, V, p, scale):
+                def forward(ctx, Q, K, V, p, scale, out_dtype):
                     O, ml = attention_fwd(p, Q, K, V, scale=scale)
                     ctx.save_for_backward(Q, K, V, O, ml)
                     ctx.plan, ctx.scale = p, scale
-                    return O
+                    return O if out_dtype is None else O.to(out_dtype)
 
                 @staticmethod
                 def backward(ctx, dO):
                     Q, K, V, O, ml = ctx.saved_tensors
-                    dO = dO.to(torch.float32).contiguous()
+                    # dO in Q's dtype goes to the _lp entry point as it is; anything else as fp32
+                    dO = (dO if dO.dtype == Q.dtype else dO.to(torch.float32)).contiguous()
                     dQ, dK, dV = attention_backward_saved(ctx.plan, Q, K, V, O, ml, dO, scale=ctx.scale)
-                    return dQ.to(Q.dtype), dK.to(K.dtype), dV.to(V.dtype), None, None
+                    return dQ.to(Q.dtype), dK.to(K.dtype), dV.to(V.dtype), None, None, None
 
             cls.fn = Fn
         return cls.fn
 
 
-def attention_autograd(p: Plan, Q, K, V, *, scale: float = 1.0):
+def attention_autograd(p: Plan, Q, K, V, *, scale: float = 1.0, out_dtype=None):
     """O = f3s attention with autograd support (training): the forward saves O and the per-row
     softmax statistics; O.backward() runs the tensor-core backward without recomputing the forward.
-    Q, K, V: contiguous fp16/bf16 CUDA tensors (gradients in the same dtypes); O: float32."""
-    return _AttentionFn.get().apply(Q, K, V, p, float(scale))
+    Q, K, V: contiguous fp16/bf16 CUDA tensors (gradients in the same dtypes); O: float32, or cast to
+    out_dtype (= Q's dtype: its gradient then reaches f3s_attention_backward_saved_lp unconverted)."""
+    return _AttentionFn.get().apply(Q, K, V, p, float(scale), out_dtype)
 
 
 def attention_trace(p: Plan, Q, K, V, O, *, scale: float, trace_chunks: int = 4096, grid: int = 0,

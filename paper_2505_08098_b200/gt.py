@@ -54,5 +54,5 @@ class GTAttention:
         f3s_attention_backward_saved (attention_autograd); set requires_grad on the weights and/or h."""
         qkv = self.project(h)
         Q, K, V = (qkv[:, i].contiguous() for i in range(3))
-        O = f3s.attention_autograd(plan, Q, K, V, scale=self.scale)
-        return O.view(h.shape[0], self.H * self.d).to(self.dtype) @ self.W_o
+        O = f3s.attention_autograd(plan, Q, K, V, scale=self.scale, out_dtype=self.dtype)
+        return O.view(h.shape[0], self.H * self.d) @ self.W_o

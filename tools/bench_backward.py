@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--config", default="arxiv")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--variant", default="tc", choices=["tc", "simt", "saved"],
+    ap.add_argument("--variant", default="tc", choices=["tc", "simt", "saved", "saved_lp"],
                     help="saved: f3s_attention_backward_saved on the outputs of f3s_attention_fwd (no recomputed forward)")
     a = ap.parse_args()
     import torch
@@ -40,9 +40,10 @@ def main():
     H, d = Q.shape[1], Q.shape[2]
     g = torch.Generator(device="cuda").manual_seed(1)
     dO = torch.randn(Q.shape, generator=g, device="cuda", dtype=torch.float32)
-    if a.variant == "saved":
+    if a.variant in ("saved", "saved_lp"):
         O, ml = f3s.attention_fwd(p, Q, K, V, scale=w.scale)
-        step = lambda: f3s.attention_backward_saved(p, Q, K, V, O, ml, dO, scale=w.scale)
+        dOs = dO.to(tdt) if a.variant == "saved_lp" else dO  # saved_lp: dO in the input dtype
+        step = lambda: f3s.attention_backward_saved(p, Q, K, V, O, ml, dOs, scale=w.scale)
     else:
         step = lambda: f3s.attention_backward(p, Q, K, V, dO, scale=w.scale, variant=a.variant)
     for _ in range(a.warmup):
@@ -56,7 +57,7 @@ def main():
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / a.steps
     fwd_ms = None
-    if a.variant == "saved":  # the training forward alone, for the fwd + bwd step time
+    if a.variant in ("saved", "saved_lp"):  # the training forward alone, for the fwd + bwd step time
         O2, ml2 = torch.empty_like(O), torch.empty_like(ml)
         for _ in range(3):
             f3s.attention_fwd(p, Q, K, V, O2, ml2, scale=w.scale)
@@ -84,6 +85,8 @@ def main():
                       "kernels": {"tc": "forward (partial) + k_bwd_prep + k_bwd_sm100 rows + k_bwd_sm100 columns (tcgen05)",
                                   "saved": "k_bwd_prep + k_bwd_sm100 rows + k_bwd_sm100 columns (tcgen05); O, (m, l) saved "
                                            "by f3s_attention_fwd",
+                                  "saved_lp": "k_bwd_prep (dO in the input dtype, read in place) + k_bwd_sm100 rows + "
+                                              "k_bwd_sm100 columns (tcgen05); O, (m, l) saved by f3s_attention_fwd",
                                   "simt": "k_bwd_rows + k_bwd_cols (CUDA cores)"}[a.variant]}))
 
 
