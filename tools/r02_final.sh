@@ -16,7 +16,7 @@ done
 for c in products arxiv reddit; do
   timeout -s KILL 600 python bench.py --config $c --dtype e4m3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_bench_${c}_e4m3.json 2> gpurun_out/${T}_bench_${c}_e4m3.err
 done
-for c in arxiv reddit batched cora; do for v in saved tc; do timeout -s KILL 300 python tools/bench_backward.py --config $c --variant $v 2>/dev/null | tail -1; done; done > gpurun_out/${T}_bench_backward.jsonl
+for c in arxiv reddit batched cora; do for v in saved saved_lp tc; do timeout -s KILL 300 python tools/bench_backward.py --config $c --variant $v 2>/dev/null | tail -1; done; done > gpurun_out/${T}_bench_backward.jsonl
 CONFIGS="arxiv reddit batched" bash tools/bwd_launches.sh ${T} > gpurun_out/${T}_bwd_launches.txt 2>&1
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:k_bwd -c 3 -o gpurun_out/${T}_prof_bwd_arxiv python tools/bench_backward.py --config arxiv --variant saved --steps 1 --warmup 0 > /dev/null 2>&1
 for c in products reddit arxiv batched cora; do
