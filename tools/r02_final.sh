@@ -24,4 +24,8 @@ for c in products reddit arxiv batched cora; do
   timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_f3s_sm100 -s 3 -c 1 -o gpurun_out/${T}_prof_$c python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --graph-batch 0 > /dev/null 2>&1
 done
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_f3s_sm100 -s 3 -c 1 -o gpurun_out/${T}_prof_arxiv_e4m3 python bench.py --config arxiv --dtype e4m3 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --graph-batch 0 > /dev/null 2>&1
+# gpurun copies back at most 64 MiB: summarise the ncu reports here and keep only the products one
+for f in gpurun_out/${T}_prof_*.ncu-rep; do python tools/ncu_summary.py $f > ${f%.ncu-rep}.txt 2>&1; done
+python tools/update_traffic.py ${T} products reddit arxiv batched cora > /dev/null 2>&1; cp profiles/traffic.json gpurun_out/${T}_traffic.json
+ls gpurun_out/${T}_prof_*.ncu-rep | grep -v "_prof_products.ncu-rep" | xargs rm -f
 ls gpurun_out | grep "^${T}_" | wc -l
