@@ -205,3 +205,31 @@ def test_training_forward_and_saved_backward(f3s, oracle_mod, dtype, graph, d, H
     ref_lp = oracle_mod.attention_backward(csr.row_ptr, csr.col_idx, qd, kd, decode(Vb, dtype), G_lp, scale=scale)
     for a, r in zip(lp, ref_lp):
         _close(a, r)
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_training_pair_split_and_mixed_widths(f3s, oracle_mod, dtype):
+    """The training forward on a plan with both launch kinds (wide windows one head per chunk, split
+    into pieces by a forced bound; narrow windows with head groups): O bitwise equal to
+    f3s_attention, and the saved-stats backward against the oracle."""
+    import torch
+    mol = fi.molecules(40, 25, 60, seed=3)
+    wide = fi.random_csr(48, mol.n_rows, 60, 400, seed=4)
+    rp = np.concatenate([mol.row_ptr, mol.row_ptr[-1] + wide.row_ptr[1:]]).astype(np.int32)
+    ci = np.concatenate([mol.col_idx, wide.col_idx]).astype(np.int32)
+    n = mol.n_rows + 48
+    p = f3s.plan(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(), n)
+    p.set_split(1)
+    assert p.info()["split_groups"] > 0 and p.info()["max_width"] > 32
+    H, d = 4, 64
+    Qb, Kb, Vb = make_qkv(n, n, H, d, dtype, seed=41)
+    Q, K, V = to_dev(Qb, dtype), to_dev(Kb, dtype), to_dev(Vb, dtype)
+    O, ml = f3s.attention_fwd(p, Q, K, V, scale=0.125)
+    assert torch.equal(O, f3s.attention(p, Q, K, V, scale=0.125))
+    G = np.random.default_rng(11).standard_normal((n, H, d)).astype(np.float32)
+    got = [x.cpu().numpy() for x in f3s.attention_backward_saved(p, Q, K, V, O, ml, torch.from_numpy(G).cuda(),
+                                                                 scale=0.125)]
+    ref = oracle_mod.attention_backward(rp, ci, decode(Qb, dtype), decode(Kb, dtype), decode(Vb, dtype),
+                                        G.astype(np.float64), scale=0.125)
+    for a, r in zip(got, ref):
+        _close(a, r)
