@@ -387,6 +387,48 @@ class _AttentionFn:
         return cls.fn
 
 
+class _AttentionQKVFn:
+    """The same over a packed projection output QKV [n, 3, H, d]: the backward writes dQ, dK, dV
+    straight into one packed gradient (three cast copies) instead of autograd's per-slice
+    zero-filled buffers and their sum."""
+    fn = None
+
+    @classmethod
+    def get(cls):
+        if cls.fn is None:
+            import torch
+
+            class Fn(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, QKV, p, scale, out_dtype):
+                    Q, K, V = (QKV[:, i].contiguous() for i in range(3))
+                    O, ml = attention_fwd(p, Q, K, V, scale=scale)
+                    ctx.save_for_backward(Q, K, V, O, ml)
+                    ctx.plan, ctx.scale = p, scale
+                    return O if out_dtype is None else O.to(out_dtype)
+
+                @staticmethod
+                def backward(ctx, dO):
+                    Q, K, V, O, ml = ctx.saved_tensors
+                    dO = (dO if dO.dtype == Q.dtype else dO.to(torch.float32)).contiguous()
+                    grads = attention_backward_saved(ctx.plan, Q, K, V, O, ml, dO, scale=ctx.scale)
+                    dQKV = torch.empty((Q.shape[0], 3) + tuple(Q.shape[1:]), dtype=Q.dtype, device=Q.device)
+                    for i, g in enumerate(grads):
+                        dQKV[:, i].copy_(g)
+                    return dQKV, None, None, None
+
+            cls.fn = Fn
+        return cls.fn
+
+
+def attention_autograd_qkv(p: Plan, QKV, *, scale: float = 1.0, out_dtype=None):
+    """attention_autograd on a packed [n, 3, H, d] projection output (Q, K, V = QKV[:, 0/1/2]);
+    the gradient comes back packed the same way."""
+    if QKV.dim() != 4 or QKV.shape[1] != 3:
+        raise ValueError("attention_autograd_qkv: QKV must be [n, 3, heads, d]")
+    return _AttentionQKVFn.get().apply(QKV, p, float(scale), out_dtype)
+
+
 def attention_autograd(p: Plan, Q, K, V, *, scale: float = 1.0, out_dtype=None):
     """O = f3s attention with autograd support (training): the forward saves O and the per-row
     softmax statistics; O.backward() runs the tensor-core backward without recomputing the forward.

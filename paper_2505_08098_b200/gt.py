@@ -51,8 +51,8 @@ class GTAttention:
     def forward_train(self, plan: "f3s.Plan", h):
         """The same layer with autograd (a training step): Q, K, V are split out of the projection
         (the backward needs them contiguous), the 3S pass runs f3s_attention_fwd and its backward
-        f3s_attention_backward_saved (attention_autograd); set requires_grad on the weights and/or h."""
+        f3s_attention_backward_saved_lp (attention_autograd_qkv: the gradient comes back packed as
+        [n, 3, H, d]); set requires_grad on the weights and/or h."""
         qkv = self.project(h)
-        Q, K, V = (qkv[:, i].contiguous() for i in range(3))
-        O = f3s.attention_autograd(plan, Q, K, V, scale=self.scale, out_dtype=self.dtype)
+        O = f3s.attention_autograd_qkv(plan, qkv, scale=self.scale, out_dtype=self.dtype)
         return O.view(h.shape[0], self.H * self.d) @ self.W_o

@@ -1,6 +1,7 @@
 """Graph Transformer attention layer on config 5 (batched molecules, 8 heads, d = 64): device time of
-the projection GEMM, the fused 3S pass (strided, in place), the cast and the output GEMM, as one
-JSON line (CUDA events, warm-up 3, median of 20)."""
+the projection GEMM, the fused 3S pass (strided, in place), the cast and the output GEMM, and of one
+training step (forward_train + autograd backward: f3s_attention_fwd / f3s_attention_backward_saved_lp
+between the GEMMs), as one JSON line (CUDA events, warm-up 3, median of 20)."""
 import json
 import os
 import sys
@@ -41,6 +42,27 @@ def main():
         for i, k in enumerate(("qkv_gemm", "fused_3s", "cast", "out_gemm")):
             ts[k].append(ev[i].elapsed_time(ev[i + 1]))
         ts["layer"].append(ev[0].elapsed_time(ev[4]))
+    # one training step of the layer: forward_train (QKV GEMM, f3s_attention_fwd, output GEMM) and
+    # the backward through autograd (output GEMM grads, f3s_attention_backward_saved_lp, QKV GEMM grads)
+    for wgt in layer.parameters():
+        wgt.requires_grad_(True)
+    G = torch.rand((csr.n_rows, H * d), device="cuda").half()
+    for _ in range(3):
+        layer.forward_train(plan, h).backward(G)
+    tr = {"train_forward": [], "train_backward": [], "train_step": []}
+    for _ in range(20):
+        for wgt in layer.parameters():
+            wgt.grad = None
+        ev[0].record()
+        out = layer.forward_train(plan, h)
+        ev[1].record()
+        out.backward(G)
+        ev[2].record()
+        torch.cuda.synchronize()
+        tr["train_forward"].append(ev[0].elapsed_time(ev[1]))
+        tr["train_backward"].append(ev[1].elapsed_time(ev[2]))
+        tr["train_step"].append(ev[0].elapsed_time(ev[2]))
+    ts.update(tr)
     med = {k: round(float(np.median(v)), 4) for k, v in ts.items()}
     D = H * d
     gemm_flops = 2.0 * csr.n_rows * D * (3 * D + D)
