@@ -66,6 +66,15 @@ def test_host_argument_validation(f3s):
     assert st == f3s.INVALID_VALUE
     assert b"NULL" in f3s._lib.f3s_last_error()
     assert f3s._lib.f3s_plan_set_split(None, 4) == f3s.INVALID_VALUE
+    # the training pair and the backward entry points: NULL plan first
+    assert f3s._lib.f3s_attention_fwd(None, None, None, None, None, None, 1.0, 1, 64, 0, None) == f3s.INVALID_VALUE
+    for fn in (f3s._lib.f3s_attention_backward_saved, f3s._lib.f3s_attention_backward_saved_lp):
+        assert fn(None, None, None, None, None, None, None, None, None, None, 1.0, 1, 64, 0, None) == f3s.INVALID_VALUE
+    assert f3s._lib.f3s_attention_backward(None, None, None, None, None, None, None, None, 1.0, 1, 64, 0,
+                                           None) == f3s.INVALID_VALUE
+    # bad sizes are rejected before any CUDA call too
+    assert f3s._lib.f3s_attention_merge(0, None, None, 4, 1, 64, None, None) == f3s.INVALID_VALUE
+    assert f3s._lib.f3s_attention_merge(2, None, None, 4, 1, 96, None, None) == f3s.INVALID_VALUE
 
 
 def nnz_of_range(rp, b, e):
