@@ -340,6 +340,8 @@ def attention_backward_saved(p: Plan, Q, K, V, O, ml, dO, *, scale: float, strea
     attention_fwd; dO float32, or in Q's dtype (the _lp entry point: read in place)."""
     import torch
     lp = dO.dtype == Q.dtype
+    if not lp and dO.dtype != torch.float32:
+        raise ValueError(f"attention_backward_saved: dO must be float32 or Q's dtype {Q.dtype}, got {dO.dtype}")
     _check_tensors(p, Q, K, V, dO, out_dtype=Q.dtype if lp else None, what="f3s_attention_backward_saved")
     _check_tensors(p, Q, K, V, O, what="f3s_attention_backward_saved")
     H, d = Q.shape[1], Q.shape[2]
