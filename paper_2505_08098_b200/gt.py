@@ -48,11 +48,18 @@ class GTAttention:
     def parameters(self):
         return [self.W_qkv, self.W_o]
 
+    def project_split(self, h):
+        """Q, K, V = h W_q, h W_k, h W_v as three contiguous [n, H, d] GEMM outputs (the column blocks
+        of W_qkv): the training pair needs contiguous operands, and three GEMMs write them directly
+        instead of one packed output plus three copies."""
+        D = self.H * self.d
+        return tuple((h @ self.W_qkv[:, i * D:(i + 1) * D]).view(h.shape[0], self.H, self.d) for i in range(3))
+
     def forward_train(self, plan: "f3s.Plan", h):
-        """The same layer with autograd (a training step): Q, K, V are split out of the projection
-        (the backward needs them contiguous), the 3S pass runs f3s_attention_fwd and its backward
-        f3s_attention_backward_saved_lp (attention_autograd_qkv: the gradient comes back packed as
-        [n, 3, H, d]); set requires_grad on the weights and/or h."""
-        qkv = self.project(h)
-        O = f3s.attention_autograd_qkv(plan, qkv, scale=self.scale, out_dtype=self.dtype)
+        """The same layer with autograd (a training step): Q, K, V from project_split, the 3S pass
+        runs f3s_attention_fwd and its backward f3s_attention_backward_saved_lp (attention_autograd,
+        the attention output cast to the input dtype so that its gradient arrives in it); set
+        requires_grad on the weights and/or h."""
+        Q, K, V = self.project_split(h)
+        O = f3s.attention_autograd(plan, Q, K, V, scale=self.scale, out_dtype=self.dtype)
         return O.view(h.shape[0], self.H * self.d) @ self.W_o

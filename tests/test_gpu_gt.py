@@ -72,9 +72,8 @@ def test_gt_layer_training_step(oracle_mod, dtype):
     (out.float() * G).sum().backward()
     torch.cuda.synchronize()
     # fp64 chain on the layer's own rounded projection values
-    qkv = layer.project(h).detach()
-    bits = qkv.view(torch.int16).cpu().numpy().view(np.uint16)
-    Qb, Kb, Vb = (np.ascontiguousarray(bits[:, i]) for i in range(3))
+    Qb, Kb, Vb = (x.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+                  for x in layer.project_split(h))
     from conftest import decode
     Q64, K64, V64 = (decode(x, dtype) for x in (Qb, Kb, Vb))
     O64 = oracle_mod.attention_f64(g.row_ptr, g.col_idx, Q64, K64, V64, scale=layer.scale)
@@ -94,3 +93,26 @@ def test_gt_layer_training_step(oracle_mod, dtype):
         # the backward's inputs enter the tensor cores in the input dtype and the weight gradients
         # are rounded to it: BASELINE's tolerances relative to the gradient's scale
         assert_close(got / scale, ref / scale)
+
+
+def test_autograd_packed_equals_split():
+    """attention_autograd_qkv (packed [n, 3, H, d] operand and gradient) and attention_autograd on
+    the three slices give the same O and the same gradients bit for bit (same kernels)."""
+    import torch
+
+    from paper_2505_08098_b200 import f3s
+    g = fi.molecules(200, seed=31)
+    n, H, d = g.n_rows, 8, 64
+    plan = f3s.plan(torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda(), n)
+    gen = torch.Generator(device="cpu").manual_seed(12)
+    qkv = (torch.rand((n, 3, H, d), generator=gen) * 2 - 1).half().cuda().requires_grad_(True)
+    G = (torch.rand((n, H, d), generator=gen) * 2 - 1).half().cuda()
+    O1 = f3s.attention_autograd_qkv(plan, qkv, scale=0.125, out_dtype=torch.float16)
+    O1.backward(G)
+    parts = [qkv.detach()[:, i].contiguous().requires_grad_(True) for i in range(3)]
+    O2 = f3s.attention_autograd(plan, *parts, scale=0.125, out_dtype=torch.float16)
+    O2.backward(G)
+    torch.cuda.synchronize()
+    assert torch.equal(O1, O2)
+    for i in range(3):
+        assert torch.equal(qkv.grad[:, i], parts[i].grad)
