@@ -262,15 +262,15 @@ f3s_status f3s_attention_backward_saved(f3s_plan_t plan, const void* Q, const vo
                                         int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream);
 
 /*
- * f3s_attention_backward_saved with dO given in the input dtype (F3S_FP16 / F3S_BF16, device
- * [n_rows, heads, d], 16-byte aligned): the tensor cores read it in place and D_i = dO_i . O_i uses
- * its values, so a layer whose attention output is cast to the input dtype hands its gradient over
- * without a conversion (half the dO bytes; no converted copy is written).
- * Errors: as f3s_attention_backward_saved.
+ * f3s_attention_backward_saved in the input dtype (F3S_FP16 / F3S_BF16): dO is given in it (device
+ * [n_rows, heads, d], 16-byte aligned; the tensor cores read it in place and D_i = dO_i . O_i uses its
+ * values) and dQ [n_rows, heads, d], dK, dV [n_cols, heads, d] are written in it (the fp32 TMEM
+ * accumulators rounded once, RNE) -- a 16-bit layer's gradients with no conversions and half the
+ * gradient bytes.  Errors: as f3s_attention_backward_saved.
  */
 f3s_status f3s_attention_backward_saved_lp(f3s_plan_t plan, const void* Q, const void* K, const void* V,
-                                           const float* O, const float* ml, const void* dO, float* dQ, float* dK,
-                                           float* dV, float scale, int32_t heads, int32_t d, f3s_dtype dtype,
+                                           const float* O, const float* ml, const void* dO, void* dQ, void* dK,
+                                           void* dV, float scale, int32_t heads, int32_t d, f3s_dtype dtype,
                                            cudaStream_t stream);
 
 /* variant 0: the tensor-core path of f3s_attention_backward; 1: the CUDA-core two-pass kernels

@@ -160,7 +160,7 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             int32_t* __restrict__ counter, int32_t n_items, int32_t heavy_items, int32_t H,
             const uint8_t* __restrict__ A1g, const uint8_t* __restrict__ A2g, int64_t ld_bytes,
             const float2* __restrict__ ld_t, int64_t nq16, float scale_log2,
-            float g2scale, float g1scale) {
+            float g2scale, float g1scale, int32_t out16) {
     using C = BCfg<D, PASS, HG>;
     using B = BBars<D, PASS, HG>;
     using Slot = BSlot<C::kScal>;
@@ -551,8 +551,12 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
             const bool nz = r.z != 0;  // an item with no entries has an untouched accumulator: zeros
             if (lead) bulk_wait_group_read<0>();
             named_bar_sync(3 + e, 128);
+            // staging tiles at ost (G1) and ost + kOBytes (G2): fp32, or the input dtype (out16,
+            // f3s_attention_backward_saved_lp: the fp32 accumulators rounded once, RNE)
             float* o1 = reinterpret_cast<float*>(smem + ost);
-            float* o2 = o1 + 16 * D * HG;
+            float* o2 = reinterpret_cast<float*>(smem + ost + C::kOBytes);
+            T* h1 = reinterpret_cast<T*>(o1);
+            T* h2 = reinterpret_cast<T*>(o2);
 #pragma unroll 1
             for (int g = 0; g < HG; ++g) {  // [16 x HG*D] tiles: head g in columns g*D ..
                 float g1[16], g2[16];
@@ -560,10 +564,18 @@ k_bwd_sm100(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
                 tmem_ld_32x32b_x16(tmem + tl + gacc, g1);
                 if (PASS == 1) tmem_ld_32x32b_x16(tmem + tl + gacc + 16, g2);
                 if (has) {
+                    if (out16) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        o1[i * (HG * D) + g * D + f] = nz ? g1[i] * g1scale : 0.f;
-                        if (PASS == 1) o2[i * (HG * D) + g * D + f] = nz ? g2[i] * g2scale : 0.f;
+                        for (int i = 0; i < 16; ++i) {
+                            h1[i * (HG * D) + g * D + f] = T(nz ? g1[i] * g1scale : 0.f);
+                            if (PASS == 1) h2[i * (HG * D) + g * D + f] = T(nz ? g2[i] * g2scale : 0.f);
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            o1[i * (HG * D) + g * D + f] = nz ? g1[i] * g1scale : 0.f;
+                            if (PASS == 1) o2[i * (HG * D) + g * D + f] = nz ? g2[i] * g2scale : 0.f;
+                        }
                     }
                 }
             }
@@ -653,8 +665,8 @@ __global__ void __launch_bounds__(256) k_bwd_prep(const float* __restrict__ Op, 
 }
 
 template <int D, typename T, int PASS, int HG>
-f3s_status launch_pass_hg(const Plan& p, const void* X, const void* Y, const void* A1, const void* A2, float* G1,
-                          float* G2, const float2* ld_t, int64_t nq16, int H, float scale,
+f3s_status launch_pass_hg(const Plan& p, const void* X, const void* Y, const void* A1, const void* A2, void* G1,
+                          void* G2, bool out16, const float2* ld_t, int64_t nq16, int H, float scale,
                           int sms, cudaStream_t stream) {
     using C = BCfg<D, PASS, HG>;
     if (p.num_rw == 0) return F3S_OK;
@@ -664,12 +676,11 @@ f3s_status launch_pass_hg(const Plan& p, const void* X, const void* Y, const voi
     f3s_status st;
     if ((st = make_map(&mx, X, dt, ld, p.n_rows, ld, 16)) != F3S_OK) return st;
     if ((st = make_map(&my, Y, dt, ld, p.n_rows, ld, 16)) != F3S_OK) return st;
-    if ((st = make_map(&mg1, G1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ld, p.n_rows, ld, D * HG, 16,
-                       CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK)
-        return st;
+    const CUtensorMapDataType gt = !out16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                   : dt == F3S_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    if ((st = make_map(&mg1, G1, gt, ld, p.n_rows, ld, D * HG, 16, CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK) return st;
     mg2 = mg1;
-    if (PASS == 1 && (st = make_map(&mg2, G2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ld, p.n_rows, ld, D * HG, 16,
-                                    CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK)
+    if (PASS == 1 && (st = make_map(&mg2, G2, gt, ld, p.n_rows, ld, D * HG, 16, CU_TENSOR_MAP_SWIZZLE_NONE)) != F3S_OK)
         return st;
     static std::atomic<uint64_t> attr_set{0};
     static std::mutex mu;
@@ -692,7 +703,7 @@ f3s_status launch_pass_hg(const Plan& p, const void* X, const void* Y, const voi
             mx, my, mg1, mg2, p.meta_lpt, p.kcols, p.kmasks, reinterpret_cast<int32_t*>(scratch), (int32_t)n_items64,
             (int32_t)std::min<int64_t>((int64_t)p.n_heavy_lpt * (H / HG), 0x7FFFFFFF), H,
             static_cast<const uint8_t*>(A1), static_cast<const uint8_t*>(A2), ld * 2, ld_t, nq16,
-            scale * 1.4426950408889634f, scale, PASS == 0 ? scale : 1.f);
+            scale * 1.4426950408889634f, scale, PASS == 0 ? scale : 1.f, out16 ? 1 : 0);
         count_launch();
         err = cudaGetLastError();
     }
@@ -704,14 +715,14 @@ f3s_status launch_pass_hg(const Plan& p, const void* X, const void* Y, const voi
 
 // head groups of 4 when d = 64, H % 4 == 0 and every window of the pass's plan has <= 32 columns
 template <int D, typename T, int PASS>
-f3s_status launch_pass(const Plan& p, const void* X, const void* Y, const void* A1, const void* A2, float* G1,
-                       float* G2, const float2* ld_t, int64_t nq16, int H, float scale,
+f3s_status launch_pass(const Plan& p, const void* X, const void* Y, const void* A1, const void* A2, void* G1,
+                       void* G2, bool out16, const float2* ld_t, int64_t nq16, int H, float scale,
                        int sms, cudaStream_t stream) {
     if constexpr (D == 64) {
         if (H % 4 == 0 && p.max_width <= 32)
-            return launch_pass_hg<D, T, PASS, 4>(p, X, Y, A1, A2, G1, G2, ld_t, nq16, H, scale, sms, stream);
+            return launch_pass_hg<D, T, PASS, 4>(p, X, Y, A1, A2, G1, G2, out16, ld_t, nq16, H, scale, sms, stream);
     }
-    return launch_pass_hg<D, T, PASS, 1>(p, X, Y, A1, A2, G1, G2, ld_t, nq16, H, scale, sms, stream);
+    return launch_pass_hg<D, T, PASS, 1>(p, X, Y, A1, A2, G1, G2, out16, ld_t, nq16, H, scale, sms, stream);
 }
 
 struct Scratch2 {
@@ -722,7 +733,7 @@ struct Scratch2 {
 
 template <int D, typename T>
 f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, const float* O_saved,
-                         const float* ml_saved, const void* dO, bool dO_lp, float* dQ, float* dK, float* dV,
+                         const float* ml_saved, const void* dO, bool dO_lp, void* dQ, void* dK, void* dV,
                          float scale, int H, cudaStream_t stream) {
     f3s_status st = build_transpose_plan(p, stream);
     if (st != F3S_OK) return st;
@@ -766,21 +777,23 @@ f3s_status launch_bwd_tc(Plan& p, const void* Q, const void* K, const void* V, c
     count_launch();
     F3S_CUDA_TRY(cudaGetLastError());
     // 2. rows: dQ
-    if ((st = launch_pass<D, T, 0>(p, Q, dO16, K, V, dQ, nullptr, ld_t, nq16, H, scale, sms, stream)) != F3S_OK)
+    // (the _lp entry point: gradients in the input dtype too)
+    if ((st = launch_pass<D, T, 0>(p, Q, dO16, K, V, dQ, nullptr, dO_lp, ld_t, nq16, H, scale, sms, stream)) != F3S_OK)
         return st;
     // 3. columns: dV (G1), dK (G2) over A^T
     if (tp.n_rows > 0 && tp.nnz == 0) {
-        F3S_CUDA_TRY(cudaMemsetAsync(dK, 0, sizeof(float) * (size_t)tp.n_rows * H * D, stream));
-        F3S_CUDA_TRY(cudaMemsetAsync(dV, 0, sizeof(float) * (size_t)tp.n_rows * H * D, stream));
+        const size_t es = dO_lp ? sizeof(T) : sizeof(float);
+        F3S_CUDA_TRY(cudaMemsetAsync(dK, 0, es * (size_t)tp.n_rows * H * D, stream));
+        F3S_CUDA_TRY(cudaMemsetAsync(dV, 0, es * (size_t)tp.n_rows * H * D, stream));
         return F3S_OK;
     }
-    return launch_pass<D, T, 1>(tp, K, V, Q, dO16, dV, dK, ld_t, nq16, H, scale, sms, stream);
+    return launch_pass<D, T, 1>(tp, K, V, Q, dO16, dV, dK, dO_lp, ld_t, nq16, H, scale, sms, stream);
 }
 
 }  // namespace
 
 f3s_status launch_attention_backward_tc(Plan& p, const void* Q, const void* K, const void* V, const float* O,
-                                        const float* ml, const void* dO, bool dO_lp, float* dQ, float* dK, float* dV,
+                                        const float* ml, const void* dO, bool dO_lp, void* dQ, void* dK, void* dV,
                                         float scale, int heads, int d, f3s_dtype dtype, cudaStream_t stream) {
     if (dtype == F3S_FP16)
         return d == 64 ? launch_bwd_tc<64, __half>(p, Q, K, V, O, ml, dO, dO_lp, dQ, dK, dV, scale, heads, stream)

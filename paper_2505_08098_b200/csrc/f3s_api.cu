@@ -302,9 +302,9 @@ f3s_status f3s_attention_fwd(f3s_plan_t plan, const void* Q, const void* K, cons
 }
 
 static f3s_status backward_saved_impl(f3s_plan_t plan, const void* Q, const void* K, const void* V, const float* O,
-                                      const float* ml, const void* dO, bool dO_lp, float* dQ, float* dK, float* dV,
+                                      const float* ml, const void* dO, bool dO_lp, void* dQ, void* dK, void* dV,
                                       float scale, int32_t heads, int32_t d, f3s_dtype dtype, cudaStream_t stream) {
-    f3s_status st = check_attention_args(plan, Q, K, V, dQ, scale, heads, d, dtype, true);
+    f3s_status st = check_attention_args(plan, Q, K, V, static_cast<float*>(dQ), scale, heads, d, dtype, true);
     if (st != F3S_OK) return st;
     if (dtype == F3S_E4M3) { set_error("backward: F3S_FP16 or F3S_BF16 only"); return F3S_ERR_UNSUPPORTED; }
     Plan& p = *reinterpret_cast<Plan*>(plan);
@@ -318,10 +318,11 @@ static f3s_status backward_saved_impl(f3s_plan_t plan, const void* Q, const void
     if (p.nnz > 0 && p.n_rows > 0)
         return launch_attention_backward_tc(p, Q, K, V, O, ml, dO, dO_lp, dQ, dK, dV, scale, heads, d, dtype, stream);
     // every row empty: all gradients are zero
-    if (p.n_rows > 0) F3S_CUDA_TRY(cudaMemsetAsync(dQ, 0, sizeof(float) * (size_t)p.n_rows * heads * d, stream));
+    const size_t es = dO_lp ? 2 : sizeof(float);
+    if (p.n_rows > 0) F3S_CUDA_TRY(cudaMemsetAsync(dQ, 0, es * (size_t)p.n_rows * heads * d, stream));
     if (p.n_cols > 0) {
-        F3S_CUDA_TRY(cudaMemsetAsync(dK, 0, sizeof(float) * (size_t)p.n_cols * heads * d, stream));
-        F3S_CUDA_TRY(cudaMemsetAsync(dV, 0, sizeof(float) * (size_t)p.n_cols * heads * d, stream));
+        F3S_CUDA_TRY(cudaMemsetAsync(dK, 0, es * (size_t)p.n_cols * heads * d, stream));
+        F3S_CUDA_TRY(cudaMemsetAsync(dV, 0, es * (size_t)p.n_cols * heads * d, stream));
     }
     return F3S_OK;
 }
@@ -338,8 +339,8 @@ f3s_status f3s_attention_backward_saved(f3s_plan_t plan, const void* Q, const vo
 }
 
 f3s_status f3s_attention_backward_saved_lp(f3s_plan_t plan, const void* Q, const void* K, const void* V,
-                                           const float* O, const float* ml, const void* dO, float* dQ, float* dK,
-                                           float* dV, float scale, int32_t heads, int32_t d, f3s_dtype dtype,
+                                           const float* O, const float* ml, const void* dO, void* dQ, void* dK,
+                                           void* dV, float scale, int32_t heads, int32_t d, f3s_dtype dtype,
                                            cudaStream_t stream) {
     try {
         return backward_saved_impl(plan, Q, K, V, O, ml, dO, true, dQ, dK, dV, scale, heads, d, dtype, stream);

@@ -155,9 +155,9 @@ constexpr int kHeavyChunks = 8;       // an item of this many chunks is claimed 
 f3s_status launch_attention_simt(const AttnArgs& a);
 f3s_status build_transpose_plan(Plan& p, cudaStream_t stream);
 // O, ml: the saved outputs of f3s_attention_fwd, or NULL (the forward is recomputed in partial mode);
-// dO: fp32, or in the input dtype when dO_lp (f3s_attention_backward_saved_lp)
+// dO, dQ, dK, dV: fp32, or in the input dtype when dO_lp (f3s_attention_backward_saved_lp)
 f3s_status launch_attention_backward_tc(Plan& p, const void* Q, const void* K, const void* V, const float* O,
-                                        const float* ml, const void* dO, bool dO_lp, float* dQ, float* dK, float* dV,
+                                        const float* ml, const void* dO, bool dO_lp, void* dQ, void* dK, void* dV,
                                         float scale, int heads, int d, f3s_dtype dtype, cudaStream_t stream);
 f3s_status launch_attention_backward(Plan& p, const void* Q, const void* K, const void* V, const float* dO, float* dQ,
                                      float* dK, float* dV, float scale, int heads, int d, f3s_dtype dtype,

@@ -337,7 +337,8 @@ def attention_fwd(p: Plan, Q, K, V, O=None, ml=None, *, scale: float = 1.0, stre
 
 def attention_backward_saved(p: Plan, Q, K, V, O, ml, dO, *, scale: float, stream=None):
     """f3s_attention_backward_saved(_lp): (dQ, dK, dV) from the saved outputs (O, ml) of
-    attention_fwd; dO float32, or in Q's dtype (the _lp entry point: read in place)."""
+    attention_fwd; dO float32 (gradients float32), or in Q's dtype (the _lp entry point: dO read in
+    place, gradients in Q's dtype)."""
     import torch
     lp = dO.dtype == Q.dtype
     if not lp and dO.dtype != torch.float32:
@@ -348,9 +349,10 @@ def attention_backward_saved(p: Plan, Q, K, V, O, ml, dO, *, scale: float, strea
     if ml.dtype != torch.float32 or tuple(ml.shape) != (Q.shape[0], H, 2) or not ml.is_contiguous() \
             or ml.device != Q.device:
         raise ValueError("attention_backward_saved: ml must be attention_fwd's float32 [N, H, 2] statistics")
-    dQ = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
-    dK = torch.empty(K.shape, dtype=torch.float32, device=K.device)
-    dV = torch.empty(V.shape, dtype=torch.float32, device=V.device)
+    gdt = Q.dtype if lp else torch.float32  # _lp: gradients in the input dtype too
+    dQ = torch.empty(Q.shape, dtype=gdt, device=Q.device)
+    dK = torch.empty(K.shape, dtype=gdt, device=K.device)
+    dV = torch.empty(V.shape, dtype=gdt, device=V.device)
     fn = _lib.f3s_attention_backward_saved_lp if lp else _lib.f3s_attention_backward_saved
     _check(fn(p.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), O.data_ptr(), ml.data_ptr(), dO.data_ptr(),
               dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(), float(scale), H, d, _dtype_code(Q), _stream(stream)),

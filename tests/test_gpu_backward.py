@@ -196,11 +196,13 @@ def test_training_forward_and_saved_backward(f3s, oracle_mod, dtype, graph, d, H
         assert np.array_equal(a, b)
         _close(a, r)
         _close(a, c.astype(np.float64))
-    # dO handed over in the input dtype (f3s_attention_backward_saved_lp): against the oracle
-    # backward of the same rounded dO
+    # dO handed over and gradients returned in the input dtype (f3s_attention_backward_saved_lp):
+    # against the oracle backward of the same rounded dO (one more rounding of each gradient, RNE)
     tdt = torch.float16 if dtype == "fp16" else torch.bfloat16
     dO_lp = dO.to(tdt)
-    lp = [x.cpu().numpy() for x in f3s.attention_backward_saved(p, Q, K, V, O, ml, dO_lp, scale=scale)]
+    lp = f3s.attention_backward_saved(p, Q, K, V, O, ml, dO_lp, scale=scale)
+    assert all(x.dtype == tdt for x in lp)  # gradients in the input dtype too
+    lp = [x.float().cpu().numpy() for x in lp]
     G_lp = dO_lp.double().cpu().numpy()
     ref_lp = oracle_mod.attention_backward(csr.row_ptr, csr.col_idx, qd, kd, decode(Vb, dtype), G_lp, scale=scale)
     for a, r in zip(lp, ref_lp):
