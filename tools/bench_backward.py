@@ -1,12 +1,16 @@
 """Time f3s_attention_backward on a bench workload and print one JSON line.
 
-  python tools/bench_backward.py [--config arxiv] [--steps 20 --warmup 5] [--variant tc|simt]
+  python tools/bench_backward.py [--config arxiv] [--steps 20 --warmup 5] [--variant tc|simt|saved|saved_lp]
 
 useful FLOPs per call: 8 * nnz * d * H (dP = dO V^T, dQ, dK, dV; the recomputed scores are not
-counted).  Algorithmic bytes per call (HBM bound, no reuse across rows or columns):
-  row pass     nnz*H*d*(2+2)   K and V rows per edge (fp16/bf16)      + N*H*d*(2+4+4)  Q, dO in, dQ out
-  column pass  nnz*H*d*(2+4)   Q and dO rows per edge                 + Nc*H*d*(2+2+4+4) K, V in, dK, dV out
-  + 8*N*H (LSE, D written) + 8*nnz*H (read back per edge).
+counted).  Algorithmic HBM bytes per call (no reuse across rows or columns; e = H*d elements per row):
+  prep         saved: O fp32 + dO fp32 read, dO16 written      N*e*(4+4+2)   + 8*N*H (LSE, D)
+               saved_lp: O fp32 + dO (input dtype) read        N*e*(4+2)     + 8*N*H
+  row pass     K and V rows per edge; Q, dO per row; dQ out    nnz*e*(2+2) + N*e*(2+2) + N*e*g
+  column pass  Q and dO rows per edge (+ LSE, D); K, V per key row; dK, dV out
+                                                               nnz*e*(2+2) + 8*nnz*H + Nc*e*(2+2) + 2*Nc*e*g
+  with g = 4 (fp32 gradients) or 2 (saved_lp: gradients in the input dtype); tc (recomputing) adds the
+  forward in partial mode: nnz*e*(2+2) + N*e*(2+4) + 8*N*H.
 """
 import argparse
 import json
@@ -70,8 +74,13 @@ def main():
     info = p.info()
     nnz, N, Nc = info["nnz"], csr.n_rows, csr.n_cols
     flops = 8.0 * nnz * d * H
-    alg = (nnz * H * d * (2 + 2) + N * H * d * (2 + 4 + 4) + nnz * H * d * (2 + 4) + Nc * H * d * (2 + 2 + 4 + 4)
-           + 8 * N * H + 8 * nnz * H)
+    e = H * d
+    g = 2 if a.variant == "saved_lp" else 4
+    prep = N * e * ((4 + 2) if a.variant == "saved_lp" else (4 + 4 + 2)) + 8 * N * H
+    rows = nnz * e * 4 + N * e * 4 + N * e * g
+    cols = nnz * e * 4 + 8 * nnz * H + Nc * e * 4 + 2 * Nc * e * g
+    fwd = nnz * e * 4 + N * e * 6 + 8 * N * H if a.variant == "tc" else 0
+    alg = prep + rows + cols + fwd
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     gbs = alg / (ms * 1e-3) / 1e9
