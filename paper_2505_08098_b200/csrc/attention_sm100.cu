@@ -123,7 +123,10 @@ struct Cfg {
     // correction warpgroups: head-group items are single chunks with no running state, so two
     // groups take alternate chunks; one-head items merge chunks in order in one group
     static constexpr int kCorrWGs = HG == 4 ? 2 : 1;
-    static constexpr int kThreads = 32 * (kCorr0 + 4 * kCorrWGs);
+    // head groups (one chunk per item): a Q warp loads the per-item Q tiles, so that waiting for a free
+    // Q slot never holds the index warp back (one-head plans: the index warp loads them itself)
+    static constexpr int kQWarp = HG > 1 ? kCorr0 + 4 * kCorrWGs : -1;
+    static constexpr int kThreads = 32 * (kCorr0 + 4 * kCorrWGs + (HG > 1 ? 1 : 0));
     static constexpr int kBatch = 8;                 // items fetched per queue round trip
     static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 };
@@ -346,7 +349,7 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 const int nch = w > 0 ? (w + chunk_rows - 1) / chunk_rows : 1;
                 const int qs = qseq % C::kNQ;
                 const int qph = (qseq / C::kNQ) & 1;
-                if (lane == 0) {  // Alg.1 l.5: Q_i of the item (the slot's previous item has left MMA1)
+                if (HG == 1 && lane == 0) {  // Alg.1 l.5: Q_i of the item (the slot's previous item has left MMA1)
                     mbar_wait(bar(B::qempty(qs)), qph ^ 1);
                     mbar_arrive_expect_tx(bar(B::qfull(qs)), C::kQBytes);
 #pragma unroll
@@ -395,6 +398,29 @@ k_f3s_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
                 mbar_arrive(bar(B::idxfull(s)));
             }
             prof_flush(0);
+        }
+        __syncwarp();
+    } else if (HG > 1 && warp == C::kQWarp) {
+        // ===== Q warp (head groups): Alg.1 l.5, the item's Q tiles by TMA once its Q slot's previous
+        // item has left MMA1; walks the chunk slots in order and loads at each item's first chunk
+        if (lane == 0) {
+            for (int32_t seq = 0;; ++seq) {
+                const int s = seq % C::kNS;
+                mbar_wait(bar(B::idxfull(s)), (seq / C::kNS) & 1);
+                const Slot& sl = slots[s];
+                const int rows = sl.rows, flags = sl.flags;
+                if (rows < 0) break;
+                if (!(flags & 1)) continue;
+                const int qs = sl.qslot, qph = (flags >> 2) & 1, k = sl.rw, h = sl.head;
+                mbar_wait(bar(B::qempty(qs)), qph ^ 1);
+                mbar_arrive_expect_tx(bar(B::qfull(qs)), C::kQBytes);
+#pragma unroll
+                for (int g = 0; g < HG; ++g)
+#pragma unroll
+                    for (int pp = 0; pp < C::P; ++pp)
+                        tma_load_2d(sb + C::oQ + qs * C::kQBytes + g * 16 * C::kRowPitch + pp * 2048, &tmQ,
+                                    bar(B::qfull(qs)), (h + g) * D + (128 / EB) * pp, 16 * k);
+            }
         }
         __syncwarp();
     } else if (warp >= C::kLoader0 && warp < C::kLoader0 + C::kLoaderWarps) {
